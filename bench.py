@@ -1,0 +1,397 @@
+"""Benchmark of the owner-subset sync (engine.aggregate, engine.py:60-79) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload resnet18|gpt2|sweep:<MiB>] [--p P]
+
+A step = one owner-subset sync of the BASELINE configs[1] workload: ResNet-18
+(CIFAR shape, d = 11,173,962), block dropping, N = 8 logical workers, P = 4,
+seed 1.  At --gpus 1 the 8 worker replicas are co-resident in one HBM (the
+reference's own in-process structure) and one k_owner_sync launch reads every
+element from its owners, sums in ascending owner order in fp32, divides by the
+owner count and writes the mean back into every owner's fp32 replica and bf16
+training copy.  At --gpus G > 1 (torchrun) the 8 workers are placed
+contiguously on the G GPUs and the same kernel reads/writes peer replicas over
+NVLink (paper_2507_09029_b200/comm.py).
+
+metric "subnet-sync GB/s": replica gradient bytes synchronised per second,
+sum over elements j of |O_j| * 4 B (fp32-equivalent) / time -- the same count
+for every arm, every N and the CPU reference.
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "subnet-sync GB/s (owner-subset replica bytes synchronised per second)"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet18")
+    ap.add_argument("--n-logical", type=int, default=8)
+    ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--strategy", default="block")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def workload(name: str):
+    from paper_2507_09029_b200 import zoo
+    if name == "resnet18":
+        return zoo.resnet18_cifar_topology(), "resnet18-cifar (configs[1], C2)"
+    if name == "gpt2":
+        return zoo.gpt2_small_topology(), "gpt2-small 124M (configs[3], C4)"
+    if name.startswith("sweep:"):
+        mib = int(name.split(":")[1])
+        return zoo.sweep_topology(mib * (1 << 20) // 4), f"sweep {mib} MiB fp32 (configs[4], C5)"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def traffic_for(tag: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(tag)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.06)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the reference algorithm (engine.py:71-74) ported to numpy
+# f64 (oracle/oracle.py, verified bit-exact against the reference), split
+# over host threads by contiguous element ranges.
+# ---------------------------------------------------------------------------
+
+def cpu_aggregate_threads(grads, masks, divisor, lo, hi, threads):
+    chunks = np.linspace(lo, hi, threads + 1).astype(np.int64)
+    out = np.empty(hi - lo, dtype=np.float64)
+
+    def run(k):
+        a, b = chunks[k], chunks[k + 1]
+        from oracle.oracle import aggregate_f64
+        out[a - lo:b - lo] = aggregate_f64([g[a:b] for g in grads], masks[:, a:b], divisor[a:b])
+
+    if threads == 1:
+        run(0)
+    else:
+        with concurrent.futures.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, range(threads)))
+    return out
+
+
+def host_workload(topo, strategy, n, p, seed=1):
+    from oracle import oracle as O
+    a = O.build_assignment(topo, strategy, n, p, seed)
+    rng = np.random.default_rng(1000)
+    grads = [(rng.standard_normal(topo.total, dtype=np.float32) * a.param_masks[w]).astype(np.float64)
+             for w in range(n)]
+    owned = int(a.coverage.sum())
+    return a, grads, owned
+
+
+def time_cpu(grads, masks, divisor, owned_per_elem, threads, budget_s, max_reps=1000):
+    """Bounded sample: whole-vector calls until the budget is spent (>= 1 call);
+    if one call exceeds the budget, a contiguous prefix sized to fit."""
+    d = masks.shape[1]
+    t0 = time.perf_counter()
+    cpu_aggregate_threads(grads, masks, divisor, 0, min(d, 1 << 20), threads)
+    est = (time.perf_counter() - t0) * d / min(d, 1 << 20)
+    hi = d if est <= budget_s else max(1 << 16, int(d * budget_s / est))
+    reps = max(1, min(max_reps, int(budget_s / max(est * hi / d, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        cpu_aggregate_threads(grads, masks, divisor, 0, hi, threads)
+    dt = (time.perf_counter() - t0) / reps
+    nbytes = float(owned_per_elem[:hi].sum()) * 4
+    return nbytes / dt / 1e9, dt, hi, reps
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    topo, tag = workload(args.workload)
+    a, grads, owned = host_workload(topo, args.strategy, args.n_logical, args.p)
+    threads = os.cpu_count() or 1
+    per_elem = a.coverage
+    # size each step so warmup + steps end within ~2 minutes
+    budget_total = 120.0
+    d = topo.total
+    t0 = time.perf_counter()
+    cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, min(d, 1 << 20), threads)
+    est_full = (time.perf_counter() - t0) * d / min(d, 1 << 20)
+    per_step = budget_total / max(1, args.steps + args.warmup)
+    hi = d if est_full <= per_step else max(1 << 16, int(d * per_step / est_full))
+    for _ in range(args.warmup):
+        cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, hi, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, hi, threads)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    nbytes = float(per_elem[:hi].sum()) * 4
+    value = nbytes / dt / 1e9
+    sample = (f"{'whole vector' if hi == d else f'first {hi} of {d} elements'} per step; "
+              f"numpy f64 port of engine.aggregate (oracle/oracle.py:aggregate_f64), "
+              f"{threads} threads over contiguous element ranges")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": tag, "d": d, "n_logical": args.n_logical, "p": args.p,
+                   "strategy": args.strategy, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_09029_b200 import _native, engine, masking
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _native.load()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    topo, tag = workload(args.workload)
+    n, p, d = args.n_logical, args.p, topo.total
+    a = masking.build_assignment(topo, args.strategy, n, p, seed=1)
+
+    if world > 1:
+        from paper_2507_09029_b200 import comm
+        step, plan_bytes, hbm_bytes, meta = comm.bench_setup(a, rank, world, dev)
+        parallelism = f"{n} logical workers on {world} GPUs, NVLink P2P owner sync"
+    else:
+        pm = a.param_masks
+        gen = torch.Generator(device=dev)
+        reps, shadows = [], []
+        for w in range(n):
+            gen.manual_seed(1000 + w)
+            reps.append(torch.randn(d, generator=gen, device=dev) * pm[w])
+            shadows.append(torch.zeros(d, dtype=torch.bfloat16, device=dev))
+        plan = a.sync_plan()
+        prep = engine.PreparedSync(reps, a, writeback=True, shadows_bf16=shadows, plan=plan)
+        step = prep.launch
+        plan_bytes = plan.owned_elems * 4
+        hbm_bytes = plan.owned_elems * (4 + 4 + 2)   # read fp32, write fp32 + bf16 per owner
+        meta = {"tiles": plan.n_tiles, "uniform_tiles": plan.n_uniform, "grid": plan.grid,
+                "tiles_per_cta": plan.tiles_per_cta}
+        parallelism = f"{n} logical workers co-resident on 1 GPU"
+        del pm
+
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            flush.zero_()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])  # ms
+    ms = float(times.mean())
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tot = torch.tensor([float(plan_bytes)], device=dev)
+        dist.all_reduce(tot)
+        total_bytes = float(tot.item())
+    else:
+        total_bytes = float(plan_bytes)
+    value = total_bytes / (ms / 1e3) / 1e9
+
+    peaks = measured_peaks()
+    peak = float(peaks["hbm_gbs"])
+    achieved = hbm_bytes / (float(times.mean()) / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic_for(f"{args.workload}:{world}"),
+                "kernel": "k_owner_sync",
+                "algorithmic_bytes_per_launch": hbm_bytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+                if not peaks.get("_fallback") else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    if world > 1:
+        roofline.update(meta.get("roofline", {}))
+
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1:
+        e2e = run_e2e(args, a, dev, total_bytes)
+        if not args.no_cpu_baseline:
+            cpu = run_cpu_baseline(args, topo)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 (bf16 copy fused)", "data": "synthetic",
+            "config": {"workload": tag, "d": d, "n_logical": n, "p": p, "strategy": args.strategy,
+                       "seed": 1, "parallelism": parallelism,
+                       "l2": "flushed between steps (256 MB write)", **meta},
+            "gpu_launches": args.steps,
+            "roofline": roofline,
+            "clocks": clocks.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, a, dev, total_bytes):
+    """The reference-facing call with HOST buffers: engine.aggregate(list of N
+    numpy arrays backed by pinned memory, assignment) -> numpy gbar.  H2D of all
+    N gradients, the sync kernel, and the D2H of the mean are inside the timing."""
+    import torch
+
+    from paper_2507_09029_b200 import engine
+    n, d = a.n_workers, a.topology.total
+    pm = a.param_masks
+    gen = torch.Generator(device=dev)
+    host = []
+    for w in range(n):
+        gen.manual_seed(1000 + w)
+        t = torch.empty(d, dtype=torch.float32, pin_memory=True)
+        t.copy_(torch.randn(d, generator=gen, device=dev) * pm[w])
+        host.append(t.numpy())
+    del pm
+    for _ in range(3):
+        engine.aggregate(host, a)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        out = engine.aggregate(host, a)
+        ts.append(time.perf_counter() - t0)
+    assert out.gbar.shape == (d,)
+    dt = float(np.mean(ts))
+    return {"value": total_bytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": n * d * 4,
+            "d2h_bytes_per_step": d * 4, "ms_per_step": dt * 1e3,
+            "api": "paper_2507_09029_b200.engine.aggregate(list[np.ndarray pinned], assignment)",
+            "timing": "host wall clock around the blocking call (returns numpy)"}
+
+
+def run_cpu_baseline(args, topo):
+    from oracle import oracle as O  # noqa: F401  (checker/baseline only)
+    a, grads, owned = host_workload(topo, args.strategy, args.n_logical, args.p)
+    value, dt, hi, reps = time_cpu(grads, a.param_masks, a.divisor, a.coverage, 1, budget_s=10.0)
+    d = topo.total
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{reps} calls over {'the whole vector' if hi == d else f'{hi} of {d} elements'}"
+                      f", numpy f64 port of engine.aggregate on 1 thread (host has {os.cpu_count()} cores)",
+            "ms_per_call": dt * 1e3}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

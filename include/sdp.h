@@ -1,0 +1,286 @@
+/*
+ * sdp.h — C ABI of libsdp.so, the B200 (sm_100a) hot path of Subnetwork Data
+ * Parallelism (arXiv 2507.09029).
+ *
+ * The reference (`/root/reference/pkg/src/subnetdp`) has no FFI: its boundary
+ * is a set of Python functions over numpy arrays.  These entry points are what
+ * those functions bind to in this framework (see INTEGRATION.md for the ctypes
+ * stub a maintainer adds, and paper_2507_09029_b200/_native.py for ours).
+ *
+ *   reference function (file:line)                     replaced by
+ *   -------------------------------------------------  -----------------------------
+ *   masking.assign_units / assign_grouped_units        sdp_assign_units
+ *     (masking.py:69-117) + slot_windows (:56-66)
+ *   induce_channel_param_mask / induce_block_param_    sdp_build_masks
+ *     mask (:120-170), _governor_counts (:288-302),
+ *     MaskAssignment.__post_init__ coverage/divisor
+ *     (:203-205), validate's active counts (:442)
+ *   MaskAssignment.worker_view param_mask (:238-243)   sdp_worker_mask
+ *   engine.aggregate (engine.py:60-79)                 sdp_plan_tiles + sdp_owner_sync
+ *   models.masked_forward  theta * mask (models.py:355) sdp_masked_extract
+ *   width-wise slice extraction (models.py:355-362)    sdp_gather_slices
+ *   models.flat_gradient write-back (models.py:369-382) sdp_scatter_slices
+ *   optim.SgdNesterov.update (optim.py:78-84)          sdp_nesterov_update / fused in
+ *                                                      sdp_owner_sync (SDP_SYNC_NESTEROV)
+ *
+ * Conventions
+ *   - Every function returns an int status: SDP_OK (0) or one of the SDP_ERR_*
+ *     codes below, which the Python layer maps 1:1 onto the reference's
+ *     exception classes (errors.py:8-45).  sdp_last_error() returns the message
+ *     of the last failure on the calling thread.
+ *   - All array pointers are DEVICE pointers owned by the caller unless marked
+ *     "host".  libsdp never allocates device memory.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it.  Calls do not synchronise the device, except where noted.
+ *   - No torch types appear here; the library links only the CUDA runtime.
+ */
+#ifndef SDP_H_
+#define SDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDP_ABI_VERSION 1
+
+/* status codes (errors.py:8-45) */
+#define SDP_OK 0
+#define SDP_ERR_CONFIG 1      /* ConfigError      */
+#define SDP_ERR_TOPOLOGY 2    /* TopologyError    */
+#define SDP_ERR_VALIDATION 3  /* ValidationError  */
+#define SDP_ERR_PROTOCOL 4    /* ProtocolError    */
+#define SDP_ERR_NUMERICAL 5   /* NumericalError   */
+#define SDP_ERR_USAGE 6       /* UsageError       */
+#define SDP_ERR_CUDA 7        /* CUDA runtime failure (no reference analogue) */
+
+#define SDP_MAX_WORKERS 64
+
+int sdp_abi_version(void);
+const char* sdp_last_error(void);
+/* Number of SMs of the current device (grid sizing helper). */
+int sdp_device_sm_count(int* out);
+
+/* ------------------------------------------------------------------------ */
+/* Mask builder                                                              */
+/* ------------------------------------------------------------------------ */
+
+/* One assignment group: units [first_unit, first_unit + size) drawn with one
+ * permutation (masking.py:110-116).  Block strategy = a single group. */
+typedef struct {
+  int32_t first_unit;
+  int32_t size;
+} sdp_group_desc;
+
+/* One parameter tensor of the flat vector (topology.py:16-23). */
+typedef struct {
+  int64_t offset;      /* flat offset of element 0 */
+  int64_t size;        /* elements */
+  int32_t rule_begin;  /* rules [rule_begin, rule_begin + rule_count) govern it */
+  int32_t rule_count;
+} sdp_param_desc;
+
+/* Element e (0-based within its parameter) is governed by unit
+ *   unit_base + (e / inner) % dim
+ * -- an own/consumer slice along one axis (masking.py:140-149; inner is the
+ * product of the trailing dims, dim the axis length) or, with inner = dim = 1,
+ * a whole block (masking.py:167-169). */
+typedef struct {
+  int64_t inner;
+  int64_t dim;
+  int32_t unit_base;
+  int32_t pad_;
+} sdp_rule_desc;
+
+/* Seeded cyclic assignment (masking.py:56-117) on the device, bit-exact with
+ * numpy's default_rng(seed).permutation (SeedSequence + PCG64).
+ *   seed_words (host): the non-negative seed as little-endian uint32 words.
+ *   groups (device):   n_groups descriptors, drawn in order from ONE generator.
+ *   unit_bits (device, out): uint64 owner mask per unit; units outside every
+ *                      group get all N bits (they are never masked).
+ *   scratch (device):  >= max group size int32 (used only when a group does not
+ *                      fit in shared memory; may be NULL otherwise).
+ * Errors: SDP_ERR_CONFIG unless 1 <= P <= N <= 64 and groups are non-empty. */
+int sdp_assign_units(const uint32_t* seed_words, int n_seed_words,
+                     const sdp_group_desc* groups, int n_groups, int max_group,
+                     int n_units, int n_workers, int replication,
+                     uint64_t* unit_bits, int32_t* scratch, void* stream);
+
+/* Same permutation as a standalone primitive: out[k] = default_rng(seed)
+ * .permutation(n)[k] after `skip` earlier permutations of sizes skip_sizes
+ * (host) were drawn from the same generator.  Used by tests. */
+int sdp_permutation(const uint32_t* seed_words, int n_seed_words,
+                    const int32_t* skip_sizes, int n_skip, int n,
+                    int32_t* out, void* stream);
+
+/* Expand unit ownership to every element of the flat vector.
+ * Outputs (all device, each may be NULL):
+ *   owner_mask   [d] elements of mask_bytes (1,2,4,8) bytes: bit w = worker w
+ *   param_masks  [N, d] bool (reference layout, masking.py:131,160)
+ *   coverage     [d] int64     (masking.py:204)
+ *   divisor      [d] float64   max(coverage, 1) (masking.py:205)
+ *   governors    [d] int64     number of governing rules (masking.py:288-302)
+ *   active_counts [N] int64    params held per worker (masking.py:442); must be
+ *                              zeroed by the caller, accumulated atomically. */
+int sdp_build_masks(const sdp_param_desc* params, int n_params,
+                    const sdp_rule_desc* rules, int n_rules,
+                    const uint64_t* unit_bits, int n_workers, int64_t total,
+                    void* owner_mask, int mask_bytes, uint8_t* param_masks,
+                    int64_t* coverage, double* divisor, int64_t* governors,
+                    int64_t* active_counts, void* stream);
+
+/* Per-worker mask view (masking.py:238-243): for worker w,
+ *   mask_f64[j] = bit w of owner_mask[j] ? 1.0 : 0.0   (nullable)
+ *   mask_u8[j]  = bit w ? 1 : 0                         (nullable) */
+int sdp_worker_mask(const void* owner_mask, int mask_bytes, int64_t total,
+                    int worker, double* mask_f64, uint8_t* mask_u8, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Owner-subset sync (engine.aggregate, engine.py:60-79)                     */
+/* ------------------------------------------------------------------------ */
+
+/* A tile is `tile` consecutive elements starting at tile_index * tile.
+ * uniform tiles carry their owner set; mixed tiles read owner_mask. */
+typedef struct {
+  uint64_t owner_bits; /* uniform: the owner set; mixed: union of owner sets */
+  uint32_t tile_index;
+  uint32_t len_flags;  /* bits 0..23: length in elements; bit 31: uniform */
+} sdp_tile_desc;
+
+#define SDP_TILE_UNIFORM 0x80000000u
+#define SDP_TILE_LEN_MASK 0x00FFFFFFu
+
+/* Classify every tile of the flat vector (warp-shuffle AND/OR reduction).
+ * tiles (device, out): ceil(total / tile) descriptors in tile order.
+ * tile must be a multiple of 1024 and <= 1<<20. */
+int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
+                   int tile, sdp_tile_desc* tiles, void* stream);
+
+#define SDP_DTYPE_F32 0
+#define SDP_DTYPE_F64 1
+
+/* flags */
+#define SDP_SYNC_WRITEBACK 0x1       /* write the mean into every owner's replica */
+#define SDP_SYNC_CHECK_UNCOVERED 0x2 /* engine.py:75-78 leak check -> status */
+#define SDP_SYNC_CHECK_FINITE 0x4    /* optim.py:79-80 isfinite(gbar) -> status */
+#define SDP_SYNC_NESTEROV 0x8        /* fused optim.py:81-84 update on theta/vel */
+
+/* status word bits written (atomicOr) by the kernel */
+#define SDP_STATUS_UNCOVERED_LEAK 0x1
+#define SDP_STATUS_NONFINITE 0x2
+#define SDP_STATUS_BARRIER_TIMEOUT 0x4
+
+typedef struct {
+  int32_t dtype;        /* SDP_DTYPE_F32 / SDP_DTYPE_F64: replicas, out, theta */
+  int32_t n_workers;    /* N <= 64 */
+  int32_t mask_bytes;   /* element size of owner_mask */
+  int32_t tile;         /* elements per tile (the plan's tile) */
+  int64_t total;        /* d */
+  const void* owner_mask;          /* [d]; needed when any tile is mixed */
+  const sdp_tile_desc* tiles;      /* CTA-major: CTA b runs tiles[b*tiles_per_cta ..] */
+  int32_t n_tiles;
+  int32_t tiles_per_cta;
+  int32_t grid;                    /* CTAs; 0 = ceil(n_tiles / tiles_per_cta) */
+  int32_t flags;
+  void* replicas[SDP_MAX_WORKERS];     /* worker gradient buffers [d] (local or peer) */
+  void* shadow_bf16[SDP_MAX_WORKERS];  /* per-worker bf16 copy of the mean, or NULL */
+  void* out;            /* [d] mean (dtype), or NULL */
+  void* out_bf16;       /* [d] bf16 mean, or NULL */
+  /* fused Nesterov (SDP_SYNC_NESTEROV): theta/velocity [d] dtype, bf16 weights */
+  void* theta;
+  void* velocity;
+  void* theta_bf16;
+  double lr;
+  double momentum;
+  uint32_t* status;     /* device word, OR-ed with SDP_STATUS_* (may be NULL) */
+  /* cross-GPU barrier (multi-process); world == 1 disables it */
+  int32_t rank;
+  int32_t world;
+  uint32_t* signal_pads[8];  /* per-rank pad (peer-mapped), >= grid*8 words */
+  uint32_t epoch;            /* increments every launch */
+  uint32_t pad_;
+  int64_t timeout_cycles;    /* spin limit per barrier */
+} sdp_sync_args;
+
+/* Launch the owner-subset sync.  For every element j with owner set O_j:
+ *   acc = +0; for w in O_j ascending: acc += replicas[w][j];
+ *   mean = acc / max(|O_j|, 1)            (IEEE division, no reciprocal)
+ * then writes mean to out/out_bf16 and, with SDP_SYNC_WRITEBACK, to every
+ * owner's replica and bf16 shadow.  Non-owner replica entries are never read
+ * (except with CHECK_UNCOVERED at zero-coverage elements). */
+int sdp_owner_sync(const sdp_sync_args* args /* host */, void* stream);
+
+/* Fused-optimizer standalone (optim.py:78-84): v = mu v + g; th -= lr (g + mu v). */
+int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity,
+                        const void* grad, double lr, double momentum,
+                        void* theta_bf16, uint32_t* status, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Extraction / write-back (models.py:333-382)                               */
+/* ------------------------------------------------------------------------ */
+
+/* out[j] = theta[j] * (bit w of owner_mask[j])  — models.py:355, bit-exact
+ * (keeps -0.0 and NaN propagation of the multiply). */
+int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask,
+                       int mask_bytes, int64_t total, int worker, void* out,
+                       void* stream);
+
+/* One compact sub-tensor of a width-wise subnetwork. Up to 4 dims; each dim
+ * either keeps all indices (map_offset = -1) or the listed ones:
+ *   fwd_maps[map_offset + c] = full index of compact index c   (gather)
+ *   inv_maps[map_offset + f] = compact index of full index f, or -1 (scatter) */
+typedef struct {
+  int64_t full_offset;
+  int64_t compact_offset;
+  int64_t full_shape[4];
+  int64_t compact_shape[4];
+  int32_t map_offset[4];
+  int32_t ndim;
+  int32_t pad_;
+} sdp_slice_desc;
+
+/* compact[k] = full[src(k)] for every element of every descriptor. */
+int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, int n_descs,
+                      const int32_t* fwd_maps, const void* full, void* compact,
+                      int64_t compact_total, void* stream);
+
+#define SDP_SCATTER_ZERO_FILL 0x1  /* full[j] = 0 where no compact element maps */
+#define SDP_SCATTER_ACCUMULATE 0x2 /* full[j] += compact[...] instead of = */
+
+/* Write compact grads back into the flat layout (models.py:376-381).
+ * Iterates over the FULL elements in [full_lo, full_hi) (coalesced stores);
+ * descriptors must be sorted by full_offset and disjoint; elements outside
+ * every descriptor are left untouched. */
+int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, int n_descs,
+                       const int32_t* inv_maps, const void* compact, void* full,
+                       int64_t full_lo, int64_t full_hi, int flags, void* stream);
+
+/* out[j] = acc[j] / divisor[j] in dtype (the engine.py:74 divide after an
+ * owner-ordered scatter-accumulate).  divisor is float64 [d]. */
+int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
+               void* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Cross-process peer mapping (multi-GPU owner sync)                         */
+/* ------------------------------------------------------------------------ */
+
+#define SDP_IPC_HANDLE_BYTES 64
+
+/* Export `ptr` (inside any cudaMalloc allocation): handle + byte offset of
+ * ptr from the allocation base. */
+int sdp_ipc_export(const void* ptr, uint8_t* handle_out /* host, 64 B */,
+                   uint64_t* offset_out /* host */);
+/* Map a peer's export into this process; *ptr_out = base + offset. */
+int sdp_ipc_import(const uint8_t* handle /* host */, uint64_t offset,
+                   void** ptr_out /* host */);
+int sdp_ipc_close(void* ptr);
+/* Enable direct peer access from the current device to `peer` (idempotent). */
+int sdp_enable_peer(int peer);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDP_H_ */

@@ -1,0 +1,486 @@
+// Block-assignment and mask builder (masking.py:56-359) on the device.
+//
+//   k_assign       one warp: SeedSequence -> PCG64 -> per-group Fisher-Yates,
+//                  cyclic windows (masking.py:56-117).  Sequential by nature
+//                  (O(units)); bit-exact with numpy default_rng.
+//   k_build_masks  HBM-bound expansion: every element ANDs the owner sets of
+//                  the units that govern it (masking.py:131-149, 160-169) and
+//                  emits owner mask / [N,d] bool / coverage / divisor /
+//                  governors / per-worker counts.
+//   k_plan_tiles   warp-per-tile AND/OR shuffle reduction: which tiles have one
+//                  owner set (block strategy: nearly all) for the sync kernel.
+#include "sdp_common.cuh"
+
+namespace sdp {
+
+// ---------------------------------------------------------------------------
+// numpy SeedSequence + PCG64 restated (oracle/oracle.py)
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+
+struct Pcg64 {
+  u128 state, inc;
+  uint32_t half;
+  bool has_half;
+
+  __device__ void step() {
+    const u128 mult = (static_cast<u128>(0x2360ED051FC65DA4ull) << 64) | 0x4385DF649FCCF645ull;
+    state = state * mult + inc;
+  }
+  __device__ uint64_t raw() {
+    step();
+    uint64_t hi = static_cast<uint64_t>(state >> 64);
+    uint64_t lo = static_cast<uint64_t>(state);
+    uint32_t rot = static_cast<uint32_t>(hi >> 58);
+    uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ uint32_t next32() {
+    if (has_half) {
+      has_half = false;
+      return half;
+    }
+    uint64_t x = raw();
+    half = static_cast<uint32_t>(x >> 32);
+    has_half = true;
+    return static_cast<uint32_t>(x);
+  }
+  // numpy random_interval: masked rejection, 32-bit draws when max fits.
+  __device__ uint64_t interval(uint64_t mx) {
+    if (mx == 0) return 0;
+    uint64_t mask = mx;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4;
+    mask |= mask >> 8; mask |= mask >> 16; mask |= mask >> 32;
+    if (mx <= 0xFFFFFFFFull) {
+      uint32_t m32 = static_cast<uint32_t>(mask), v;
+      while ((v = (next32() & m32)) > mx) {}
+      return v;
+    }
+    uint64_t v;
+    while ((v = (raw() & mask)) > mx) {}
+    return v;
+  }
+};
+
+__device__ void seed_pcg(Pcg64& g, const uint32_t* ent, int n_ent) {
+  const uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u;
+  const uint32_t INIT_B = 0x8b51f9ddu, MULT_B = 0x58f38dedu;
+  const uint32_t MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
+  uint32_t hc = INIT_A;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= MULT_A;
+    v *= hc;
+    return v ^ (v >> 16);
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    uint32_t r = MIX_L * x - MIX_R * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t pool[4];
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < n_ent ? ent[i] : 0u);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+  for (int k = 4; k < n_ent; ++k)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[k]));
+  uint32_t hb = INIT_B, w[8];
+  for (int i = 0; i < 8; ++i) {
+    uint32_t d = pool[i & 3] ^ hb;
+    hb *= MULT_B;
+    d *= hb;
+    w[i] = d ^ (d >> 16);
+  }
+  uint64_t v0 = w[0] | (static_cast<uint64_t>(w[1]) << 32);
+  uint64_t v1 = w[2] | (static_cast<uint64_t>(w[3]) << 32);
+  uint64_t v2 = w[4] | (static_cast<uint64_t>(w[5]) << 32);
+  uint64_t v3 = w[6] | (static_cast<uint64_t>(w[7]) << 32);
+  u128 initstate = (static_cast<u128>(v0) << 64) | v1;
+  u128 initseq = (static_cast<u128>(v2) << 64) | v3;
+  g.inc = (initseq << 1) | 1;
+  g.state = 0;
+  g.step();
+  g.state += initstate;
+  g.step();
+  g.has_half = false;
+  g.half = 0;
+}
+
+struct SeedWords {
+  uint32_t w[8];
+  int n;
+};
+
+__device__ __forceinline__ uint64_t window_bits(uint64_t slot, int n, int p) {
+  uint64_t start = (slot * static_cast<uint64_t>(p)) % static_cast<uint64_t>(n);
+  uint64_t bits = 0;
+  for (int t = 0; t < p; ++t) bits |= 1ull << ((start + t) % n);
+  return bits;
+}
+
+__global__ void k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups,
+                         int n_groups, int n_units, int n_workers, int replication,
+                         uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch,
+                         int smem_cap) {
+  extern __shared__ int32_t s_perm[];
+  const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
+  for (int u = threadIdx.x; u < n_units; u += blockDim.x) unit_bits[u] = full;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  Pcg64 g;
+  seed_pcg(g, seed.w, seed.n);
+  uint64_t slot = 0;
+  for (int gi = 0; gi < n_groups; ++gi) {
+    const int first = groups[gi].first_unit, size = groups[gi].size;
+    int32_t* a = size <= smem_cap ? s_perm : scratch;
+    for (int i = 0; i < size; ++i) a[i] = i;
+    for (int i = size - 1; i > 0; --i) {  // Generator.shuffle (Fisher-Yates)
+      int j = static_cast<int>(g.interval(static_cast<uint64_t>(i)));
+      int32_t t = a[i];
+      a[i] = a[j];
+      a[j] = t;
+    }
+    for (int k = 0; k < size; ++k) unit_bits[first + a[k]] = window_bits(slot++, n_workers, replication);
+  }
+}
+
+__global__ void k_permutation(SeedWords seed, const int32_t* skip_sizes_dev, int n_skip, int n,
+                              int32_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Pcg64 g;
+  seed_pcg(g, seed.w, seed.n);
+  for (int s = 0; s < n_skip; ++s)
+    for (int i = skip_sizes_dev[s] - 1; i > 0; --i) (void)g.interval(static_cast<uint64_t>(i));
+  for (int i = 0; i < n; ++i) out[i] = i;
+  for (int i = n - 1; i > 0; --i) {
+    int j = static_cast<int>(g.interval(static_cast<uint64_t>(i)));
+    int32_t t = out[i];
+    out[i] = out[j];
+    out[j] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// element expansion
+// ---------------------------------------------------------------------------
+constexpr int kBuildElems = 16;   // elements per thread (one 16-B bool vector per worker row)
+constexpr int kBuildThreads = 256;
+
+__device__ __forceinline__ int find_param(const sdp_param_desc* __restrict__ p, int n, int64_t j) {
+  int lo = 0, hi = n - 1;  // last param with offset <= j
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p[mid].offset <= j) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int MB>
+__global__ void __launch_bounds__(kBuildThreads)
+k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
+              const sdp_rule_desc* __restrict__ rules, const uint64_t* __restrict__ unit_bits,
+              int n_workers, int64_t total, typename MaskT<MB>::T* __restrict__ owner_mask,
+              uint8_t* __restrict__ param_masks, int64_t* __restrict__ coverage,
+              double* __restrict__ divisor, int64_t* __restrict__ governors,
+              unsigned long long* __restrict__ active_counts) {
+  using M = typename MaskT<MB>::T;
+  const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
+  const int64_t n_chunks = (total + kBuildElems - 1) / kBuildElems;
+  const bool rows_aligned = (total % 16) == 0;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // uniform trip count across the warp so the shuffle reductions stay converged
+    const bool live = c < n_chunks;
+    const int64_t j0 = c * kBuildElems;
+    uint64_t bits[kBuildElems];
+    int gov[kBuildElems];
+#pragma unroll
+    for (int e = 0; e < kBuildElems; ++e) bits[e] = 0;
+    int nvalid = 0;
+    if (live) {
+      nvalid = static_cast<int>(min(static_cast<int64_t>(kBuildElems), total - j0));
+      int pi = find_param(params, n_params, j0);
+      int64_t pend = params[pi].offset + params[pi].size;
+#pragma unroll
+      for (int e = 0; e < kBuildElems; ++e) {
+        const int64_t j = j0 + e;
+        bits[e] = 0;
+        gov[e] = 0;
+        if (e < nvalid) {
+          while (j >= pend) {
+            ++pi;
+            pend = params[pi].offset + params[pi].size;
+          }
+          const sdp_param_desc pd = params[pi];
+          const uint32_t le = static_cast<uint32_t>(j - pd.offset);
+          uint64_t b = full;
+          for (int r = 0; r < pd.rule_count; ++r) {
+            const sdp_rule_desc rd = rules[pd.rule_begin + r];
+            const uint32_t u = static_cast<uint32_t>(rd.unit_base) +
+                               (le / static_cast<uint32_t>(rd.inner)) % static_cast<uint32_t>(rd.dim);
+            b &= __ldg(unit_bits + u);
+          }
+          bits[e] = b;
+          gov[e] = pd.rule_count;
+        }
+      }
+      const bool vec = nvalid == kBuildElems;
+      if (owner_mask) {
+        if (vec) {
+          M m[kBuildElems];
+#pragma unroll
+          for (int e = 0; e < kBuildElems; ++e) m[e] = static_cast<M>(bits[e]);
+          const uint4* src = reinterpret_cast<const uint4*>(m);
+          uint4* dst = reinterpret_cast<uint4*>(owner_mask + j0);
+#pragma unroll
+          for (int q = 0; q < kBuildElems * MB / 16; ++q) dst[q] = src[q];
+        } else {
+          for (int e = 0; e < nvalid; ++e) owner_mask[j0 + e] = static_cast<M>(bits[e]);
+        }
+      }
+      if (param_masks) {
+        for (int w = 0; w < n_workers; ++w) {
+          uint8_t* row = param_masks + static_cast<int64_t>(w) * total + j0;
+          if (vec && rows_aligned) {
+            uint32_t wd[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t v = 0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) v |= static_cast<uint32_t>((bits[q * 4 + b] >> w) & 1ull) << (8 * b);
+              wd[q] = v;
+            }
+            *reinterpret_cast<uint4*>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+          } else {
+            for (int e = 0; e < nvalid; ++e) row[e] = static_cast<uint8_t>((bits[e] >> w) & 1ull);
+          }
+        }
+      }
+      if (coverage || divisor) {
+        for (int e = 0; e < kBuildElems; e += 2) {
+          const int c0 = __popcll(bits[e]), c1 = __popcll(bits[e + 1]);
+          if (vec) {
+            if (coverage) *reinterpret_cast<longlong2*>(coverage + j0 + e) = make_longlong2(c0, c1);
+            if (divisor)
+              *reinterpret_cast<double2*>(divisor + j0 + e) =
+                  make_double2(static_cast<double>(max(c0, 1)), static_cast<double>(max(c1, 1)));
+          } else {
+            if (e < nvalid) {
+              if (coverage) coverage[j0 + e] = c0;
+              if (divisor) divisor[j0 + e] = static_cast<double>(max(c0, 1));
+            }
+            if (e + 1 < nvalid) {
+              if (coverage) coverage[j0 + e + 1] = c1;
+              if (divisor) divisor[j0 + e + 1] = static_cast<double>(max(c1, 1));
+            }
+          }
+        }
+      }
+      if (governors) {
+        for (int e = 0; e < kBuildElems; e += 2) {
+          if (vec) {
+            *reinterpret_cast<longlong2*>(governors + j0 + e) = make_longlong2(gov[e], gov[e + 1]);
+          } else {
+            if (e < nvalid) governors[j0 + e] = gov[e];
+            if (e + 1 < nvalid) governors[j0 + e + 1] = gov[e + 1];
+          }
+        }
+      }
+    }
+    if (active_counts) {
+      // per-worker held-parameter counts: warp-shuffle reduce, one atomic per warp
+      for (int w = 0; w < n_workers; ++w) {
+        unsigned cnt = 0;
+#pragma unroll
+        for (int e = 0; e < kBuildElems; ++e) cnt += static_cast<unsigned>((bits[e] >> w) & 1ull);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(active_counts + w, static_cast<unsigned long long>(cnt));
+      }
+    }
+    // exit once the whole warp is past the end
+    if (!__any_sync(0xffffffffu, c + static_cast<int64_t>(gridDim.x) * blockDim.x < n_chunks)) break;
+  }
+}
+
+template <int MB>
+__global__ void k_worker_mask(const typename MaskT<MB>::T* __restrict__ owner_mask, int64_t total,
+                              int worker, double* __restrict__ mf, uint8_t* __restrict__ mu) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool on = (static_cast<uint64_t>(owner_mask[j]) >> worker) & 1ull;
+    if (mf) mf[j] = on ? 1.0 : 0.0;
+    if (mu) mu[j] = on ? 1 : 0;
+  }
+}
+
+// One warp per tile: uniform iff AND == OR over the tile's owner sets.
+template <int MB>
+__global__ void k_plan_tiles(const typename MaskT<MB>::T* __restrict__ owner_mask, int64_t total,
+                             int tile, int64_t n_tiles, sdp_tile_desc* __restrict__ tiles) {
+  using M = typename MaskT<MB>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = warp; t < n_tiles; t += nwarps) {
+    const int64_t s = t * tile;
+    const int len = static_cast<int>(min(static_cast<int64_t>(tile), total - s));
+    uint64_t a = ~0ull, o = 0;
+    const M* base = owner_mask + s;
+    if (len == tile) {
+      constexpr int per = 16 / MB;  // mask elements per 16-B vector
+      const uint4* v = reinterpret_cast<const uint4*>(base);
+      for (int q = lane; q < tile / per; q += 32) {
+        uint4 x = __ldg(v + q);
+        const M* m = reinterpret_cast<const M*>(&x);
+#pragma unroll
+        for (int e = 0; e < per; ++e) {
+          a &= static_cast<uint64_t>(m[e]);
+          o |= static_cast<uint64_t>(m[e]);
+        }
+      }
+    } else {
+      for (int e = lane; e < len; e += 32) {
+        uint64_t m = static_cast<uint64_t>(base[e]);
+        a &= m;
+        o |= m;
+      }
+    }
+    const uint32_t alo = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(a));
+    const uint32_t ahi = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(a >> 32));
+    const uint32_t olo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o));
+    const uint32_t ohi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(o >> 32));
+    if (lane == 0) {
+      const uint64_t A = (static_cast<uint64_t>(ahi) << 32) | alo;
+      const uint64_t O = (static_cast<uint64_t>(ohi) << 32) | olo;
+      sdp_tile_desc d;
+      d.owner_bits = O;
+      d.tile_index = static_cast<uint32_t>(t);
+      d.len_flags = static_cast<uint32_t>(len) | (A == O ? SDP_TILE_UNIFORM : 0u);
+      tiles[t] = d;
+    }
+  }
+}
+
+static int check_mask_bytes(int mb) {
+  if (mb == 1 || mb == 2 || mb == 4 || mb == 8) return SDP_OK;
+  return set_error(SDP_ERR_CONFIG, "mask_bytes must be 1, 2, 4 or 8 (got %d)", mb);
+}
+
+static SeedWords make_seed(const uint32_t* w, int n) {
+  SeedWords s{};
+  s.n = n;
+  for (int i = 0; i < n && i < 8; ++i) s.w[i] = w[i];
+  return s;
+}
+
+}  // namespace sdp
+
+using namespace sdp;
+
+extern "C" {
+
+int sdp_assign_units(const uint32_t* seed_words, int n_seed_words, const sdp_group_desc* groups,
+                     int n_groups, int max_group, int n_units, int n_workers, int replication,
+                     uint64_t* unit_bits, int32_t* scratch, void* stream) {
+  if (n_workers < 1 || n_workers > SDP_MAX_WORKERS)
+    return set_error(SDP_ERR_CONFIG, "n_workers must lie in [1, %d], got %d", SDP_MAX_WORKERS, n_workers);
+  if (replication < 1 || replication > n_workers)
+    return set_error(SDP_ERR_CONFIG, "replication must satisfy 1 <= P <= N, got P=%d, N=%d",
+                     replication, n_workers);
+  if (n_groups < 1 || max_group < 1) return set_error(SDP_ERR_CONFIG, "assignment requires non-empty groups");
+  if (!seed_words || n_seed_words < 1 || n_seed_words > 8)
+    return set_error(SDP_ERR_CONFIG, "seed must be given as 1..8 uint32 words");
+  if (!unit_bits || !groups) return set_error(SDP_ERR_USAGE, "null device pointer");
+  const int smem_cap = 48 * 1024 / 4;
+  const int smem_elems = max_group <= smem_cap ? max_group : 0;
+  if (max_group > smem_cap && !scratch)
+    return set_error(SDP_ERR_USAGE, "group of %d units needs a scratch buffer", max_group);
+  k_assign<<<1, 256, smem_elems * sizeof(int32_t), as_stream(stream)>>>(
+      make_seed(seed_words, n_seed_words), groups, n_groups, n_units, n_workers, replication,
+      unit_bits, scratch, smem_elems);
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_permutation(const uint32_t* seed_words, int n_seed_words, const int32_t* skip_sizes,
+                    int n_skip, int n, int32_t* out, void* stream) {
+  if (!seed_words || n_seed_words < 1 || n_seed_words > 8)
+    return set_error(SDP_ERR_CONFIG, "seed must be given as 1..8 uint32 words");
+  if (n < 0 || n_skip < 0) return set_error(SDP_ERR_USAGE, "negative size");
+  k_permutation<<<1, 32, 0, as_stream(stream)>>>(make_seed(seed_words, n_seed_words), skip_sizes,
+                                                 n_skip, n, out);
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_build_masks(const sdp_param_desc* params, int n_params, const sdp_rule_desc* rules,
+                    int n_rules, const uint64_t* unit_bits, int n_workers, int64_t total,
+                    void* owner_mask, int mask_bytes, uint8_t* param_masks, int64_t* coverage,
+                    double* divisor, int64_t* governors, int64_t* active_counts, void* stream) {
+  (void)n_rules;
+  if (n_workers < 1 || n_workers > SDP_MAX_WORKERS)
+    return set_error(SDP_ERR_CONFIG, "n_workers must lie in [1, %d], got %d", SDP_MAX_WORKERS, n_workers);
+  if (owner_mask && (check_mask_bytes(mask_bytes) || mask_bytes * 8 < n_workers))
+    return set_error(SDP_ERR_CONFIG, "mask_bytes=%d cannot hold %d workers", mask_bytes, n_workers);
+  if (n_params < 1 || total < 1) return set_error(SDP_ERR_TOPOLOGY, "empty topology");
+  const int64_t n_chunks = (total + kBuildElems - 1) / kBuildElems;
+  const int64_t want = (n_chunks + kBuildThreads - 1) / kBuildThreads;
+  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 8));
+  auto ac = reinterpret_cast<unsigned long long*>(active_counts);
+  cudaStream_t s = as_stream(stream);
+  const int mb = owner_mask ? mask_bytes : 1;
+#define SDP_BUILD(MB)                                                                         \
+  k_build_masks<MB><<<grid, kBuildThreads, 0, s>>>(params, n_params, rules, unit_bits,        \
+                                                   n_workers, total,                          \
+                                                   static_cast<MaskT<MB>::T*>(owner_mask),    \
+                                                   param_masks, coverage, divisor, governors, ac)
+  switch (mb) {
+    case 1: SDP_BUILD(1); break;
+    case 2: SDP_BUILD(2); break;
+    case 4: SDP_BUILD(4); break;
+    default: SDP_BUILD(8); break;
+  }
+#undef SDP_BUILD
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_worker_mask(const void* owner_mask, int mask_bytes, int64_t total, int worker,
+                    double* mask_f64, uint8_t* mask_u8, void* stream) {
+  if (check_mask_bytes(mask_bytes)) return SDP_ERR_CONFIG;
+  if (worker < 0 || worker >= mask_bytes * 8)
+    return set_error(SDP_ERR_CONFIG, "worker id %d outside the mask width", worker);
+  if (total <= 0) return SDP_OK;
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sm_count() * 8));
+  cudaStream_t s = as_stream(stream);
+  switch (mask_bytes) {
+    case 1: k_worker_mask<1><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(owner_mask), total, worker, mask_f64, mask_u8); break;
+    case 2: k_worker_mask<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(owner_mask), total, worker, mask_f64, mask_u8); break;
+    case 4: k_worker_mask<4><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(owner_mask), total, worker, mask_f64, mask_u8); break;
+    default: k_worker_mask<8><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(owner_mask), total, worker, mask_f64, mask_u8); break;
+  }
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total, int tile,
+                   sdp_tile_desc* tiles, void* stream) {
+  if (check_mask_bytes(mask_bytes)) return SDP_ERR_CONFIG;
+  if (tile < 1024 || tile > (1 << 20) || tile % 1024)
+    return set_error(SDP_ERR_CONFIG, "tile must be a multiple of 1024 in [1024, 2^20], got %d", tile);
+  if (total <= 0) return SDP_OK;
+  const int64_t n_tiles = (total + tile - 1) / tile;
+  if (n_tiles > 0xFFFFFFFFll) return set_error(SDP_ERR_CONFIG, "too many tiles");
+  const int64_t warps_per_cta = 8;
+  const int grid = static_cast<int>(std::min<int64_t>((n_tiles + warps_per_cta - 1) / warps_per_cta, sm_count() * 8));
+  cudaStream_t s = as_stream(stream);
+  switch (mask_bytes) {
+    case 1: k_plan_tiles<1><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(owner_mask), total, tile, n_tiles, tiles); break;
+    case 2: k_plan_tiles<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(owner_mask), total, tile, n_tiles, tiles); break;
+    case 4: k_plan_tiles<4><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(owner_mask), total, tile, n_tiles, tiles); break;
+    default: k_plan_tiles<8><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(owner_mask), total, tile, n_tiles, tiles); break;
+  }
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,500 @@
+// Owner-subset sync: engine.aggregate (engine.py:60-79) as one HBM/NVLink-bound
+// kernel.
+//
+// Work unit = a tile of `tile` consecutive elements of the flat vector.  Each
+// CTA owns a CTA-major run of tile descriptors, staged into shared memory by
+// one bulk copy (cp.async.bulk + mbarrier, the TMA engine's non-tensor form).
+// For each element j with owner set O_j:
+//     acc = +0; for w in O_j ascending: acc += replica[w][j]
+//     mean = acc / max(|O_j|, 1)                 (IEEE divide)
+// and the mean goes to out / out_bf16 and (WRITEBACK) into every owner's replica
+// and bf16 shadow.  Uniform tiles (one owner set, the block strategy) run fully
+// vectorised 16-B loads with all owners' loads in flight; mixed tiles (neuron
+// strategy) read a per-element owner mask and only ever add owners.
+//
+// Replica pointers may be local (N logical workers co-resident in one HBM) or
+// peer-mapped NVLink addresses (one worker per GPU); with world > 1 each rank
+// runs only the tiles it leads, bracketed by release/acquire flag barriers.
+#include "sdp_common.cuh"
+
+namespace sdp {
+
+constexpr int kSyncThreads = 256;
+constexpr int kStage = 512;  // descriptors staged per bulk copy (8 KB)
+
+template <typename T> struct V;
+template <> struct V<float> {
+  static constexpr int N = 4;
+  struct type { float x[4]; };
+  __device__ static __forceinline__ type ld(const float* p) {
+    float4 r = ld_stream_f4(reinterpret_cast<const float4*>(p));
+    return type{{r.x, r.y, r.z, r.w}};
+  }
+  __device__ static __forceinline__ type ld_rw(const float* p) {
+    float4 r = *reinterpret_cast<const float4*>(p);
+    return type{{r.x, r.y, r.z, r.w}};
+  }
+  __device__ static __forceinline__ void st(float* p, const type& v) {
+    st_f4(reinterpret_cast<float4*>(p), make_float4(v.x[0], v.x[1], v.x[2], v.x[3]));
+  }
+  __device__ static __forceinline__ void st_bf16(__nv_bfloat16* p, const type& v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x[0], v.x[1]);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v.x[2], v.x[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+template <> struct V<double> {
+  static constexpr int N = 2;
+  struct type { double x[2]; };
+  __device__ static __forceinline__ type ld(const double* p) {
+    double2 r = ld_stream_d2(reinterpret_cast<const double2*>(p));
+    return type{{r.x, r.y}};
+  }
+  __device__ static __forceinline__ type ld_rw(const double* p) {
+    double2 r = *reinterpret_cast<const double2*>(p);
+    return type{{r.x, r.y}};
+  }
+  __device__ static __forceinline__ void st(double* p, const type& v) {
+    st_d2(reinterpret_cast<double2*>(p), make_double2(v.x[0], v.x[1]));
+  }
+  __device__ static __forceinline__ void st_bf16(__nv_bfloat16* p, const type& v) {
+    __nv_bfloat162 a;
+    a.x = __double2bfloat16(v.x[0]);
+    a.y = __double2bfloat16(v.x[1]);
+    *reinterpret_cast<__nv_bfloat162*>(p) = a;
+  }
+};
+
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ __nv_bfloat16 to_bf16(float x) { return __float2bfloat16_rn(x); }
+__device__ __forceinline__ __nv_bfloat16 to_bf16(double x) { return __double2bfloat16(x); }
+__device__ __forceinline__ bool finite(float x) { return isfinite(x); }
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+// Kernel parameter block (lives in the constant bank; ~1.2 KB).
+struct SyncParams {
+  const void* owner_mask;
+  const sdp_tile_desc* tiles;
+  void* replicas[SDP_MAX_WORKERS];
+  void* shadow[SDP_MAX_WORKERS];
+  void* out;
+  void* out_bf16;
+  void* theta;
+  void* velocity;
+  void* theta_bf16;
+  uint32_t* status;
+  uint32_t* pads[8];
+  double lr, momentum;
+  int64_t total;
+  int64_t timeout_cycles;
+  int32_t n_workers, tile, n_tiles, tiles_per_cta, flags, rank, world;
+  uint32_t epoch;
+  bool has_shadow;
+};
+
+// Pairwise per-CTA barrier: CTA b of every rank meets CTA b of every other rank.
+// Completion of a launch therefore implies every peer CTA has finished too.
+__device__ bool cross_rank_barrier(const SyncParams& p, uint32_t value) {
+  bool ok = true;
+  __syncthreads();
+  if (threadIdx.x < p.world) {
+    __threadfence_system();
+    const int peer = threadIdx.x;
+    st_release_sys(p.pads[peer] + blockIdx.x * p.world + p.rank, value);
+    const uint32_t* mine = p.pads[p.rank] + blockIdx.x * p.world + peer;
+    const long long t0 = clock64();
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - value) < 0) {
+      if (clock64() - t0 > p.timeout_cycles) {
+        ok = false;
+        if (p.status) atomicOr(p.status, SDP_STATUS_BARRIER_TIMEOUT);
+        break;
+      }
+    }
+  }
+  return __syncthreads_and(ok);
+}
+
+template <typename T>
+__device__ __forceinline__ void nesterov_elem(const SyncParams& p, int64_t j, T g) {
+  T* th = static_cast<T*>(p.theta);
+  T* ve = static_cast<T*>(p.velocity);
+  const T mu = static_cast<T>(p.momentum), lr = static_cast<T>(p.lr);
+  const T v = add_rn(mul_rn(ve[j], mu), g);           // velocity *= mu; velocity += g
+  const T t = sub_rn(th[j], mul_rn(lr, add_rn(g, mul_rn(mu, v))));  // theta -= lr*(g + mu*v)
+  ve[j] = v;
+  th[j] = t;
+  if (p.theta_bf16) static_cast<__nv_bfloat16*>(p.theta_bf16)[j] = to_bf16(t);
+}
+
+// Scalar path: one element, owner set `m` (partial tiles, unaligned tails).
+template <typename T>
+__device__ __forceinline__ void sync_elem(const SyncParams& p, int64_t j, uint64_t m, uint32_t& st) {
+  T acc = static_cast<T>(0);
+  for (uint64_t b = m; b; b &= b - 1) {
+    const int w = __ffsll(static_cast<long long>(b)) - 1;
+    acc = add_rn(acc, static_cast<const T*>(p.replicas[w])[j]);
+  }
+  const int c = __popcll(m);
+  const T mean = div_rn(acc, static_cast<T>(c > 0 ? c : 1));
+  if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+    for (int w = 0; w < p.n_workers; ++w)
+      if (!finite(static_cast<const T*>(p.replicas[w])[j])) st |= SDP_STATUS_UNCOVERED_LEAK;
+  }
+  if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean)) st |= SDP_STATUS_NONFINITE;
+  if (p.out) static_cast<T*>(p.out)[j] = mean;
+  if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[j] = to_bf16(mean);
+  if (p.flags & SDP_SYNC_WRITEBACK) {
+    for (uint64_t b = m; b; b &= b - 1) {
+      const int w = __ffsll(static_cast<long long>(b)) - 1;
+      static_cast<T*>(p.replicas[w])[j] = mean;
+      if (p.has_shadow && p.shadow[w]) static_cast<__nv_bfloat16*>(p.shadow[w])[j] = to_bf16(mean);
+    }
+  }
+  if (p.flags & SDP_SYNC_NESTEROV) nesterov_elem<T>(p, j, mean);
+}
+
+// Epilogue for one vector of VN consecutive elements with a common owner set.
+template <typename T>
+__device__ __forceinline__ void emit_vec(const SyncParams& p, int64_t j, uint64_t bits,
+                                         const typename V<T>::type& mean) {
+  constexpr int VN = V<T>::N;
+  if (p.out) V<T>::st(static_cast<T*>(p.out) + j, mean);
+  if (p.out_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.out_bf16) + j, mean);
+  if (p.flags & SDP_SYNC_WRITEBACK) {
+    for (uint64_t b = bits; b; b &= b - 1) {
+      const int w = __ffsll(static_cast<long long>(b)) - 1;
+      V<T>::st(static_cast<T*>(p.replicas[w]) + j, mean);
+      if (p.has_shadow && p.shadow[w]) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.shadow[w]) + j, mean);
+    }
+  }
+  if (p.flags & SDP_SYNC_NESTEROV) {
+    T* thp = static_cast<T*>(p.theta) + j;
+    T* vep = static_cast<T*>(p.velocity) + j;
+    typename V<T>::type th = V<T>::ld_rw(thp), ve = V<T>::ld_rw(vep);
+    const T mu = static_cast<T>(p.momentum), lr = static_cast<T>(p.lr);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      const T g = mean.x[e];
+      const T v = add_rn(mul_rn(ve.x[e], mu), g);
+      ve.x[e] = v;
+      th.x[e] = sub_rn(th.x[e], mul_rn(lr, add_rn(g, mul_rn(mu, v))));
+    }
+    V<T>::st(vep, ve);
+    V<T>::st(thp, th);
+    if (p.theta_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.theta_bf16) + j, th);
+  }
+}
+
+// Uniform tile: every element has owner set `bits`.  R vectors per thread per
+// round, owners consumed two at a time so 2R 16-B loads are in flight.
+template <typename T, int R>
+__device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s, uint64_t bits,
+                                                  uint32_t& st) {
+  constexpr int VN = V<T>::N;
+  using Vt = typename V<T>::type;
+  const int per_round = R * VN * kSyncThreads;
+  const int c = __popcll(bits);
+  const T denom = static_cast<T>(c > 0 ? c : 1);
+  for (int r0 = 0; r0 < p.tile; r0 += per_round) {
+    Vt acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[k].x[e] = static_cast<T>(0);
+    int64_t jv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) jv[k] = s + r0 + (k * kSyncThreads + threadIdx.x) * VN;
+    uint64_t b = bits;
+    while (b) {
+      const int w0 = __ffsll(static_cast<long long>(b)) - 1;
+      b &= b - 1;
+      const T* g0 = static_cast<const T*>(p.replicas[w0]);
+      Vt a[R], bb[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) a[k] = V<T>::ld(g0 + jv[k]);
+      const bool two = b != 0;
+      int w1 = 0;
+      if (two) {
+        w1 = __ffsll(static_cast<long long>(b)) - 1;
+        b &= b - 1;
+        const T* g1 = static_cast<const T*>(p.replicas[w1]);
+#pragma unroll
+        for (int k = 0; k < R; ++k) bb[k] = V<T>::ld(g1 + jv[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[k].x[e] = add_rn(acc[k].x[e], a[k].x[e]);
+      if (two) {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int e = 0; e < VN; ++e) acc[k].x[e] = add_rn(acc[k].x[e], bb[k].x[e]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      Vt mean;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        mean.x[e] = div_rn(acc[k].x[e], denom);
+        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+      }
+      if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+        for (int w = 0; w < p.n_workers; ++w) {
+          Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + jv[k]);
+#pragma unroll
+          for (int e = 0; e < VN; ++e)
+            if (!finite(g.x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
+        }
+      }
+      emit_vec<T>(p, jv[k], bits, mean);
+    }
+  }
+}
+
+// Mixed tile: per-element owner sets from the owner mask.  A vector is loaded
+// from every worker in the union of its VN elements' owner sets; each element
+// adds only its own owners, in ascending order.
+template <typename T, int MB>
+__device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, uint32_t& st) {
+  constexpr int VN = V<T>::N;
+  using Vt = typename V<T>::type;
+  using M = typename MaskT<MB>::T;
+  const M* mask = static_cast<const M*>(p.owner_mask);
+  for (int q = threadIdx.x; q < p.tile / VN; q += kSyncThreads) {
+    const int64_t j = s + static_cast<int64_t>(q) * VN;
+    uint64_t m[VN];
+    uint64_t uni = 0, inter = ~0ull;
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      m[e] = static_cast<uint64_t>(__ldg(mask + j + e));
+      uni |= m[e];
+      inter &= m[e];
+    }
+    if (uni == inter) {  // the VN elements agree: vector path
+      Vt acc;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc.x[e] = static_cast<T>(0);
+      for (uint64_t b = uni; b; b &= b - 1) {
+        const int w = __ffsll(static_cast<long long>(b)) - 1;
+        Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc.x[e] = add_rn(acc.x[e], g.x[e]);
+      }
+      const int c = __popcll(uni);
+      Vt mean;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        mean.x[e] = div_rn(acc.x[e], static_cast<T>(c > 0 ? c : 1));
+        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+      }
+      if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+        for (int w = 0; w < p.n_workers; ++w) {
+          Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
+#pragma unroll
+          for (int e = 0; e < VN; ++e)
+            if (!finite(g.x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
+        }
+      }
+      emit_vec<T>(p, j, uni, mean);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VN; ++e) sync_elem<T>(p, j + e, m[e], st);
+    }
+  }
+}
+
+template <typename T, int MB, int R>
+__global__ void __launch_bounds__(kSyncThreads)
+k_owner_sync(const __grid_constant__ SyncParams p) {
+  __shared__ alignas(16) sdp_tile_desc s_desc[kStage];
+  __shared__ alignas(8) uint64_t s_bar;
+  uint32_t st = 0;
+  if (p.world > 1 && !cross_rank_barrier(p, 2u * p.epoch + 1u)) return;
+
+  const int first = blockIdx.x * p.tiles_per_cta;
+  const int count = min(p.tiles_per_cta, p.n_tiles - first);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int k0 = 0; k0 < count; k0 += kStage) {
+    const int nk = min(kStage, count - k0);
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(nk * sizeof(sdp_tile_desc));
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      bulk_g2s(s_desc, p.tiles + first + k0, bytes, &s_bar);
+    }
+    mbar_wait(&s_bar, phase);
+    phase ^= 1;
+    for (int k = 0; k < nk; ++k) {
+      const sdp_tile_desc d = s_desc[k];
+      const int len = static_cast<int>(d.len_flags & SDP_TILE_LEN_MASK);
+      if (len == 0) continue;
+      const int64_t s = static_cast<int64_t>(d.tile_index) * p.tile;
+      const bool uniform = (d.len_flags & SDP_TILE_UNIFORM) != 0;
+      if (len == p.tile) {
+        if (uniform) sync_uniform_tile<T, R>(p, s, d.owner_bits, st);
+        else sync_mixed_tile<T, MB>(p, s, st);
+      } else {
+        const typename MaskT<MB>::T* mask = static_cast<const typename MaskT<MB>::T*>(p.owner_mask);
+        for (int e = threadIdx.x; e < len; e += kSyncThreads) {
+          const uint64_t m = uniform ? d.owner_bits : static_cast<uint64_t>(mask[s + e]);
+          sync_elem<T>(p, s + e, m, st);
+        }
+      }
+    }
+    __syncthreads();  // s_desc is overwritten by the next stage
+  }
+  if (st && p.status) atomicOr(p.status, st);
+  if (p.world > 1) cross_rank_barrier(p, 2u * p.epoch + 2u);
+}
+
+template <typename T>
+__global__ void k_nesterov(int64_t total, T* __restrict__ theta, T* __restrict__ vel,
+                           const T* __restrict__ grad, double lr, double momentum,
+                           __nv_bfloat16* __restrict__ theta_bf16, uint32_t* status) {
+  const T mu = static_cast<T>(momentum), lrt = static_cast<T>(lr);
+  uint32_t st = 0;
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T g = grad[j];
+    if (!finite(g)) st = SDP_STATUS_NONFINITE;
+    const T v = add_rn(mul_rn(vel[j], mu), g);
+    const T t = sub_rn(theta[j], mul_rn(lrt, add_rn(g, mul_rn(mu, v))));
+    vel[j] = v;
+    theta[j] = t;
+    if (theta_bf16) theta_bf16[j] = to_bf16(t);
+  }
+  if (__any_sync(0xffffffffu, st != 0) && (threadIdx.x & 31) == 0 && status)
+    atomicOr(status, SDP_STATUS_NONFINITE);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace sdp
+
+using namespace sdp;
+
+extern "C" {
+
+int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
+  if (!a) return set_error(SDP_ERR_USAGE, "null args");
+  if (a->dtype != SDP_DTYPE_F32 && a->dtype != SDP_DTYPE_F64)
+    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  if (a->n_workers < 1 || a->n_workers > SDP_MAX_WORKERS)
+    return set_error(SDP_ERR_CONFIG, "n_workers must lie in [1, %d]", SDP_MAX_WORKERS);
+  const int mb = a->mask_bytes;
+  if (!(mb == 1 || mb == 2 || mb == 4 || mb == 8) || mb * 8 < a->n_workers)
+    return set_error(SDP_ERR_CONFIG, "mask_bytes=%d cannot hold %d workers", mb, a->n_workers);
+  if (a->tile < 4096 || a->tile % 4096 || a->tile > (1 << 20))
+    return set_error(SDP_ERR_CONFIG, "sync tile must be a multiple of 4096 in [4096, 2^20]");
+  if (a->n_tiles < 0 || a->tiles_per_cta < 1) return set_error(SDP_ERR_CONFIG, "bad tile plan");
+  if (a->world < 1 || a->world > 8 || a->rank < 0 || a->rank >= a->world)
+    return set_error(SDP_ERR_CONFIG, "rank %d / world %d invalid (world <= 8)", a->rank, a->world);
+  if (a->n_tiles == 0) return SDP_OK;
+  if (!a->tiles || !aligned16(a->tiles)) return set_error(SDP_ERR_USAGE, "tile table must be 16-byte aligned");
+  for (int w = 0; w < a->n_workers; ++w) {
+    if (!a->replicas[w]) return set_error(SDP_ERR_PROTOCOL, "replica %d is NULL", w);
+    if (!aligned16(a->replicas[w]) || (a->shadow_bf16[w] && (reinterpret_cast<uintptr_t>(a->shadow_bf16[w]) & 7u)))
+      return set_error(SDP_ERR_USAGE, "replica %d buffers are not 16-byte aligned", w);
+  }
+  if ((a->out && !aligned16(a->out)) || (a->out_bf16 && (reinterpret_cast<uintptr_t>(a->out_bf16) & 7u)))
+    return set_error(SDP_ERR_USAGE, "output buffers are not 16-byte aligned");
+  if (a->flags & SDP_SYNC_NESTEROV) {
+    if (!a->theta || !a->velocity || !aligned16(a->theta) || !aligned16(a->velocity))
+      return set_error(SDP_ERR_USAGE, "fused Nesterov needs 16-byte aligned theta and velocity");
+  }
+  if (a->world > 1) {
+    for (int r = 0; r < a->world; ++r)
+      if (!a->signal_pads[r]) return set_error(SDP_ERR_USAGE, "signal pad of rank %d missing", r);
+  }
+
+  SyncParams p{};
+  p.owner_mask = a->owner_mask;
+  p.tiles = a->tiles;
+  p.has_shadow = false;
+  for (int w = 0; w < SDP_MAX_WORKERS; ++w) {
+    p.replicas[w] = w < a->n_workers ? a->replicas[w] : nullptr;
+    p.shadow[w] = w < a->n_workers ? a->shadow_bf16[w] : nullptr;
+    p.has_shadow |= p.shadow[w] != nullptr;
+  }
+  p.out = a->out;
+  p.out_bf16 = a->out_bf16;
+  p.theta = a->theta;
+  p.velocity = a->velocity;
+  p.theta_bf16 = a->theta_bf16;
+  p.status = a->status;
+  for (int r = 0; r < 8; ++r) p.pads[r] = r < a->world ? a->signal_pads[r] : nullptr;
+  p.lr = a->lr;
+  p.momentum = a->momentum;
+  p.total = a->total;
+  p.timeout_cycles = a->timeout_cycles > 0 ? a->timeout_cycles : (int64_t)20000000000ll;
+  p.n_workers = a->n_workers;
+  p.tile = a->tile;
+  p.n_tiles = a->n_tiles;
+  p.tiles_per_cta = a->tiles_per_cta;
+  p.flags = a->flags;
+  p.rank = a->rank;
+  p.world = a->world;
+  p.epoch = a->epoch;
+
+  const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
+  cudaStream_t s = as_stream(stream);
+  // R vectors per thread per round: a 4096-element fp32 tile = 4 float4/thread.
+#define SDP_SYNC_LAUNCH(T, MB) k_owner_sync<T, MB, 4><<<grid, kSyncThreads, 0, s>>>(p)
+  if (a->dtype == SDP_DTYPE_F32) {
+    switch (mb) {
+      case 1: SDP_SYNC_LAUNCH(float, 1); break;
+      case 2: SDP_SYNC_LAUNCH(float, 2); break;
+      case 4: SDP_SYNC_LAUNCH(float, 4); break;
+      default: SDP_SYNC_LAUNCH(float, 8); break;
+    }
+  } else {
+    switch (mb) {
+      case 1: SDP_SYNC_LAUNCH(double, 1); break;
+      case 2: SDP_SYNC_LAUNCH(double, 2); break;
+      case 4: SDP_SYNC_LAUNCH(double, 4); break;
+      default: SDP_SYNC_LAUNCH(double, 8); break;
+    }
+  }
+#undef SDP_SYNC_LAUNCH
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity, const void* grad,
+                        double lr, double momentum, void* theta_bf16, uint32_t* status,
+                        void* stream) {
+  if (total <= 0) return SDP_OK;
+  if (!theta || !velocity || !grad) return set_error(SDP_ERR_USAGE, "null buffer");
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sm_count() * 8));
+  cudaStream_t s = as_stream(stream);
+  if (dtype == SDP_DTYPE_F32)
+    k_nesterov<float><<<grid, 256, 0, s>>>(total, static_cast<float*>(theta), static_cast<float*>(velocity),
+                                           static_cast<const float*>(grad), lr, momentum,
+                                           static_cast<__nv_bfloat16*>(theta_bf16), status);
+  else if (dtype == SDP_DTYPE_F64)
+    k_nesterov<double><<<grid, 256, 0, s>>>(total, static_cast<double*>(theta), static_cast<double*>(velocity),
+                                            static_cast<const double*>(grad), lr, momentum,
+                                            static_cast<__nv_bfloat16*>(theta_bf16), status);
+  else
+    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,305 @@
+"""Owner-subset sync behind the reference's `aggregate` (engine.py:60-79).
+
+    aggregate(grads, assignment) -> AggregatedGradient(gbar, divisor)
+
+keeps the reference signature, argument meaning and errors: `grads` is a list
+of N flat gradients (CUDA tensors -- or numpy arrays, which are copied to the
+device and the mean copied back), `gbar` is a fresh buffer, `divisor` is the
+assignment's float64 divisor, ProtocolError on a wrong count or an uncovered
+leak.  Underneath, one launch of libsdp's k_owner_sync reads each element from
+its owners only, in ascending worker order, and divides by the owner count.
+
+`owner_sync` is the B200-native form of the same step: the
+mean is written back into every owner's replica (and an optional bf16
+training copy) -- what an all-reduce over the owner subset leaves behind --
+optionally fused with the SGD-Nesterov update (optim.py:78-84).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._device import device, ptr, sdp_dtype, stream_ptr, upload_struct
+from .errors import NumericalError, ProtocolError, UsageError
+
+TILE = 4096              # elements per sync tile (16 KB of fp32 per replica)
+TILE_DTYPE = np.dtype([("owner_bits", "<u8"), ("tile_index", "<u4"), ("len_flags", "<u4")])
+CTAS_PER_SM = 4          # 64 regs x 256 threads -> 4 resident CTAs per SM
+
+
+@dataclass
+class AggregatedGradient:
+    gbar: object
+    divisor: object
+
+
+def _sm_count() -> int:
+    n = C.c_int(0)
+    N.call("sdp_device_sm_count", C.byref(n))
+    return int(n.value)
+
+
+def gpu_of_worker(n_workers: int, world: int) -> np.ndarray:
+    """Contiguous placement of N logical workers on `world` GPUs: w -> w*G//N."""
+    return np.array([w * world // n_workers for w in range(n_workers)], dtype=np.int64)
+
+
+def tile_leaders(tiles: np.ndarray, gpu_of: np.ndarray, world: int) -> np.ndarray:
+    """Rank that reduces each tile: the owner GPUs of the tile take turns
+    (tile t -> the (t mod k)-th of its k owner GPUs), so one of the reads is
+    always local and every owner GPU leads an equal share; uncovered tiles are
+    dealt round-robin."""
+    n = len(tiles)
+    out = np.empty(n, dtype=np.int64)
+    bits = tiles["owner_bits"].astype(np.uint64)
+    # owner-GPU set per tile as a bitmask over ranks
+    gmask = np.zeros(n, dtype=np.int64)
+    for w, g in enumerate(gpu_of):
+        on = ((bits >> np.uint64(w)) & np.uint64(1)).astype(bool)
+        gmask[on] |= 1 << int(g)
+    for m in np.unique(gmask):
+        sel = np.nonzero(gmask == m)[0]
+        gpus = [g for g in range(world) if m >> g & 1]
+        out[sel] = [gpus[t % len(gpus)] for t in sel] if gpus else sel % world
+    return out
+
+
+def plan_grid(n_tiles: int, sms: int, resident: bool) -> int:
+    """Persistent grid for co-residency (cross-rank barrier), else enough
+    CTAs for ~8 waves of single tiles so the tail is short."""
+    cap = sms * CTAS_PER_SM * (1 if resident else 8)
+    return max(1, min(n_tiles, cap))
+
+
+def cta_major(tiles: np.ndarray, grid: int, tiles_per_cta: int) -> np.ndarray:
+    """Descriptor table where CTA b's tiles (b, b+grid, b+2*grid, ...) are
+    contiguous, so one bulk copy stages them; holes have length 0."""
+    table = np.zeros(grid * tiles_per_cta, dtype=TILE_DTYPE)
+    for k in range(tiles_per_cta):
+        sel = tiles[k * grid:(k + 1) * grid]
+        table[np.arange(len(sel)) * tiles_per_cta + k] = sel
+    return table
+
+
+class SyncPlan:
+    """Tile plan of one assignment: which tiles have a single owner set, which
+    rank leads each tile, and the CTA-major descriptor table k_owner_sync
+    stages into shared memory.
+
+    world/rank: multi-GPU split (tiles led by `rank`); gpu_of_worker maps the
+    logical workers to ranks (contiguous placement, SURVEY.md §7 hard part 6).
+    """
+
+    def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int = TILE,
+                 resident: bool = False):
+        self.assignment = assignment
+        dev = assignment.device
+        d = assignment.topology.total
+        self.tile = tile
+        self.world, self.rank = world, rank
+        n_tiles = (d + tile - 1) // tile
+        raw = torch.empty(max(1, n_tiles) * TILE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        N.call("sdp_plan_tiles", ptr(assignment.owner_mask), assignment.mask_bytes, d, tile,
+               ptr(raw), stream_ptr(dev))
+        tiles = raw.cpu().numpy().view(TILE_DTYPE)[:n_tiles].copy()
+        self.all_tiles = tiles
+        self.n_uniform = int(((tiles["len_flags"] & N.TILE_UNIFORM) != 0).sum())
+        nw = assignment.n_workers
+        self.gpu_of_worker = gpu_of_worker(nw, world)
+        if world > 1:
+            mine = tiles[tile_leaders(tiles, self.gpu_of_worker, world) == rank]
+        else:
+            mine = tiles
+        self.n_tiles = len(mine)
+        # every CTA must be co-resident for the cross-rank flag barrier
+        self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1)
+        self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
+        self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
+        self.owned_elems = self._owned_elems(mine)
+
+    def _owned_elems(self, tiles) -> int:
+        """sum over this rank's tiles of |O_j| elements (exact for uniform tiles)."""
+        if len(tiles) == 0:
+            return 0
+        lens = (tiles["len_flags"] & N.TILE_LEN_MASK).astype(np.int64)
+        bits = tiles["owner_bits"]
+        pop = np.zeros(len(tiles), dtype=np.int64)
+        for b in range(64):
+            pop += ((bits >> np.uint64(b)) & np.uint64(1)).astype(np.int64)
+        return int((lens * pop).sum())
+
+    def args(self, dtype: int) -> N.SyncArgs:
+        a = self.assignment
+        s = N.SyncArgs()
+        s.dtype = dtype
+        s.n_workers = a.n_workers
+        s.mask_bytes = a.mask_bytes
+        s.tile = self.tile
+        s.total = a.topology.total
+        s.owner_mask = a.owner_mask.data_ptr()
+        s.tiles = self.table.data_ptr()
+        s.n_tiles = self.grid * self.tiles_per_cta
+        s.tiles_per_cta = self.tiles_per_cta
+        s.grid = self.grid
+        s.rank = self.rank
+        s.world = 1
+        return s
+
+
+def _as_replica_list(grads, n: int, d: int):
+    if torch.is_tensor(grads) and grads.dim() == 2:
+        if grads.shape != (n, d):
+            raise ProtocolError(f"aggregate received {grads.shape[0]} gradients for {n} workers")
+        return [grads[i] for i in range(n)]
+    if len(grads) != n:
+        raise ProtocolError(f"aggregate received {len(grads)} gradients for {n} workers")
+    return list(grads)
+
+
+def _aligned(t: torch.Tensor) -> bool:
+    return t.is_contiguous() and t.data_ptr() % 16 == 0
+
+
+class PreparedSync:
+    """A fully bound k_owner_sync launch (args built once): the steady-state
+    form used by training loops and the benchmark -- one ctypes call per step."""
+
+    def __init__(self, replicas, assignment, **kw):
+        self._keep = (replicas, kw)
+        self.args = _bind(replicas, assignment, **kw)
+        self.status = kw.get("status")
+        self.device = assignment.device
+        self._fn = N.lib().sdp_owner_sync
+        self._ref = C.byref(self.args)
+
+    def launch(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self._fn(self._ref, C.c_void_p(s.cuda_stream))
+        if rc:
+            N.check(rc, "sdp_owner_sync")
+
+
+def owner_sync(replicas, assignment, **kw) -> torch.Tensor | None:
+    """One launch of k_owner_sync over co-resident replicas (one GPU, N logical
+    workers).  Returns the device status word tensor (not synchronised).
+
+    out / out_bf16: the mean (dtype / bf16); writeback: mean into every owner's
+    replica; shadows_bf16: per-worker bf16 training copies;
+    nesterov: {"theta": t, "velocity": v, "lr": float, "momentum": float,
+               "theta_bf16": optional} applies optim.py:81-84 in the epilogue.
+    """
+    if kw.get("status") is None and (kw.get("check_uncovered") or kw.get("check_finite")):
+        kw["status"] = torch.zeros(1, dtype=torch.int32, device=assignment.device)
+    a = _bind(replicas, assignment, **kw)
+    N.check(N.lib().sdp_owner_sync(C.byref(a), stream_ptr(assignment.device)), "sdp_owner_sync")
+    return kw.get("status")
+
+
+def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
+          out_bf16: torch.Tensor | None = None, writeback: bool = True,
+          shadows_bf16=None, check_uncovered: bool = False, check_finite: bool = False,
+          nesterov: dict | None = None, status: torch.Tensor | None = None,
+          plan: SyncPlan | None = None) -> N.SyncArgs:
+    n, d = assignment.n_workers, assignment.topology.total
+    reps = _as_replica_list(replicas, n, d)
+    dt = reps[0].dtype
+    dev = assignment.device
+    for r in reps:
+        if r.dtype != dt or r.numel() != d or r.device != dev or not _aligned(r):
+            raise UsageError("replicas must be contiguous, 16-byte aligned, same dtype, "
+                             f"[{d}] on {dev}")
+    plan = plan or assignment.sync_plan()
+    a = plan.args(sdp_dtype(dt))
+    flags = 0
+    if writeback:
+        flags |= N.SYNC_WRITEBACK
+    if check_uncovered:
+        flags |= N.SYNC_CHECK_UNCOVERED
+    if check_finite:
+        flags |= N.SYNC_CHECK_FINITE
+    for w, r in enumerate(reps):
+        a.replicas[w] = r.data_ptr()
+    if shadows_bf16 is not None:
+        for w, sh in enumerate(shadows_bf16):
+            a.shadow_bf16[w] = None if sh is None else sh.data_ptr()
+    a.out = None if out is None else out.data_ptr()
+    a.out_bf16 = None if out_bf16 is None else out_bf16.data_ptr()
+    if nesterov is not None:
+        flags |= N.SYNC_NESTEROV
+        a.theta = nesterov["theta"].data_ptr()
+        a.velocity = nesterov["velocity"].data_ptr()
+        tb = nesterov.get("theta_bf16")
+        a.theta_bf16 = None if tb is None else tb.data_ptr()
+        a.lr = float(nesterov["lr"])
+        a.momentum = float(nesterov.get("momentum", 0.9))
+    a.status = None if status is None else status.data_ptr()
+    a.flags = flags
+    return a
+
+
+def aggregate(grads, assignment) -> AggregatedGradient:
+    """Masked averaging gbar_j = sum_i m_ij g_ij / sum_i m_ij (engine.py:60-79).
+
+    Workers are accumulated in ascending id order from +0; uncovered entries get
+    0.  float64 inputs reproduce the reference bit for bit; float32 inputs follow
+    the same recurrence in fp32.  numpy inputs are copied to the device and the
+    mean is returned as numpy (the host-buffer end-to-end path).
+    """
+    n, d = assignment.n_workers, assignment.topology.total
+    if not torch.is_tensor(grads) and len(grads) != n:
+        raise ProtocolError(f"aggregate received {len(grads)} gradients for {n} workers")
+    host = not torch.is_tensor(grads) and len(grads) > 0 and isinstance(grads[0], np.ndarray)
+    dev = assignment.device
+    if host:
+        dt = torch.float64 if grads[0].dtype == np.float64 else torch.float32
+        # async H2D when the numpy buffers are views of pinned memory
+        reps = [torch.from_numpy(np.ascontiguousarray(g, dtype=dt_np(dt))).to(dev, non_blocking=True)
+                for g in grads]
+    else:
+        reps = _as_replica_list(grads, n, d)
+        dt = reps[0].dtype
+        reps = [r if _aligned(r) and r.dtype == dt else r.contiguous().clone() for r in reps]
+    gbar = torch.empty(d, dtype=dt, device=dev)
+    check = assignment.uncovered_params > 0
+    status = owner_sync(reps, assignment, out=gbar, writeback=False, check_uncovered=check)
+    if check and int(status.item()) & N.STATUS_UNCOVERED_LEAK:
+        raise ProtocolError("a gradient reached a parameter with zero mask coverage")
+    if host:
+        out = torch.empty(d, dtype=dt, pin_memory=True)
+        out.copy_(gbar, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return AggregatedGradient(gbar=out.numpy(), divisor=assignment.host_divisor())
+    return AggregatedGradient(gbar=gbar, divisor=assignment.divisor)
+
+
+def dt_np(dt: torch.dtype):
+    return np.float64 if dt == torch.float64 else np.float32
+
+
+class SgdNesterov:
+    """optim.SgdNesterov (optim.py:71-87) over a device theta, on libsdp's
+    k_nesterov: v = mu v + g; theta -= lr (g + mu v); NumericalError on a
+    non-finite gradient."""
+
+    kind = "sgd-nesterov"
+
+    def __init__(self, dim: int, momentum: float = 0.9, dtype=torch.float32, device_=None):
+        self.momentum = momentum
+        self.velocity = torch.zeros(dim, dtype=dtype, device=device(device_))
+
+    def update(self, theta: torch.Tensor, grad: torch.Tensor, lr: float,
+               theta_bf16: torch.Tensor | None = None) -> None:
+        status = torch.zeros(1, dtype=torch.int32, device=theta.device)
+        N.call("sdp_nesterov_update", sdp_dtype(theta.dtype), theta.numel(), ptr(theta),
+               ptr(self.velocity), ptr(grad), float(lr), float(self.momentum), ptr(theta_bf16),
+               ptr(status), stream_ptr(theta.device))
+        if int(status.item()) & N.STATUS_NONFINITE:
+            raise NumericalError("aggregated gradient contains non-finite values")
+
+    def state_elements(self) -> int:
+        return self.velocity.numel()

@@ -1,0 +1,233 @@
+"""k_owner_sync vs the reference's aggregate (golden) and the fp32 restatement.
+
+Criteria:
+  1. float64: bit-identical to reference engine.aggregate;
+  2. float32: bit-identical to the oracle's ordered fp32 recurrence, and within
+     |out - ref| <= 1e-6 * max(|ref|, sum_owners|g| / P) of the float64 reference
+     (the condition-scaled tolerance; north star: 1e-6 relative in fp32);
+  3. bf16 output == RNE(fp32 output) bit for bit (=> <= 1 ulp vs bf16(ref)).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import _golden as G
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL_F32 = 1e-6
+
+
+def _pkg():
+    from paper_2507_09029_b200 import engine, masking
+    return engine, masking
+
+
+def _build(case):
+    _, masking = _pkg()
+    return masking.build_assignment(G.topology(case["model"]), case["strategy"], case["n"],
+                                    case["p"], case["seed"])
+
+
+@pytest.mark.parametrize("case", G.cases(with_grads=True), ids=lambda c: f"c{c['id']}-{c['strategy']}-N{c['n']}P{c['p']}")
+def test_aggregate_f64_bitexact_vs_reference(cuda, case):
+    engine, _ = _pkg()
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    dev_grads = [torch.from_numpy(g).to(cuda) for g in grads]
+    out = engine.aggregate(dev_grads, a)
+    ref = G.arrays()[f"c{case['id']}_gbar"]
+    assert np.array_equal(out.gbar.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+    assert torch.equal(out.divisor, a.divisor)
+    # host numpy path (end-to-end) returns the same bits
+    host = engine.aggregate(list(grads), a)
+    assert np.array_equal(host.gbar.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("case", G.cases(with_grads=True), ids=lambda c: f"c{c['id']}")
+def test_aggregate_f32_bitexact_vs_restatement_and_tolerance(cuda, case):
+    engine, _ = _pkg()
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    g32 = grads.astype(np.float32)
+    out = engine.aggregate([torch.from_numpy(g).to(cuda) for g in g32], a).gbar.cpu().numpy()
+    want = O.aggregate_f32_ordered(list(g32), masks)
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32))
+    ref = O.aggregate_f64(list(g32.astype(np.float64)), masks, np.maximum(masks.sum(0), 1).astype(np.float64))
+    scale = np.maximum(np.abs(ref), (np.abs(g32.astype(np.float64)) * masks).sum(0) / np.maximum(masks.sum(0), 1))
+    assert np.all(np.abs(out - ref) <= REL_TOL_F32 * scale)
+
+
+def test_disjoint_known_answer(cuda):
+    """m1=[1,0], m2=[0,1], g1=[2,0], g2=[0,4] -> [2,4]."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    topo = zoo.residual_mlp_topology(width=1, blocks=2, classes=1, in_dim=1)
+    # blocks 0 and 1 (2 params each) on disjoint workers
+    ba = np.array([[1, 0], [0, 1]], dtype=bool)
+    pm = masking.induce_block_param_mask(topo, ba)
+    a = masking.MaskAssignment(2, 1, "block", 0, topo, {}, pm, torch.zeros(topo.total, dtype=torch.int64))
+    g = [torch.zeros(topo.total, dtype=torch.float64, device=cuda) for _ in range(2)]
+    b0, b1 = topo.slice_of("block0.lin1.w"), topo.slice_of("block1.lin1.w")
+    g[0][b0] = 2.0
+    g[1][b1] = 4.0
+    out = engine.aggregate(g, a).gbar
+    assert out[b0].item() == 2.0 and out[b1].item() == 4.0
+
+
+def test_wrong_count_raises_protocol_error(cuda):
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import ProtocolError
+    case = G.cases(with_grads=True)[0]
+    a = _build(case)
+    with pytest.raises(ProtocolError, match="gradients for"):
+        engine.aggregate([torch.zeros(case["d"], device=cuda)], a)
+
+
+def test_uncovered_leak_raises_protocol_error(cuda):
+    """engine.py:75-78: a non-finite entry at a zero-coverage parameter."""
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import ProtocolError
+    case = next(c for c in G.cases(with_grads=True) if c["uncovered_params"] > 0)
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    unc = np.nonzero(~masks.any(0))[0]
+    grads[1, unc[0]] = np.inf
+    with pytest.raises(ProtocolError, match="zero mask coverage"):
+        engine.aggregate([torch.from_numpy(g).to(cuda) for g in grads], a)
+    # finite junk at an uncovered entry is masked away exactly as 0*g is
+    grads[1, unc[0]] = 3.0
+    out = engine.aggregate([torch.from_numpy(g).to(cuda) for g in grads], a).gbar
+    assert out[int(unc[0])].item() == 0.0
+
+
+def _replicas(a, dtype, seed, cuda):
+    """N logical replicas, seeded randn, zero off-mask (reference nullity)."""
+    n, d = a.n_workers, a.topology.total
+    gen = torch.Generator(device=cuda)
+    reps = []
+    pm = a.param_masks
+    for w in range(n):
+        gen.manual_seed(seed + w)
+        reps.append(torch.randn(d, generator=gen, device=cuda, dtype=torch.float32).to(dtype) * pm[w])
+    return reps
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_writeback_bf16_and_replica_identity(cuda, strategy):
+    """Replica mode: every owner ends with the identical mean; bf16 shadow == RNE(fp32)."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32))
+    a = masking.build_assignment(topo, strategy, 8, 3, seed=1)
+    reps = _replicas(a, torch.float32, 1000, cuda)
+    host = [r.cpu().numpy() for r in reps]
+    masks = a.param_masks.cpu().numpy()
+    want = O.aggregate_f32_ordered(host, masks)
+    shadows = [torch.zeros(topo.total, dtype=torch.bfloat16, device=cuda) for _ in reps]
+    out = torch.empty(topo.total, device=cuda)
+    outb = torch.empty(topo.total, dtype=torch.bfloat16, device=cuda)
+    engine.owner_sync(reps, a, out=out, out_bf16=outb, shadows_bf16=shadows)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    wb = O.bf16_rne(want)
+    assert np.array_equal(outb.view(torch.int16).cpu().numpy().view(np.uint16), wb)
+    for w in range(8):
+        m = masks[w]
+        got = reps[w].cpu().numpy()
+        assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32))
+        assert np.array_equal(got[~m], host[w][~m])  # non-owned entries untouched
+        sh = shadows[w].view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(sh[m], wb[m]) and np.all(sh[~m] == 0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fused_nesterov_matches_reference_step(cuda, dtype):
+    """SDP_SYNC_NESTEROV epilogue == aggregate then optim.SgdNesterov.update (optim.py:78-84)."""
+    engine, _ = _pkg()
+    for case in G.cases(with_grads=True)[:6]:
+        a = _build(case)
+        masks = G.case_masks(case)
+        grads, theta0, vel0 = G.case_inputs(case, masks)
+        npdt = np.float64 if dtype == torch.float64 else np.float32
+        th = torch.from_numpy(theta0.astype(npdt)).to(cuda)
+        ve = torch.from_numpy(vel0.astype(npdt)).to(cuda)
+        reps = [torch.from_numpy(g.astype(npdt)).to(cuda) for g in grads]
+        thb = torch.empty(case["d"], dtype=torch.bfloat16, device=cuda)
+        engine.owner_sync(reps, a, writeback=False,
+                          nesterov={"theta": th, "velocity": ve, "lr": 0.05, "momentum": 0.9,
+                                    "theta_bf16": thb})
+        if dtype == torch.float64:
+            assert np.array_equal(th.cpu().numpy().view(np.uint64),
+                                  G.arrays()[f"c{case['id']}_theta1"].view(np.uint64))
+            assert np.array_equal(ve.cpu().numpy().view(np.uint64),
+                                  G.arrays()[f"c{case['id']}_vel1"].view(np.uint64))
+        else:
+            g = O.aggregate_f32_ordered(list(grads.astype(np.float32)), masks)
+            t1, v1 = O.nesterov_update(theta0.astype(np.float32), vel0.astype(np.float32), g, 0.05, 0.9)
+            assert np.array_equal(th.cpu().numpy().view(np.uint32), t1.astype(np.float32).view(np.uint32))
+            assert np.array_equal(ve.cpu().numpy().view(np.uint32), v1.astype(np.float32).view(np.uint32))
+            assert np.array_equal(thb.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(t1))
+
+
+def test_standalone_nesterov_and_nonfinite(cuda):
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import NumericalError
+    d = 10001
+    rng = np.random.default_rng(3)
+    th0, g = rng.standard_normal(d), rng.standard_normal(d)
+    opt = engine.SgdNesterov(d, momentum=0.9, dtype=torch.float64)
+    th = torch.from_numpy(th0).to(cuda)
+    opt.update(th, torch.from_numpy(g).to(cuda), 0.1)
+    t1, v1 = O.nesterov_update(th0, np.zeros(d), g, 0.1, 0.9)
+    assert np.array_equal(th.cpu().numpy().view(np.uint64), t1.view(np.uint64))
+    g[5] = np.nan
+    with pytest.raises(NumericalError):
+        opt.update(th, torch.from_numpy(g).to(cuda), 0.1)
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (8, 3), (8, 8), (16, 5), (33, 7), (64, 20)])
+def test_mask_widths_and_partial_tiles(cuda, n, p):
+    """uint8/16/32/64 owner masks; d not a multiple of the tile or of 4."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    topo = zoo.residual_mlp_topology(width=37, blocks=max(n, 4), classes=3, in_dim=5)
+    for strategy in ("block", "neuron"):
+        a = masking.build_assignment(topo, strategy, n, p, seed=n * 100 + p)
+        reps = _replicas(a, torch.float32, 7, cuda)
+        masks = a.param_masks.cpu().numpy()
+        want = O.aggregate_f32_ordered([r.cpu().numpy() for r in reps], masks)
+        got = engine.aggregate(reps, a).gbar.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (strategy, n, p)
+
+
+@pytest.mark.slow
+def test_resnet18_and_gpt2_full_size_properties(cuda):
+    """Full C2/C4 sizes: replicas bit-identical after writeback, mean of an
+    all-equal input is that input, and linearity sync(a*x) == a*sync(x) for a=2."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    for topo in (zoo.resnet18_cifar_topology(), zoo.gpt2_small_topology()):
+        a = masking.build_assignment(topo, "block", 8, 4, seed=1)
+        reps = _replicas(a, torch.float32, 11, cuda)
+        doubled = [r * 2 for r in reps]
+        out1 = torch.empty(topo.total, device=cuda)
+        out2 = torch.empty(topo.total, device=cuda)
+        engine.owner_sync(reps, a, out=out1)
+        engine.owner_sync(doubled, a, out=out2)
+        assert torch.equal(out2, out1 * 2)  # exact: scaling by 2 commutes with RN
+        pm = a.param_masks
+        for w in range(8):
+            assert torch.equal(reps[w][pm[w]], out1[pm[w]])
+        # identical inputs on every owner -> mean equals the input when P is a power of 2
+        x = torch.randn(topo.total, device=cuda)
+        same = [x * pm[w] for w in range(8)]
+        out3 = torch.empty_like(x)
+        engine.owner_sync(same, a, out=out3, writeback=False)
+        assert torch.equal(out3, x)
+        del reps, doubled, same
+        torch.cuda.empty_cache()
