@@ -269,11 +269,20 @@ def run_ours(args):
         parallelism = f"{n} logical workers co-resident on 1 GPU"
         del pm
 
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    # L2 flush between timed launches: write 256 MB (> 126 MB L2), then read
+    # another 256 MB so the lines left behind are clean -- otherwise the timed
+    # kernel pays for evicting the flush's dirty lines.
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    flush_rd = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        flush.zero_()
+        flush_rd.sum()
+
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         step()
-        flush.zero_()
+        flush_l2()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -285,7 +294,7 @@ def run_ours(args):
             starts[i].record(stream)
             step()
             ends[i].record(stream)
-            flush.zero_()
+            flush_l2()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -327,7 +336,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "fp32 (bf16 copy fused)", "data": "synthetic",
             "config": {"workload": tag, "d": d, "n_logical": n, "p": p, "strategy": args.strategy,
                        "seed": 1, "parallelism": parallelism,
-                       "l2": "flushed between steps (256 MB write)", **meta},
+                       "l2": "flushed between steps: 256 MB write + 256 MB read (cold, clean L2)", **meta},
             "gpu_launches": args.steps,
             "roofline": roofline,
             "clocks": clocks.summary(),

@@ -1,0 +1,216 @@
+"""Multi-GPU owner-subset sync: one process per GPU, replicas peer-mapped over
+NVLink, no NCCL on the data path.
+
+Placement: the N logical workers sit contiguously on the G ranks
+(worker w on rank w*G//N, SURVEY.md §7 hard part 6), so at N = G each GPU is
+one worker and at G < N several workers share an HBM.
+
+Bootstrap (once): every rank allocates its local workers' replicas (+ bf16
+shadows) and a signal pad, exports CUDA-IPC handles, and all-gathers them
+through torch.distributed (the only collective, plumbing only); each rank
+then opens its peers' handles.  After that a sync step is ONE k_owner_sync
+launch per rank: the rank reduces the tiles it leads (engine.tile_leaders),
+reading every owner's replica -- local or over NVLink -- in ascending worker
+order, and writes the mean into every owner's replica and bf16 shadow.
+Per-CTA release/acquire flag barriers on the signal pads bracket the launch
+(entry: every peer's gradients are ready; exit: every peer's writes into my
+replicas have landed), with a spin timeout that reports instead of hanging.
+
+The exchange logic (`exchange_handles`, `rank_layout`) is CUDA-free so the
+N > 1 host path is tested with gloo on CPU (tests/test_multirank_gloo.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .engine import SyncPlan, gpu_of_worker
+from .errors import CudaError, ProtocolError
+
+PAD_WORDS_PER_CTA = 8  # >= world (<= 8 ranks)
+IPC_HANDLE_BYTES = 64  # SDP_IPC_HANDLE_BYTES
+
+
+@dataclass
+class RankLayout:
+    world: int
+    rank: int
+    n_workers: int
+    gpu_of: np.ndarray
+
+    @property
+    def local_workers(self) -> list[int]:
+        return [w for w in range(self.n_workers) if int(self.gpu_of[w]) == self.rank]
+
+
+def rank_layout(n_workers: int, world: int, rank: int) -> RankLayout:
+    if not 1 <= world <= 8:
+        raise ProtocolError(f"the peer-mapped sync supports 1..8 ranks, got {world}")
+    if world > n_workers:
+        raise ProtocolError(f"{world} ranks for {n_workers} workers: a rank would hold no replica")
+    return RankLayout(world, rank, n_workers, gpu_of_worker(n_workers, world))
+
+
+def exchange_handles(local: dict, all_gather) -> list[dict]:
+    """All-gather every rank's {name: (handle_bytes, offset)} export table.
+
+    `all_gather(obj) -> list[obj]` is torch.distributed.all_gather_object bound
+    to the process group (or a fake in tests)."""
+    tables = all_gather({k: (bytes(h), int(off)) for k, (h, off) in local.items()})
+    for r, t in enumerate(tables):
+        for k, (h, _) in t.items():
+            if len(h) != IPC_HANDLE_BYTES:
+                raise ProtocolError(f"rank {r} sent a malformed IPC handle for {k}")
+    return tables
+
+
+def ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64(0)
+    N.call("sdp_ipc_export", C.c_void_p(t.data_ptr()), h, C.byref(off))
+    return bytes(h), int(off.value)
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p(0)
+    N.call("sdp_ipc_import", h, C.c_uint64(offset), C.byref(p))
+    return int(p.value)
+
+
+def bind_rank_args(plan: SyncPlan, dtype: int, rep_ptr, sh_ptr, pad_ptr, status_ptr: int,
+                   timeout_cycles: int = 20_000_000_000) -> N.SyncArgs:
+    """k_owner_sync arguments of one rank: every worker's replica address (local
+    or peer-mapped), the ranks' signal pads, and the rank's own tile table."""
+    a = plan.args(dtype)
+    for w in range(plan.assignment.n_workers):
+        a.replicas[w] = rep_ptr[w]
+        a.shadow_bf16[w] = sh_ptr[w] or None
+    a.world = plan.world
+    a.rank = plan.rank
+    for r in range(plan.world):
+        a.signal_pads[r] = pad_ptr[r]
+    a.flags = N.SYNC_WRITEBACK
+    a.status = status_ptr
+    a.timeout_cycles = timeout_cycles
+    return a
+
+
+class PeerGroup:
+    """Peer-mapped replicas of one assignment across the ranks of a process group."""
+
+    def __init__(self, assignment, rank: int, world: int, device, all_gather,
+                 dtype=torch.float32, shadows: bool = True, max_grid: int | None = None,
+                 timeout_cycles: int = 20_000_000_000):
+        self.assignment = assignment
+        self.layout = rank_layout(assignment.n_workers, world, rank)
+        self.device = torch.device(device)
+        d = assignment.topology.total
+        self.replicas = {w: torch.zeros(d, dtype=dtype, device=self.device) for w in self.layout.local_workers}
+        self.shadows = ({w: torch.zeros(d, dtype=torch.bfloat16, device=self.device)
+                         for w in self.layout.local_workers} if shadows else {})
+        self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True, max_grid=max_grid)
+        # every rank must launch the same grid for the pairwise per-CTA barrier
+        self.grid = max(all_gather(self.plan.grid))
+        if self.plan.grid != self.grid:
+            self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True,
+                                 force_grid=self.grid)
+        self.pad = torch.zeros(self.grid * PAD_WORDS_PER_CTA, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._imported: list[int] = []
+        exports = {f"rep{w}": ipc_export(t) for w, t in self.replicas.items()}
+        exports.update({f"sh{w}": ipc_export(t) for w, t in self.shadows.items()})
+        exports["pad"] = ipc_export(self.pad)
+        tables = exchange_handles(exports, all_gather)
+        self.rep_ptr = [0] * assignment.n_workers
+        self.sh_ptr = [0] * assignment.n_workers
+        self.pad_ptr = [0] * world
+        for r, table in enumerate(tables):
+            for key, (h, off) in table.items():
+                if r == rank:
+                    p = {"pad": self.pad.data_ptr()}.get(key)
+                    if p is None:
+                        w = int(key[3:] if key.startswith("rep") else key[2:])
+                        p = (self.replicas if key.startswith("rep") else self.shadows)[w].data_ptr()
+                else:
+                    p = ipc_import(h, off)
+                    self._imported.append(p)
+                if key == "pad":
+                    self.pad_ptr[r] = p
+                elif key.startswith("rep"):
+                    self.rep_ptr[int(key[3:])] = p
+                else:
+                    self.sh_ptr[int(key[2:])] = p
+        self.epoch = 0
+        self.args = bind_rank_args(self.plan, N.DTYPE_F32 if dtype == torch.float32 else N.DTYPE_F64,
+                                   self.rep_ptr, self.sh_ptr, self.pad_ptr, self.status.data_ptr(),
+                                   timeout_cycles)
+        self._fn = N.lib().sdp_owner_sync
+
+    def launch(self, stream=None) -> None:
+        """One synchronised owner-subset sync step (asynchronous on the stream)."""
+        self.epoch += 1
+        self.args.epoch = self.epoch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self._fn(C.byref(self.args), C.c_void_p(s.cuda_stream))
+        if rc:
+            N.check(rc, "sdp_owner_sync")
+
+    def check(self) -> None:
+        st = int(self.status.item())
+        if st & N.STATUS_BARRIER_TIMEOUT:
+            raise CudaError(f"rank {self.layout.rank}: cross-GPU barrier timed out (a peer stalled)")
+
+    def close(self) -> None:
+        for p in self._imported:
+            N.call("sdp_ipc_close", C.c_void_p(p))
+        self._imported.clear()
+
+
+def bench_setup(assignment, rank: int, world: int, device):
+    """bench.py --gpus G: peer group with seeded replicas (randn, zero off-mask)."""
+    import torch.distributed as dist
+
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    for peer in range(world):
+        if peer != rank:
+            try:
+                N.call("sdp_enable_peer", peer)
+            except Exception:
+                pass  # IPC mappings enable peer access lazily
+    g = PeerGroup(assignment, rank, world, device, all_gather)
+    pm = assignment.param_masks
+    gen = torch.Generator(device=device)
+    for w, t in g.replicas.items():
+        gen.manual_seed(1000 + w)
+        t.copy_(torch.randn(t.numel(), generator=gen, device=device) * pm[w])
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    own = g.plan.owned_elems
+    nvl = _nvlink_bytes(g.plan, g.layout)
+    meta = {"tiles": g.plan.n_tiles, "grid": g.grid, "tiles_per_cta": g.plan.tiles_per_cta,
+            "roofline": {"nvlink_bytes_per_launch": nvl,
+                         "nvlink_note": "bytes this rank moves over NVLink per launch (peer reads + peer writes)"}}
+    return g.launch, own * 4, own * 10, meta
+
+
+def _nvlink_bytes(plan: SyncPlan, layout: RankLayout) -> int:
+    """Peer bytes the leader moves: 4 B read + 6 B written per non-local owner."""
+    tiles = plan.mine
+    if len(tiles) == 0:
+        return 0
+    lens = (tiles["len_flags"] & N.TILE_LEN_MASK).astype(np.int64)
+    remote = np.zeros(len(tiles), dtype=np.int64)
+    for w in range(layout.n_workers):
+        if int(layout.gpu_of[w]) != layout.rank:
+            remote += ((tiles["owner_bits"] >> np.uint64(w)) & np.uint64(1)).astype(np.int64)
+    return int((lens * remote).sum() * 10)

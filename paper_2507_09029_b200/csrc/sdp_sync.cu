@@ -136,6 +136,9 @@ __device__ __forceinline__ void nesterov_elem(const SyncParams& p, int64_t j, T 
   if (p.theta_bf16) static_cast<__nv_bfloat16*>(p.theta_bf16)[j] = to_bf16(t);
 }
 
+template <typename T>
+__device__ __forceinline__ void emit_scalar(const SyncParams& p, int64_t j, uint64_t m, T mean);
+
 // Scalar path: one element, owner set `m` (partial tiles, unaligned tails).
 template <typename T>
 __device__ __forceinline__ void sync_elem(const SyncParams& p, int64_t j, uint64_t m, uint32_t& st) {
@@ -151,6 +154,12 @@ __device__ __forceinline__ void sync_elem(const SyncParams& p, int64_t j, uint64
       if (!finite(static_cast<const T*>(p.replicas[w])[j])) st |= SDP_STATUS_UNCOVERED_LEAK;
   }
   if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean)) st |= SDP_STATUS_NONFINITE;
+  emit_scalar<T>(p, j, m, mean);
+}
+
+// Epilogue for one element with owner set `m`.
+template <typename T>
+__device__ __forceinline__ void emit_scalar(const SyncParams& p, int64_t j, uint64_t m, T mean) {
   if (p.out) static_cast<T*>(p.out)[j] = mean;
   if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[j] = to_bf16(mean);
   if (p.flags & SDP_SYNC_WRITEBACK) {
@@ -266,57 +275,83 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
 // Mixed tile: per-element owner sets from the owner mask.  A vector is loaded
 // from every worker in the union of its VN elements' owner sets; each element
 // adds only its own owners, in ascending order.
-template <typename T, int MB>
-__device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, uint32_t& st) {
+template <typename T, int MB, int R>
+__device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, uint64_t tile_union,
+                                                uint32_t& st) {
   constexpr int VN = V<T>::N;
   using Vt = typename V<T>::type;
   using M = typename MaskT<MB>::T;
   const M* mask = static_cast<const M*>(p.owner_mask);
-  for (int q = threadIdx.x; q < p.tile / VN; q += kSyncThreads) {
-    const int64_t j = s + static_cast<int64_t>(q) * VN;
-    uint64_t m[VN];
-    uint64_t uni = 0, inter = ~0ull;
+  const int per_round = R * VN * kSyncThreads;
+  for (int r0 = 0; r0 < p.tile; r0 += per_round) {
+    int64_t jv[R];
+    uint64_t m[R][VN];
+    uint64_t vu[R];
+    Vt acc[R];
 #pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      m[e] = static_cast<uint64_t>(__ldg(mask + j + e));
-      uni |= m[e];
-      inter &= m[e];
-    }
-    if (uni == inter) {  // the VN elements agree: vector path
-      Vt acc;
-#pragma unroll
-      for (int e = 0; e < VN; ++e) acc.x[e] = static_cast<T>(0);
-      for (uint64_t b = uni; b; b &= b - 1) {
-        const int w = __ffsll(static_cast<long long>(b)) - 1;
-        Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
-#pragma unroll
-        for (int e = 0; e < VN; ++e) acc.x[e] = add_rn(acc.x[e], g.x[e]);
-      }
-      const int c = __popcll(uni);
-      Vt mean;
+    for (int k = 0; k < R; ++k) {
+      jv[k] = s + r0 + (k * kSyncThreads + threadIdx.x) * VN;
+      vu[k] = 0;
 #pragma unroll
       for (int e = 0; e < VN; ++e) {
-        mean.x[e] = div_rn(acc.x[e], static_cast<T>(c > 0 ? c : 1));
-        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+        m[k][e] = static_cast<uint64_t>(__ldg(mask + jv[k] + e));
+        vu[k] |= m[k][e];
+        acc[k].x[e] = static_cast<T>(0);
       }
-      if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
-        for (int w = 0; w < p.n_workers; ++w) {
-          Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
+    }
+    // Owners of the whole tile in ascending order, two at a time; a vector is
+    // fetched from worker w only if one of its elements is owned by w, and an
+    // element adds only its own owners -- so the per-element order is exact.
+    uint64_t b = tile_union;
+    while (b) {
+      const int w0 = __ffsll(static_cast<long long>(b)) - 1;
+      b &= b - 1;
+      const bool two = b != 0;
+      const int w1 = two ? __ffsll(static_cast<long long>(b)) - 1 : w0;
+      if (two) b &= b - 1;
+      const T* g0 = static_cast<const T*>(p.replicas[w0]);
+      const T* g1 = static_cast<const T*>(p.replicas[w1]);
+      Vt a[R], c[R];
 #pragma unroll
-          for (int e = 0; e < VN; ++e)
-            if (!finite(g.x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
+      for (int k = 0; k < R; ++k) {
+        if ((vu[k] >> w0) & 1ull) a[k] = V<T>::ld(g0 + jv[k]);
+        if (two && ((vu[k] >> w1) & 1ull)) c[k] = V<T>::ld(g1 + jv[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          if ((m[k][e] >> w0) & 1ull) acc[k].x[e] = add_rn(acc[k].x[e], a[k].x[e]);
+          if (two && ((m[k][e] >> w1) & 1ull)) acc[k].x[e] = add_rn(acc[k].x[e], c[k].x[e]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      Vt mean;
+      uint64_t inter = ~0ull;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        const int cnt = __popcll(m[k][e]);
+        mean.x[e] = div_rn(acc[k].x[e], static_cast<T>(cnt > 0 ? cnt : 1));
+        inter &= m[k][e];
+        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+        if (cnt == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+          for (int w = 0; w < p.n_workers; ++w)
+            if (!finite(static_cast<const T*>(p.replicas[w])[jv[k] + e])) st |= SDP_STATUS_UNCOVERED_LEAK;
         }
       }
-      emit_vec<T>(p, j, uni, mean);
-    } else {
+      if (inter == vu[k]) {
+        emit_vec<T>(p, jv[k], vu[k], mean);  // the VN elements share one owner set
+      } else {
 #pragma unroll
-      for (int e = 0; e < VN; ++e) sync_elem<T>(p, j + e, m[e], st);
+        for (int e = 0; e < VN; ++e) emit_scalar<T>(p, jv[k] + e, m[k][e], mean.x[e]);
+      }
     }
   }
 }
 
 template <typename T, int MB, int R>
-__global__ void __launch_bounds__(kSyncThreads)
+__global__ void __launch_bounds__(kSyncThreads, 4)
 k_owner_sync(const __grid_constant__ SyncParams p) {
   __shared__ alignas(16) sdp_tile_desc s_desc[kStage];
   __shared__ alignas(8) uint64_t s_bar;
@@ -348,7 +383,7 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
       const bool uniform = (d.len_flags & SDP_TILE_UNIFORM) != 0;
       if (len == p.tile) {
         if (uniform) sync_uniform_tile<T, R>(p, s, d.owner_bits, st);
-        else sync_mixed_tile<T, MB>(p, s, st);
+        else sync_mixed_tile<T, MB, (R > 2 ? 2 : R)>(p, s, d.owner_bits, st);
       } else {
         const typename MaskT<MB>::T* mask = static_cast<const typename MaskT<MB>::T*>(p.owner_mask);
         for (int e = threadIdx.x; e < len; e += kSyncThreads) {
@@ -400,8 +435,8 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   const int mb = a->mask_bytes;
   if (!(mb == 1 || mb == 2 || mb == 4 || mb == 8) || mb * 8 < a->n_workers)
     return set_error(SDP_ERR_CONFIG, "mask_bytes=%d cannot hold %d workers", mb, a->n_workers);
-  if (a->tile < 4096 || a->tile % 4096 || a->tile > (1 << 20))
-    return set_error(SDP_ERR_CONFIG, "sync tile must be a multiple of 4096 in [4096, 2^20]");
+  if (a->tile < 1024 || a->tile % 1024 || a->tile > (1 << 20))
+    return set_error(SDP_ERR_CONFIG, "sync tile must be a multiple of 1024 in [1024, 2^20]");
   if (a->n_tiles < 0 || a->tiles_per_cta < 1) return set_error(SDP_ERR_CONFIG, "bad tile plan");
   if (a->world < 1 || a->world > 8 || a->rank < 0 || a->rank >= a->world)
     return set_error(SDP_ERR_CONFIG, "rank %d / world %d invalid (world <= 8)", a->rank, a->world);
@@ -454,8 +489,17 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
 
   const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
   cudaStream_t s = as_stream(stream);
-  // R vectors per thread per round: a 4096-element fp32 tile = 4 float4/thread.
-#define SDP_SYNC_LAUNCH(T, MB) k_owner_sync<T, MB, 4><<<grid, kSyncThreads, 0, s>>>(p)
+  // R vectors of 16 B per thread per round: R = 4 for 4096-element fp32 tiles,
+  // smaller tiles (shorter tail on small buffers) run R = 2 or 1.
+  const int vn = a->dtype == SDP_DTYPE_F32 ? 4 : 2;
+  const int rounds = a->tile / (vn * kSyncThreads);
+  const int R = rounds % 4 == 0 ? 4 : (rounds % 2 == 0 ? 2 : 1);
+#define SDP_SYNC_LAUNCH(T, MB)                                                    \
+  switch (R) {                                                                    \
+    case 4: k_owner_sync<T, MB, 4><<<grid, kSyncThreads, 0, s>>>(p); break;       \
+    case 2: k_owner_sync<T, MB, 2><<<grid, kSyncThreads, 0, s>>>(p); break;       \
+    default: k_owner_sync<T, MB, 1><<<grid, kSyncThreads, 0, s>>>(p); break;      \
+  }
   if (a->dtype == SDP_DTYPE_F32) {
     switch (mb) {
       case 1: SDP_SYNC_LAUNCH(float, 1); break;

@@ -27,7 +27,8 @@ from . import _native as N
 from ._device import device, ptr, sdp_dtype, stream_ptr, upload_struct
 from .errors import NumericalError, ProtocolError, UsageError
 
-TILE = 4096              # elements per sync tile (16 KB of fp32 per replica)
+TILE = 2048              # elements per sync tile (8 KB of fp32 per replica); measured
+                         # best on B200 for 11M..268M buffers (tools/sync_probe.py)
 TILE_DTYPE = np.dtype([("owner_bits", "<u8"), ("tile_index", "<u4"), ("len_flags", "<u4")])
 CTAS_PER_SM = 4          # 64 regs x 256 threads -> 4 resident CTAs per SM
 
@@ -96,7 +97,8 @@ class SyncPlan:
     """
 
     def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int = TILE,
-                 resident: bool = False):
+                 resident: bool = False, max_grid: int | None = None,
+                 force_grid: int | None = None):
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
@@ -118,20 +120,18 @@ class SyncPlan:
         self.n_tiles = len(mine)
         # every CTA must be co-resident for the cross-rank flag barrier
         self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1)
+        if max_grid:
+            self.grid = max(1, min(self.grid, max_grid))
+        if force_grid:
+            self.grid = int(force_grid)  # all ranks launch the same grid (pairwise barrier)
         self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
+        self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
-        self.owned_elems = self._owned_elems(mine)
-
-    def _owned_elems(self, tiles) -> int:
-        """sum over this rank's tiles of |O_j| elements (exact for uniform tiles)."""
-        if len(tiles) == 0:
-            return 0
-        lens = (tiles["len_flags"] & N.TILE_LEN_MASK).astype(np.int64)
-        bits = tiles["owner_bits"]
-        pop = np.zeros(len(tiles), dtype=np.int64)
-        for b in range(64):
-            pop += ((bits >> np.uint64(b)) & np.uint64(1)).astype(np.int64)
-        return int((lens * pop).sum())
+        # exact sum of |O_j| over this rank's elements (per-tile coverage sums)
+        padded = torch.zeros(max(1, n_tiles) * tile, dtype=torch.int64, device=dev)
+        padded[:d] = assignment.coverage
+        self.tile_owned = padded.view(-1, tile).sum(dim=1).cpu().numpy()
+        self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
     def args(self, dtype: int) -> N.SyncArgs:
         a = self.assignment
