@@ -1,0 +1,427 @@
+"""Extraction / write-back behind the reference's model API (models.py:147-382).
+
+    masked_forward(model, worker, xs, ys, block_mode="skip", record=True,
+                   layout="full") -> (loss, tape, params)
+    flat_gradient(model, tape, loss, params) -> flat [d] gradient
+
+layout="full" is the reference's semantics: the worker's parameters are
+theta * mask over the full tensors (models.py:355), extracted by libsdp's
+`sdp_masked_extract`; dropped blocks are skipped ("skip") or scaled by zero
+("multiply"), inactive channels leave the active-channel GroupNorm as exact
+zeros (ops.py:140-204).
+
+layout="compact" runs the worker's structurally smaller subnetwork: the live
+rows/columns of every weight are gathered into one contiguous compact buffer
+(`sdp_gather_slices`), the forward/backward runs dense cuDNN/cuBLAS on the
+compact tensors with ragged per-group GroupNorm statistics, and
+flat_gradient scatters the compact gradient back into the flat [d] layout with
+zeros elsewhere (`sdp_scatter_slices`).  Both layouts give the same loss and
+gradient; the forward/backward math itself is torch (dense
+GEMMs, not the optimisation target).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _native as N
+from ._device import device, ptr, sdp_dtype, stream_ptr
+from .errors import ConfigError, InputError
+from .topology import GlobalModel
+from . import zoo
+
+
+# ---------------------------------------------------------------------------
+# group norm over active channels (ops.py:140-204)
+# ---------------------------------------------------------------------------
+
+def _group_norm_by_membership(x: torch.Tensor, member: torch.Tensor, gamma: torch.Tensor,
+                              beta: torch.Tensor, eps: float) -> torch.Tensor:
+    """x [B, C, H, W]; member [C, G] 0/1: statistics of group g over its member
+    channels only.  Non-member channels produce 0."""
+    b, c, h, w = x.shape
+    m = member.to(x.dtype)
+    count = m.sum(dim=0) * (h * w)                                  # [G]
+    s = x.sum(dim=(2, 3)) @ m                                       # [B, G]
+    mean = s / count
+    xc = x - (mean @ m.t())[:, :, None, None]
+    var = (xc * xc).sum(dim=(2, 3)) @ m / count
+    inv = 1.0 / torch.sqrt(var + eps)
+    xhat = xc * (inv @ m.t())[:, :, None, None]
+    live = (m.sum(dim=1) > 0)[None, :, None, None]
+    return torch.where(live, xhat * gamma[None, :, None, None] + beta[None, :, None, None],
+                       torch.zeros((), dtype=x.dtype, device=x.device))
+
+
+def active_group_norm(x, groups: int, gamma, beta, active: torch.Tensor, eps: float = 1e-5):
+    c = x.shape[1]
+    if c % groups:
+        raise ConfigError(f"group_norm: {groups} groups do not divide {c} channels")
+    gsize = c // groups
+    member = F.one_hot(torch.arange(c, device=x.device) // gsize, groups) * active.to(torch.long)[:, None]
+    if bool((member.sum(dim=0) == 0).any()):
+        raise ConfigError("group_norm: a group has no active channels")
+    return _group_norm_by_membership(x, member, gamma, beta, eps)
+
+
+def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: float = 1e-5):
+    """Compact channels, each tagged with its original norm group (F4: ragged)."""
+    member = F.one_hot(group_of.to(torch.long), groups)
+    return _group_norm_by_membership(x, member, gamma, beta, eps)
+
+
+# ---------------------------------------------------------------------------
+# architectures (same constructor arguments as models.py:45-267)
+# ---------------------------------------------------------------------------
+
+class MiniResNet:
+    def __init__(self, channels, blocks, classes, norm_groups=2, in_channels=3, image_hw=(8, 8)):
+        if blocks < 1:
+            raise ConfigError(f"mini resnet needs at least one block, got {blocks}")
+        if channels % norm_groups:
+            raise ConfigError(f"{norm_groups} norm groups do not divide {channels} channels")
+        self.channels, self.blocks, self.classes = channels, blocks, classes
+        self.norm_groups, self.in_channels, self.image_hw = norm_groups, in_channels, tuple(image_hw)
+
+    def build_topology(self):
+        return zoo.mini_resnet_topology(self.channels, self.blocks, self.classes, self.norm_groups,
+                                        self.in_channels, self.image_hw)
+
+    def forward(self, params, x, worker=None, block_mode="skip"):
+        g = self.norm_groups
+        ones = torch.ones(self.channels, dtype=torch.bool, device=x.device)
+        h = F.conv2d(x, params["stem.w"], params["stem.b"], padding=1)
+        h = F.relu(active_group_norm(h, g, params["stem_gn.gamma"], params["stem_gn.beta"], ones))
+        for i in range(self.blocks):
+            live = True if worker is None else bool(worker.block_active[i])
+            if not live and block_mode == "skip":
+                continue
+            a1 = _flags(worker, f"block{i}.conv1", ones)
+            a2 = _flags(worker, f"block{i}.conv2", ones)
+            hb = F.conv2d(h, params[f"block{i}.conv1.w"], params[f"block{i}.conv1.b"], padding=1)
+            hb = F.relu(active_group_norm(hb, g, params[f"block{i}.gn1.gamma"], params[f"block{i}.gn1.beta"], a1))
+            hb = F.conv2d(hb, params[f"block{i}.conv2.w"], params[f"block{i}.conv2.b"], padding=1)
+            hb = active_group_norm(hb, g, params[f"block{i}.gn2.gamma"], params[f"block{i}.gn2.beta"], a2)
+            if not live:
+                hb = hb * 0.0
+            h = h + hb
+        return F.linear(h.mean(dim=(2, 3)), params["head.w"], params["head.b"])
+
+    def forward_compact(self, cp, x, sub):
+        """Compact subnetwork: cp holds only live rows/columns (SubnetLayout)."""
+        g = self.norm_groups
+        gsize = self.channels // g
+        ones = torch.ones(self.channels, dtype=torch.bool, device=x.device)
+        h = F.conv2d(x, cp["stem.w"], cp["stem.b"], padding=1)
+        h = F.relu(active_group_norm(h, g, cp["stem_gn.gamma"], cp["stem_gn.beta"], ones))
+        for i in range(self.blocks):
+            if not sub.present(f"block{i}.conv1.w"):
+                continue  # dropped block: never executed (models.py:161-163)
+            a1 = sub.channels(f"block{i}.conv1", self.channels)
+            a2 = sub.channels(f"block{i}.conv2", self.channels)
+            hb = F.conv2d(h, cp[f"block{i}.conv1.w"], cp[f"block{i}.conv1.b"], padding=1)
+            hb = F.relu(ragged_group_norm(hb, a1 // gsize, g, cp[f"block{i}.gn1.gamma"], cp[f"block{i}.gn1.beta"]))
+            hb = F.conv2d(hb, cp[f"block{i}.conv2.w"], cp[f"block{i}.conv2.b"], padding=1)
+            hb = ragged_group_norm(hb, a2 // gsize, g, cp[f"block{i}.gn2.gamma"], cp[f"block{i}.gn2.beta"])
+            h = h.index_add(1, a2, hb)
+        return F.linear(h.mean(dim=(2, 3)), cp["head.w"], cp["head.b"])
+
+
+class ResidualMLP:
+    def __init__(self, width, blocks, classes, in_dim=16):
+        if blocks < 1:
+            raise ConfigError(f"residual mlp needs at least one block, got {blocks}")
+        self.width, self.blocks, self.classes, self.in_dim = width, blocks, classes, in_dim
+
+    def build_topology(self):
+        return zoo.residual_mlp_topology(self.width, self.blocks, self.classes, self.in_dim)
+
+    def forward(self, params, x, worker=None, block_mode="skip"):
+        h = F.relu(F.linear(x, params["stem.w"], params["stem.b"]))
+        for i in range(self.blocks):
+            live = True if worker is None else bool(worker.block_active[i])
+            if not live and block_mode == "skip":
+                continue
+            hb = F.relu(F.linear(h, params[f"block{i}.lin1.w"], params[f"block{i}.lin1.b"]))
+            hb = F.linear(hb, params[f"block{i}.lin2.w"], params[f"block{i}.lin2.b"])
+            if not live:
+                hb = hb * 0.0
+            h = h + hb
+        return F.linear(h, params["head.w"], params["head.b"])
+
+    def forward_compact(self, cp, x, sub):
+        h = F.relu(F.linear(x, cp["stem.w"], cp["stem.b"]))
+        for i in range(self.blocks):
+            if not sub.present(f"block{i}.lin1.w"):
+                continue
+            hb = F.relu(F.linear(h, cp[f"block{i}.lin1.w"], cp[f"block{i}.lin1.b"]))
+            h = h + F.linear(hb, cp[f"block{i}.lin2.w"], cp[f"block{i}.lin2.b"])
+        return F.linear(h, cp["head.w"], cp["head.b"])
+
+
+def _flags(worker, layer_id, ones):
+    if worker is None or layer_id not in worker.channel_active:
+        return ones
+    return torch.as_tensor(np.array(worker.channel_active[layer_id], dtype=bool), device=ones.device)
+
+
+def _make_global(arch, theta: torch.Tensor | None, dtype, dev) -> GlobalModel:
+    topo = arch.build_topology()
+    if theta is None:
+        theta = torch.zeros(topo.total, dtype=dtype, device=dev)
+    return GlobalModel(arch=arch, topology=topo, theta=theta)
+
+
+def build_mini_resnet(channels, blocks, classes, norm_groups=2, in_channels=3, image_hw=(8, 8),
+                      seed=0, dtype=torch.float32, device_=None, theta=None) -> GlobalModel:
+    m = _make_global(MiniResNet(channels, blocks, classes, norm_groups, in_channels, image_hw),
+                     theta, dtype, device(device_))
+    if theta is None:
+        m.theta = kaiming_fan_out_init(m, None, seed)
+    return m
+
+
+def build_residual_mlp(width, blocks, classes, in_dim=16, seed=0, dtype=torch.float32,
+                       device_=None, theta=None) -> GlobalModel:
+    m = _make_global(ResidualMLP(width, blocks, classes, in_dim), theta, dtype, device(device_))
+    if theta is None:
+        m.theta = kaiming_fan_out_init(m, None, seed)
+    return m
+
+
+def kaiming_fan_out_init(model: GlobalModel, assignment, seed: int) -> torch.Tensor:
+    """masked_kaiming_init's rule (models.py:270-298): N(0, 2/fan_out_active) for
+    weights, gamma = 1, bias/beta = 0.  Drawn with torch's device generator, so
+    the values (not the distribution) differ from the reference's numpy draw."""
+    t = model.theta
+    gen = torch.Generator(device=t.device)
+    gen.manual_seed(int(seed))
+    theta = torch.zeros_like(t)
+    for spec in model.topology.params:
+        sl = slice(spec.offset, spec.offset + spec.size)
+        if spec.kind == "conv_w":
+            fan_out = spec.shape[0] * spec.shape[2] * spec.shape[3]
+        elif spec.kind == "linear_w":
+            fan_out = spec.shape[0]
+        elif spec.kind in ("gamma", "norm_w"):
+            theta[sl] = 1.0
+            continue
+        else:
+            continue
+        frac = 1.0 if assignment is None else assignment.output_fraction(spec.layer_id)
+        std = math.sqrt(2.0 / max(1, round(fan_out * frac)))
+        theta[sl] = torch.randn(spec.size, generator=gen, device=t.device, dtype=t.dtype) * std
+    return theta
+
+
+# ---------------------------------------------------------------------------
+# compact subnetwork layout (gather / scatter descriptor tables)
+# ---------------------------------------------------------------------------
+
+SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("full_shape", "<i8", 4),
+                        ("compact_shape", "<i8", 4), ("map_offset", "<i4", 4), ("ndim", "<i4"),
+                        ("pad_", "<i4")])
+
+
+class SubnetLayout:
+    """One worker's compact subnetwork: for every parameter the live index set
+    along each governed axis (own/consumer slices, masking.py:140-149) or, for
+    block masking, presence of the whole tensor (masking.py:160-169)."""
+
+    def __init__(self, assignment, worker: int):
+        topo = assignment.topology
+        self.topology = topo
+        self.worker = worker
+        dev = assignment.device
+        view = assignment.worker_view(worker)
+        self.view = view
+        # live channel indices per layer (neuron) / live blocks (block)
+        live_ch: dict[str, np.ndarray] = {}
+        axes: dict[str, dict[int, str]] = {p.name: {} for p in topo.params}
+        present = {p.name: True for p in topo.params}
+        if assignment.strategy == "neuron":
+            for layer in topo.channel_layers:
+                if not layer.maskable:
+                    continue
+                live_ch[layer.layer_id] = np.nonzero(view.channel_active[layer.layer_id])[0]
+                for pname, axis in tuple(layer.own_slices) + tuple(layer.consumer_slices):
+                    if axis in axes[pname]:
+                        raise ConfigError(f"{pname} axis {axis} governed twice")
+                    axes[pname][axis] = layer.layer_id
+        else:
+            for b in topo.blocks:
+                if b.maskable and not view.block_active[b.index]:
+                    for pname in b.param_names:
+                        present[pname] = False
+        self.live_channels = {k: torch.as_tensor(v, dtype=torch.long, device=dev) for k, v in live_ch.items()}
+        self.present_map = present
+        # forward / inverse index maps, one pair per layer
+        fwd, inv, fwd_off, inv_off = [], [], {}, {}
+        for lid, idx in live_ch.items():
+            layer = topo.channel_layer(lid)
+            fwd_off[lid] = sum(len(a) for a in fwd)
+            fwd.append(idx.astype(np.int32))
+            m = np.full(layer.channels, -1, dtype=np.int32)
+            m[idx] = np.arange(len(idx), dtype=np.int32)
+            inv_off[lid] = sum(len(a) for a in inv)
+            inv.append(m)
+        descs = np.zeros(len(topo.params), dtype=SLICE_DTYPE)
+        self.shapes: dict[str, tuple[int, ...]] = {}
+        self.offsets: dict[str, int] = {}
+        imaps: list[list[int]] = []
+        pos = 0
+        for i, p in enumerate(topo.params):
+            shape = list(p.shape)
+            cshape = list(p.shape)
+            fmap, imap = [-1] * 4, [-1] * 4
+            for axis, lid in axes[p.name].items():
+                cshape[axis] = len(live_ch[lid])
+                fmap[axis] = fwd_off[lid]
+                imap[axis] = inv_off[lid]
+            if not present[p.name]:
+                cshape[0] = 0
+            n = int(np.prod(cshape)) if cshape else 1
+            nd = len(shape)
+            if nd > 4:
+                raise ConfigError(f"{p.name}: at most 4 dims supported")
+            descs[i]["full_offset"] = p.offset
+            descs[i]["compact_offset"] = pos
+            descs[i]["full_shape"][:nd] = shape
+            descs[i]["full_shape"][nd:] = 1
+            descs[i]["compact_shape"][:nd] = cshape
+            descs[i]["compact_shape"][nd:] = 1
+            descs[i]["ndim"] = nd
+            descs[i]["map_offset"] = fmap
+            self.shapes[p.name] = tuple(cshape)
+            self.offsets[p.name] = pos
+            pos += n
+            imaps.append(imap)  # the scatter side reads the inverse maps, same axis slots
+        self.compact_total = pos
+        self.descs_fwd = descs
+        descs_inv = descs.copy()
+        for i, imap in enumerate(imaps):
+            descs_inv[i]["map_offset"] = imap
+        from ._device import upload_struct
+        self.d_fwd = upload_struct(descs, dev)
+        self.d_inv = upload_struct(descs_inv, dev)
+        fw = np.concatenate(fwd) if fwd else np.zeros(1, np.int32)
+        iv = np.concatenate(inv) if inv else np.zeros(1, np.int32)
+        self.fwd_maps = torch.from_numpy(fw.astype(np.int32)).to(dev)
+        self.inv_maps = torch.from_numpy(iv.astype(np.int32)).to(dev)
+        self.n_descs = len(descs)
+
+    def present(self, name: str) -> bool:
+        return self.present_map[name] and int(np.prod(self.shapes[name])) > 0
+
+    def channels(self, layer_id: str, c: int) -> torch.Tensor:
+        t = self.live_channels.get(layer_id)
+        if t is None:
+            return torch.arange(c, device=self.fwd_maps.device)
+        return t
+
+    def views(self, compact: torch.Tensor) -> dict:
+        return {p.name: compact[self.offsets[p.name]:self.offsets[p.name] + int(np.prod(self.shapes[p.name]))]
+                .view(self.shapes[p.name]) for p in self.topology.params}
+
+    # -- kernels --------------------------------------------------------------
+    def gather(self, theta: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Full theta -> compact buffer (sdp_gather_slices)."""
+        if out is None:
+            out = torch.empty(max(1, self.compact_total), dtype=theta.dtype, device=theta.device)
+        N.call("sdp_gather_slices", sdp_dtype(theta.dtype), ptr(self.d_fwd), self.n_descs,
+               ptr(self.fwd_maps), ptr(theta), ptr(out), self.compact_total, stream_ptr(theta.device))
+        return out
+
+    def scatter(self, compact: torch.Tensor, full: torch.Tensor | None = None,
+                accumulate: bool = False) -> torch.Tensor:
+        """Compact gradient -> flat [d] (zero elsewhere), or += into `full`."""
+        d = self.topology.total
+        if full is None:
+            full = torch.empty(d, dtype=compact.dtype, device=compact.device)
+            accumulate = False
+        flags = N.SCATTER_ACCUMULATE if accumulate else N.SCATTER_ZERO_FILL
+        N.call("sdp_scatter_slices", sdp_dtype(compact.dtype), ptr(self.d_inv), self.n_descs,
+               ptr(self.inv_maps), ptr(compact), ptr(full), 0, d, flags, stream_ptr(compact.device))
+        return full
+
+
+# ---------------------------------------------------------------------------
+# reference-facing entry points
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Tape:
+    """What flat_gradient needs from masked_forward (the reference's tape role)."""
+    leaf: torch.Tensor
+    layout: SubnetLayout | None
+
+
+def _extract(theta: torch.Tensor, worker) -> torch.Tensor:
+    """theta * mask (models.py:355) via sdp_masked_extract on the worker's byte mask."""
+    out = torch.empty_like(theta)
+    mask = worker.param_mask_bool.view(torch.uint8)
+    N.call("sdp_masked_extract", sdp_dtype(theta.dtype), ptr(theta), ptr(mask), 1, theta.numel(), 0,
+           ptr(out), stream_ptr(theta.device))
+    return out
+
+
+def masked_forward(model: GlobalModel, worker, xs, ys, block_mode: str = "skip",
+                   record: bool = True, layout: str = "full", subnet: SubnetLayout | None = None):
+    """One loss evaluation on the worker's subnetwork (models.py:333-366)."""
+    topo = model.topology
+    xs = torch.as_tensor(xs, device=model.theta.device)
+    if tuple(xs.shape[1:]) != tuple(topo.input_shape):
+        raise InputError(f"batch shape {tuple(xs.shape[1:])} does not match model input {topo.input_shape}")
+    if block_mode not in ("skip", "multiply"):
+        raise ConfigError(f"unknown block_mode {block_mode!r}")
+    ys = torch.as_tensor(ys, device=model.theta.device, dtype=torch.long)
+    xs = xs.to(model.theta.dtype)
+    if layout == "compact":
+        if subnet is None:
+            raise ConfigError("layout='compact' needs the worker's SubnetLayout")
+        leaf = subnet.gather(model.theta).requires_grad_(record)
+        cp = subnet.views(leaf)
+        logits = model.arch.forward_compact(cp, xs, subnet)
+        loss = F.cross_entropy(logits, ys)
+        return loss, Tape(leaf, subnet), cp
+    if layout != "full":
+        raise ConfigError(f"unknown layout {layout!r}")
+    theta = model.theta if worker is None else _extract(model.theta, worker)
+    leaf = theta.detach().requires_grad_(record)
+    params = {p.name: leaf[p.offset:p.offset + p.size].view(p.shape) for p in topo.params}
+    logits = model.arch.forward(params, xs, worker, block_mode)
+    loss = F.cross_entropy(logits, ys)
+    return loss, Tape(leaf, None), params
+
+
+def aggregate_compact(compact_grads, layouts, assignment) -> torch.Tensor:
+    """engine.aggregate over compact per-worker gradients: each worker's compact
+    gradient is scatter-ACCUMULATED into one [d] buffer in ascending worker id
+    (exactly the reference's num += m_i * g_i order, engine.py:71-73), then
+    divided by the divisor (engine.py:74) -- no [d] gradient per worker."""
+    d = assignment.topology.total
+    dt = compact_grads[0].dtype
+    acc = torch.zeros(d, dtype=dt, device=assignment.device)
+    for g, lay in sorted(zip(compact_grads, layouts), key=lambda x: x[1].worker):
+        lay.scatter(g, acc, accumulate=True)
+    out = torch.empty_like(acc)
+    N.call("sdp_divide", sdp_dtype(dt), ptr(acc), ptr(assignment.divisor), d, ptr(out),
+           stream_ptr(assignment.device))
+    return out
+
+
+def flat_gradient(model: GlobalModel, tape: Tape, loss, params) -> torch.Tensor:
+    """Backward pass assembled into a vector aligned with the flat theta
+    (models.py:369-382): entries of dropped / dead parameters are exactly 0."""
+    (g,) = torch.autograd.grad(loss, tape.leaf, allow_unused=True)
+    if g is None:
+        g = torch.zeros_like(tape.leaf)
+    if tape.layout is None:
+        return g
+    return tape.layout.scatter(g.contiguous())
