@@ -88,9 +88,11 @@ typedef struct {
  * product of the trailing dims, dim the axis length) or, with inner = dim = 1,
  * a whole block (masking.py:167-169). */
 typedef struct {
-  int64_t inner;
-  int64_t dim;
+  int32_t inner;
+  int32_t dim;
   int32_t unit_base;
+  uint32_t inner_mul, inner_shr; /* q = umulhi(e, mul) >> shr == e / inner (e < 2^31) */
+  uint32_t dim_mul, dim_shr;     /* same for / dim; mul = 0 encodes a divisor of 1 */
   int32_t pad_;
 } sdp_rule_desc;
 
@@ -227,35 +229,54 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask,
                        int mask_bytes, int64_t total, int worker, void* out,
                        void* stream);
 
-/* One compact sub-tensor of a width-wise subnetwork. Up to 4 dims; each dim
- * either keeps all indices (map_offset = -1) or the listed ones:
- *   fwd_maps[map_offset + c] = full index of compact index c   (gather)
- *   inv_maps[map_offset + f] = compact index of full index f, or -1 (scatter) */
+/* One parameter tensor of a width-wise subnetwork in canonical 3-D form: the
+ * full tensor is viewed as [rows, cols, inner] (inner = the contiguous
+ * trailing dims no slice governs), its compact sub-tensor as
+ * [crows, ccols, inner]; rows and/or cols are selected through index maps
+ * (masking.py:140-149 own slices = rows, consumer slices = cols):
+ *   fwd_maps[row_map + r] = full row of compact row r          (gather)
+ *   inv_maps[row_map + f] = compact row of full row f, or -1   (scatter)
+ * and the same for columns; a map offset of -1 is the identity.  crows = 0
+ * marks a tensor the worker does not hold (a dropped block).
+ * inner_mul / inner_shr: fast division by inner, q = umulhi(n, mul) >> shr
+ * (valid for n < 2^31; mul = 0, shr = 0 when inner == 1). */
 typedef struct {
   int64_t full_offset;
   int64_t compact_offset;
-  int64_t full_shape[4];
-  int64_t compact_shape[4];
-  int32_t map_offset[4];
-  int32_t ndim;
+  int32_t rows, cols, inner;
+  int32_t crows, ccols;
+  int32_t row_map, col_map;
+  uint32_t inner_mul;
+  uint32_t inner_shr;
+  uint32_t rowlen_mul;  /* fast division by the row length the kernel walks: */
+  uint32_t rowlen_shr;  /* ccols*inner (gather table), cols*inner (scatter) */
   int32_t pad_;
 } sdp_slice_desc;
 
-/* compact[k] = full[src(k)] for every element of every descriptor. */
-int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, int n_descs,
-                      const int32_t* fwd_maps, const void* full, void* compact,
-                      int64_t compact_total, void* stream);
+/* A unit of work of the gather/scatter kernels: rows [row_begin, row_end) of
+ * descriptor `desc` (compact rows for gather, full rows for scatter), and
+ * within each of those rows the elements [elem_begin, elem_end). */
+typedef struct {
+  int32_t desc;
+  int32_t row_begin, row_end;
+  int32_t elem_begin, elem_end;
+  int32_t pad_[3];
+} sdp_slice_task;
+
+/* compact[...] = full[...] over every task (one CTA per task). */
+int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                      int n_tasks, const int32_t* fwd_maps, const void* full,
+                      void* compact, void* stream);
 
 #define SDP_SCATTER_ZERO_FILL 0x1  /* full[j] = 0 where no compact element maps */
 #define SDP_SCATTER_ACCUMULATE 0x2 /* full[j] += compact[...] instead of = */
 
-/* Write compact grads back into the flat layout (models.py:376-381).
- * Iterates over the FULL elements in [full_lo, full_hi) (coalesced stores);
- * descriptors must be sorted by full_offset and disjoint; elements outside
- * every descriptor are left untouched. */
-int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, int n_descs,
-                       const int32_t* inv_maps, const void* compact, void* full,
-                       int64_t full_lo, int64_t full_hi, int flags, void* stream);
+/* Write compact grads back into the flat layout (models.py:376-381): tasks
+ * cover FULL rows (coalesced stores, every covered full element written once
+ * in ZERO_FILL mode; in ACCUMULATE mode only mapped elements are touched). */
+int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                       int n_tasks, const int32_t* inv_maps, const void* compact, void* full,
+                       int flags, void* stream);
 
 /* out[j] = acc[j] / divisor[j] in dtype (the engine.py:74 divide after an
  * owner-ordered scatter-accumulate).  divisor is float64 [d]. */

@@ -49,8 +49,9 @@ class ParamDesc(C.Structure):
 
 
 class RuleDesc(C.Structure):
-    _fields_ = [("inner", C.c_int64), ("dim", C.c_int64),
-                ("unit_base", C.c_int32), ("pad_", C.c_int32)]
+    _fields_ = [("inner", C.c_int32), ("dim", C.c_int32), ("unit_base", C.c_int32),
+                ("inner_mul", C.c_uint32), ("inner_shr", C.c_uint32),
+                ("dim_mul", C.c_uint32), ("dim_shr", C.c_uint32), ("pad_", C.c_int32)]
 
 
 class TileDesc(C.Structure):
@@ -60,8 +61,17 @@ class TileDesc(C.Structure):
 
 class SliceDesc(C.Structure):
     _fields_ = [("full_offset", C.c_int64), ("compact_offset", C.c_int64),
-                ("full_shape", C.c_int64 * 4), ("compact_shape", C.c_int64 * 4),
-                ("map_offset", C.c_int32 * 4), ("ndim", C.c_int32), ("pad_", C.c_int32)]
+                ("rows", C.c_int32), ("cols", C.c_int32), ("inner", C.c_int32),
+                ("crows", C.c_int32), ("ccols", C.c_int32),
+                ("row_map", C.c_int32), ("col_map", C.c_int32),
+                ("inner_mul", C.c_uint32), ("inner_shr", C.c_uint32),
+                ("rowlen_mul", C.c_uint32), ("rowlen_shr", C.c_uint32), ("pad_", C.c_int32)]
+
+
+class SliceTask(C.Structure):
+    _fields_ = [("desc", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
+                ("elem_begin", C.c_int32), ("elem_end", C.c_int32), ("pad_", C.c_int32 * 3)]
+
 
 
 class SyncArgs(C.Structure):
@@ -98,8 +108,8 @@ SIGNATURES = {
     "sdp_owner_sync": (C.c_int, [C.POINTER(SyncArgs), VP]),
     "sdp_nesterov_update": (C.c_int, [I32, I64, VP, VP, VP, DBL, DBL, VP, VP, VP]),
     "sdp_masked_extract": (C.c_int, [I32, VP, VP, I32, I64, I32, VP, VP]),
-    "sdp_gather_slices": (C.c_int, [I32, VP, I32, VP, VP, VP, I64, VP]),
-    "sdp_scatter_slices": (C.c_int, [I32, VP, I32, VP, VP, VP, I64, I64, I32, VP]),
+    "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, VP]),
+    "sdp_scatter_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
     "sdp_divide": (C.c_int, [I32, VP, VP, I64, VP, VP]),
     "sdp_ipc_export": (C.c_int, [VP, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
     "sdp_ipc_import": (C.c_int, [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_void_p)]),

@@ -111,13 +111,20 @@ struct SeedWords {
   int n;
 };
 
+// Workers of slot j: {(j*P + t) mod N : t < P} as a bitmask = the low P bits
+// rotated left by (j*P) mod N inside an N-bit ring (masking.py:63-65).
 __device__ __forceinline__ uint64_t window_bits(uint64_t slot, int n, int p) {
-  uint64_t start = (slot * static_cast<uint64_t>(p)) % static_cast<uint64_t>(n);
-  uint64_t bits = 0;
-  for (int t = 0; t < p; ++t) bits |= 1ull << ((start + t) % n);
-  return bits;
+  const uint64_t full = n == 64 ? ~0ull : ((1ull << n) - 1);
+  const uint64_t low = p == 64 ? ~0ull : ((1ull << p) - 1);
+  const uint32_t start = (static_cast<uint32_t>(slot % static_cast<uint64_t>(n)) * static_cast<uint32_t>(p)) %
+                         static_cast<uint32_t>(n);
+  if (start == 0) return low;
+  return ((low << start) | (low >> (n - start))) & full;
 }
 
+// One CTA.  Thread 0 runs the inherently sequential Fisher-Yates draws of each
+// group (one generator across groups, masking.py:107-116); the whole CTA then
+// writes that group's window masks.
 __global__ void k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups,
                          int n_groups, int n_units, int n_workers, int replication,
                          uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch,
@@ -125,22 +132,26 @@ __global__ void k_assign(SeedWords seed, const sdp_group_desc* __restrict__ grou
   extern __shared__ int32_t s_perm[];
   const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
   for (int u = threadIdx.x; u < n_units; u += blockDim.x) unit_bits[u] = full;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
   Pcg64 g;
-  seed_pcg(g, seed.w, seed.n);
+  if (threadIdx.x == 0) seed_pcg(g, seed.w, seed.n);
   uint64_t slot = 0;
   for (int gi = 0; gi < n_groups; ++gi) {
     const int first = groups[gi].first_unit, size = groups[gi].size;
     int32_t* a = size <= smem_cap ? s_perm : scratch;
-    for (int i = 0; i < size; ++i) a[i] = i;
-    for (int i = size - 1; i > 0; --i) {  // Generator.shuffle (Fisher-Yates)
-      int j = static_cast<int>(g.interval(static_cast<uint64_t>(i)));
-      int32_t t = a[i];
-      a[i] = a[j];
-      a[j] = t;
+    __syncthreads();  // previous group's readers are done with a[]
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < size; ++i) a[i] = i;
+      for (int i = size - 1; i > 0; --i) {  // Generator.shuffle (Fisher-Yates)
+        const int j = static_cast<int>(g.interval(static_cast<uint64_t>(i)));
+        const int32_t t = a[i];
+        a[i] = a[j];
+        a[j] = t;
+      }
     }
-    for (int k = 0; k < size; ++k) unit_bits[first + a[k]] = window_bits(slot++, n_workers, replication);
+    __syncthreads();
+    for (int k = threadIdx.x; k < size; k += blockDim.x)
+      unit_bits[first + a[k]] = window_bits(slot + k, n_workers, replication);
+    slot += size;
   }
 }
 
@@ -163,8 +174,9 @@ __global__ void k_permutation(SeedWords seed, const int32_t* skip_sizes_dev, int
 // ---------------------------------------------------------------------------
 // element expansion
 // ---------------------------------------------------------------------------
-constexpr int kBuildElems = 16;   // elements per thread (one 16-B bool vector per worker row)
 constexpr int kBuildThreads = 256;
+constexpr int kLaneElems = 16;                  // elements per lane per warp chunk
+constexpr int kWarpChunk = 32 * kLaneElems;     // 512 consecutive elements per warp
 
 __device__ __forceinline__ int find_param(const sdp_param_desc* __restrict__ p, int n, int64_t j) {
   int lo = 0, hi = n - 1;  // last param with offset <= j
@@ -175,6 +187,13 @@ __device__ __forceinline__ int find_param(const sdp_param_desc* __restrict__ p, 
   return lo;
 }
 
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t mul, uint32_t shr) {
+  return mul ? (__umulhi(n, mul) >> shr) : n;
+}
+
+// A warp owns 512 consecutive elements; lane l takes elements l, l+32, ... so
+// every store instruction writes 32 consecutive elements (fully coalesced for
+// the 8-B coverage / divisor / governor arrays and the 1-B masks alike).
 template <int MB>
 __global__ void __launch_bounds__(kBuildThreads)
 k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
@@ -185,121 +204,52 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
               unsigned long long* __restrict__ active_counts) {
   using M = typename MaskT<MB>::T;
   const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
-  const int64_t n_chunks = (total + kBuildElems - 1) / kBuildElems;
-  const bool rows_aligned = (total % 16) == 0;
-  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // uniform trip count across the warp so the shuffle reductions stay converged
-    const bool live = c < n_chunks;
-    const int64_t j0 = c * kBuildElems;
-    uint64_t bits[kBuildElems];
-    int gov[kBuildElems];
+  const int lane = threadIdx.x & 31;
+  const int64_t n_chunks = (total + kWarpChunk - 1) / kWarpChunk;
+  const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = warp0; c < n_chunks; c += n_warps) {  // warp-uniform trip count
+    const int64_t base = c * kWarpChunk;
+    int pi = find_param(params, n_params, min(base + lane, total - 1));
+    sdp_param_desc pd = params[pi];
+    uint64_t bits[kLaneElems];
 #pragma unroll
-    for (int e = 0; e < kBuildElems; ++e) bits[e] = 0;
-    int nvalid = 0;
-    if (live) {
-      nvalid = static_cast<int>(min(static_cast<int64_t>(kBuildElems), total - j0));
-      int pi = find_param(params, n_params, j0);
-      int64_t pend = params[pi].offset + params[pi].size;
-#pragma unroll
-      for (int e = 0; e < kBuildElems; ++e) {
-        const int64_t j = j0 + e;
-        bits[e] = 0;
-        gov[e] = 0;
-        if (e < nvalid) {
-          while (j >= pend) {
-            ++pi;
-            pend = params[pi].offset + params[pi].size;
-          }
-          const sdp_param_desc pd = params[pi];
-          const uint32_t le = static_cast<uint32_t>(j - pd.offset);
-          uint64_t b = full;
-          for (int r = 0; r < pd.rule_count; ++r) {
-            const sdp_rule_desc rd = rules[pd.rule_begin + r];
-            const uint32_t u = static_cast<uint32_t>(rd.unit_base) +
-                               (le / static_cast<uint32_t>(rd.inner)) % static_cast<uint32_t>(rd.dim);
-            b &= __ldg(unit_bits + u);
-          }
-          bits[e] = b;
-          gov[e] = pd.rule_count;
-        }
+    for (int e = 0; e < kLaneElems; ++e) {
+      const int64_t j = base + e * 32 + lane;
+      bits[e] = 0;
+      if (j >= total) continue;
+      while (j >= pd.offset + pd.size) pd = params[++pi];
+      const uint32_t le = static_cast<uint32_t>(j - pd.offset);
+      uint64_t b = full;
+      for (int r = 0; r < pd.rule_count; ++r) {
+        const sdp_rule_desc rd = rules[pd.rule_begin + r];
+        const uint32_t q = fdiv(le, rd.inner_mul, rd.inner_shr);
+        const uint32_t u = q - fdiv(q, rd.dim_mul, rd.dim_shr) * static_cast<uint32_t>(rd.dim);
+        b &= __ldg(unit_bits + static_cast<uint32_t>(rd.unit_base) + u);
       }
-      const bool vec = nvalid == kBuildElems;
-      if (owner_mask) {
-        if (vec) {
-          M m[kBuildElems];
-#pragma unroll
-          for (int e = 0; e < kBuildElems; ++e) m[e] = static_cast<M>(bits[e]);
-          const uint4* src = reinterpret_cast<const uint4*>(m);
-          uint4* dst = reinterpret_cast<uint4*>(owner_mask + j0);
-#pragma unroll
-          for (int q = 0; q < kBuildElems * MB / 16; ++q) dst[q] = src[q];
-        } else {
-          for (int e = 0; e < nvalid; ++e) owner_mask[j0 + e] = static_cast<M>(bits[e]);
-        }
-      }
-      if (param_masks) {
-        for (int w = 0; w < n_workers; ++w) {
-          uint8_t* row = param_masks + static_cast<int64_t>(w) * total + j0;
-          if (vec && rows_aligned) {
-            uint32_t wd[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t v = 0;
-#pragma unroll
-              for (int b = 0; b < 4; ++b) v |= static_cast<uint32_t>((bits[q * 4 + b] >> w) & 1ull) << (8 * b);
-              wd[q] = v;
-            }
-            *reinterpret_cast<uint4*>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-          } else {
-            for (int e = 0; e < nvalid; ++e) row[e] = static_cast<uint8_t>((bits[e] >> w) & 1ull);
-          }
-        }
-      }
-      if (coverage || divisor) {
-        for (int e = 0; e < kBuildElems; e += 2) {
-          const int c0 = __popcll(bits[e]), c1 = __popcll(bits[e + 1]);
-          if (vec) {
-            if (coverage) *reinterpret_cast<longlong2*>(coverage + j0 + e) = make_longlong2(c0, c1);
-            if (divisor)
-              *reinterpret_cast<double2*>(divisor + j0 + e) =
-                  make_double2(static_cast<double>(max(c0, 1)), static_cast<double>(max(c1, 1)));
-          } else {
-            if (e < nvalid) {
-              if (coverage) coverage[j0 + e] = c0;
-              if (divisor) divisor[j0 + e] = static_cast<double>(max(c0, 1));
-            }
-            if (e + 1 < nvalid) {
-              if (coverage) coverage[j0 + e + 1] = c1;
-              if (divisor) divisor[j0 + e + 1] = static_cast<double>(max(c1, 1));
-            }
-          }
-        }
-      }
-      if (governors) {
-        for (int e = 0; e < kBuildElems; e += 2) {
-          if (vec) {
-            *reinterpret_cast<longlong2*>(governors + j0 + e) = make_longlong2(gov[e], gov[e + 1]);
-          } else {
-            if (e < nvalid) governors[j0 + e] = gov[e];
-            if (e + 1 < nvalid) governors[j0 + e + 1] = gov[e + 1];
-          }
-        }
-      }
+      bits[e] = b;
+      const int cnt = __popcll(b);
+      if (owner_mask) owner_mask[j] = static_cast<M>(b);
+      if (coverage) coverage[j] = cnt;
+      if (divisor) divisor[j] = static_cast<double>(cnt > 0 ? cnt : 1);
+      if (governors) governors[j] = pd.rule_count;
+      if (param_masks)
+        for (int w = 0; w < n_workers; ++w)
+          param_masks[static_cast<int64_t>(w) * total + j] = static_cast<uint8_t>((b >> w) & 1ull);
     }
     if (active_counts) {
-      // per-worker held-parameter counts: warp-shuffle reduce, one atomic per warp
+      // held-parameter count per worker: warp-shuffle reduce, one atomic per warp
       for (int w = 0; w < n_workers; ++w) {
         unsigned cnt = 0;
 #pragma unroll
-        for (int e = 0; e < kBuildElems; ++e) cnt += static_cast<unsigned>((bits[e] >> w) & 1ull);
+        for (int e = 0; e < kLaneElems; ++e) cnt += static_cast<unsigned>((bits[e] >> w) & 1ull);
         cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(active_counts + w, static_cast<unsigned long long>(cnt));
+        if (lane == 0 && cnt) atomicAdd(active_counts + w, static_cast<unsigned long long>(cnt));
       }
     }
-    // exit once the whole warp is past the end
-    if (!__any_sync(0xffffffffu, c + static_cast<int64_t>(gridDim.x) * blockDim.x < n_chunks)) break;
   }
 }
+
 
 template <int MB>
 __global__ void k_worker_mask(const typename MaskT<MB>::T* __restrict__ owner_mask, int64_t total,
@@ -422,8 +372,8 @@ int sdp_build_masks(const sdp_param_desc* params, int n_params, const sdp_rule_d
   if (owner_mask && (check_mask_bytes(mask_bytes) || mask_bytes * 8 < n_workers))
     return set_error(SDP_ERR_CONFIG, "mask_bytes=%d cannot hold %d workers", mask_bytes, n_workers);
   if (n_params < 1 || total < 1) return set_error(SDP_ERR_TOPOLOGY, "empty topology");
-  const int64_t n_chunks = (total + kBuildElems - 1) / kBuildElems;
-  const int64_t want = (n_chunks + kBuildThreads - 1) / kBuildThreads;
+  const int64_t n_chunks = (total + kWarpChunk - 1) / kWarpChunk;
+  const int64_t want = (n_chunks + kBuildThreads / 32 - 1) / (kBuildThreads / 32);
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 8));
   auto ac = reinterpret_cast<unsigned long long*>(active_counts);
   cudaStream_t s = as_stream(stream);

@@ -1,18 +1,20 @@
 // Width-wise slice extraction and write-back (models.py:333-382).
 //
 //   k_masked_extract  theta * mask for one worker (models.py:355), bit-exact
-//   k_gather          full -> compact sub-tensors (iterates compact elements:
-//                     coalesced stores, rows of the source read contiguously)
-//   k_scatter         compact -> full with zero fill or accumulate (iterates
-//                     full elements through inverse maps: coalesced stores,
-//                     every full element written exactly once)
+//   k_gather          full -> compact: one CTA per task (a run of compact rows
+//                     of one tensor); stores are contiguous over the compact
+//                     row, loads follow the row/column index maps
+//   k_scatter         compact -> full: one CTA per run of FULL rows; every full
+//                     element of a covered row is written once (zero fill) or
+//                     accumulated (owner-ordered write-back), stores coalesced
 //   k_divide          acc / divisor after owner-ordered accumulation
+// Tensors are in canonical [rows, cols, inner] form (include/sdp.h); division
+// by `inner` uses a precomputed multiply-high (no integer divide per element).
 #include "sdp_common.cuh"
 
 namespace sdp {
 
 constexpr int kSliceThreads = 256;
-constexpr int kSliceElems = 4;  // consecutive elements per thread
 
 template <typename T, int MB>
 __global__ void k_masked_extract(const T* __restrict__ theta, const typename MaskT<MB>::T* __restrict__ mask,
@@ -24,82 +26,74 @@ __global__ void k_masked_extract(const T* __restrict__ theta, const typename Mas
   }
 }
 
-__device__ __forceinline__ int find_desc(const sdp_slice_desc* __restrict__ d, int n, int64_t j,
-                                         bool by_compact) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    const int64_t off = by_compact ? d[mid].compact_offset : d[mid].full_offset;
-    if (off <= j) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ int64_t numel(const int64_t* shape, int nd) {
-  int64_t n = 1;
-  for (int k = 0; k < nd; ++k) n *= shape[k];
-  return n;
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t shr) {
+  return mul ? (__umulhi(n, mul) >> shr) : n;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kSliceThreads)
-k_gather(const sdp_slice_desc* __restrict__ descs, int n_descs, const int32_t* __restrict__ fwd,
-         const T* __restrict__ full, T* __restrict__ compact, int64_t compact_total) {
-  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < compact_total;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int di = find_desc(descs, n_descs, k, true);
-    const sdp_slice_desc& d = descs[di];
-    int64_t local = k - d.compact_offset;
-    if (local >= numel(d.compact_shape, d.ndim)) continue;  // hole between descriptors
-    int64_t src = 0, stride = 1;
-    for (int a = d.ndim - 1; a >= 0; --a) {
-      const int64_t cs = d.compact_shape[a];
-      const int64_t c = local % cs;
-      local /= cs;
-      const int64_t f = d.map_offset[a] >= 0 ? static_cast<int64_t>(__ldg(fwd + d.map_offset[a] + c)) : c;
-      src += f * stride;
-      stride *= d.full_shape[a];
+k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks,
+         const int32_t* __restrict__ fwd, const T* __restrict__ full, T* __restrict__ compact) {
+  const sdp_slice_task tk = tasks[blockIdx.x];
+  const sdp_slice_desc d = descs[tk.desc];
+  const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
+  // (row, element) pairs of the task flattened over the CTA: independent
+  // loads across rows instead of one dependent round trip per row.
+  const uint32_t seg = static_cast<uint32_t>(tk.elem_end - tk.elem_begin);
+  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * seg;
+  const int64_t row_stride = static_cast<int64_t>(d.cols) * d.inner;
+#pragma unroll 4
+  for (uint32_t idx = threadIdx.x; idx < n_el; idx += kSliceThreads) {
+    const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);  // 0 for single-row tasks
+    const uint32_t r = tk.row_begin + rr;
+    const uint32_t t = tk.elem_begin + (idx - rr * row_len);
+    const int64_t fr = d.row_map >= 0 ? __ldg(fwd + d.row_map + r) : r;
+    int64_t src = d.full_offset + fr * row_stride;
+    if (d.col_map < 0) {
+      src += t;
+    } else {
+      const uint32_t b = fast_div(t, d.inner_mul, d.inner_shr);
+      src += static_cast<int64_t>(__ldg(fwd + d.col_map + b)) * d.inner + (t - b * d.inner);
     }
-    compact[k] = full[d.full_offset + src];
+    compact[d.compact_offset + static_cast<int64_t>(r) * row_len + t] = full[src];
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kSliceThreads)
-k_scatter(const sdp_slice_desc* __restrict__ descs, int n_descs, const int32_t* __restrict__ inv,
-          const T* __restrict__ compact, T* __restrict__ full, int64_t lo, int64_t hi, int flags) {
-  const bool zero_fill = flags & SDP_SCATTER_ZERO_FILL;
-  const bool accumulate = flags & SDP_SCATTER_ACCUMULATE;
-  for (int64_t j0 = lo + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * kSliceElems;
-       j0 < hi; j0 += static_cast<int64_t>(gridDim.x) * blockDim.x * kSliceElems) {
-    int di = find_desc(descs, n_descs, j0, false);
-#pragma unroll
-    for (int e = 0; e < kSliceElems; ++e) {
-      const int64_t j = j0 + e;
-      if (j >= hi) break;
-      while (di + 1 < n_descs && descs[di + 1].full_offset <= j) ++di;
-      const sdp_slice_desc& d = descs[di];
-      int64_t local = j - d.full_offset;
-      if (local < 0 || local >= numel(d.full_shape, d.ndim)) continue;  // not covered
-      int64_t src = 0, stride = 1;
-      bool live = true;
-      for (int a = d.ndim - 1; a >= 0; --a) {
-        const int64_t fs = d.full_shape[a];
-        const int64_t f = local % fs;
-        local /= fs;
-        int64_t c;
-        if (d.map_offset[a] >= 0) c = __ldg(inv + d.map_offset[a] + f);
-        else c = d.compact_shape[a] > 0 ? f : -1;
-        live &= c >= 0;
-        src += c * stride;
-        stride *= d.compact_shape[a];
+k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks,
+          const int32_t* __restrict__ inv, const T* __restrict__ compact, T* __restrict__ full,
+          int flags) {
+  const bool zero_fill = (flags & SDP_SCATTER_ZERO_FILL) && !(flags & SDP_SCATTER_ACCUMULATE);
+  const bool accumulate = (flags & SDP_SCATTER_ACCUMULATE) != 0;
+  const sdp_slice_task tk = tasks[blockIdx.x];
+  const sdp_slice_desc d = descs[tk.desc];
+  const int64_t crow_len = static_cast<int64_t>(d.ccols) * d.inner;
+  const uint32_t row_len = static_cast<uint32_t>(d.cols) * d.inner;
+  const uint32_t seg = static_cast<uint32_t>(tk.elem_end - tk.elem_begin);
+  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * seg;
+#pragma unroll 4
+  for (uint32_t idx = threadIdx.x; idx < n_el; idx += kSliceThreads) {
+    const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);  // 0 for single-row tasks
+    const uint32_t f = tk.row_begin + rr;
+    const uint32_t t = tk.elem_begin + (idx - rr * row_len);
+    T* dst = full + d.full_offset + static_cast<int64_t>(f) * row_len + t;
+    const int32_t a = d.crows == 0 ? -1 : (d.row_map >= 0 ? __ldg(inv + d.row_map + f) : static_cast<int32_t>(f));
+    int64_t src = -1;
+    if (a >= 0) {
+      if (d.col_map < 0) {
+        src = a * crow_len + t;
+      } else {
+        const uint32_t fb = fast_div(t, d.inner_mul, d.inner_shr);
+        const int32_t cb = __ldg(inv + d.col_map + fb);
+        if (cb >= 0) src = a * crow_len + static_cast<int64_t>(cb) * d.inner + (t - fb * d.inner);
       }
-      if (live) {
-        const T v = compact[d.compact_offset + src];
-        full[j] = accumulate ? static_cast<T>(full[j] + v) : v;
-      } else if (zero_fill && !accumulate) {
-        full[j] = static_cast<T>(0);
-      }
+    }
+    if (src >= 0) {
+      const T v = compact[d.compact_offset + src];
+      *dst = accumulate ? static_cast<T>(*dst + v) : v;
+    } else if (zero_fill) {
+      *dst = T(0);  // the worker does not hold this element
     }
   }
 }
@@ -112,9 +106,8 @@ __global__ void k_divide(const T* __restrict__ acc, const double* __restrict__ d
     out[j] = acc[j] / static_cast<T>(divisor[j]);
 }
 
-static int grid_for(int64_t n, int per_thread = 1) {
-  const int64_t want = (n + static_cast<int64_t>(kSliceThreads) * per_thread - 1) /
-                       (static_cast<int64_t>(kSliceThreads) * per_thread);
+static int grid_for(int64_t n) {
+  const int64_t want = (n + kSliceThreads - 1) / kSliceThreads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 8)));
 }
 
@@ -136,12 +129,12 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask, int
 #define SDP_EXTRACT(TT, MB)                                                                  \
   k_masked_extract<TT, MB><<<grid, kSliceThreads, 0, s>>>(static_cast<const TT*>(theta),    \
       static_cast<const MaskT<MB>::T*>(owner_mask), total, worker, static_cast<TT*>(out))
-#define SDP_EXTRACT_T(T)                  \
-  switch (mask_bytes) {                   \
-    case 1: SDP_EXTRACT(T, 1); break;     \
-    case 2: SDP_EXTRACT(T, 2); break;     \
-    case 4: SDP_EXTRACT(T, 4); break;     \
-    default: SDP_EXTRACT(T, 8); break;    \
+#define SDP_EXTRACT_T(TT)                  \
+  switch (mask_bytes) {                    \
+    case 1: SDP_EXTRACT(TT, 1); break;     \
+    case 2: SDP_EXTRACT(TT, 2); break;     \
+    case 4: SDP_EXTRACT(TT, 4); break;     \
+    default: SDP_EXTRACT(TT, 8); break;    \
   }
   if (dtype == SDP_DTYPE_F32) { SDP_EXTRACT_T(float) }
   else if (dtype == SDP_DTYPE_F64) { SDP_EXTRACT_T(double) }
@@ -152,43 +145,38 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask, int
   return SDP_OK;
 }
 
-static int check_descs(const sdp_slice_desc* d, int n) {
-  (void)d;
-  if (n < 1) return set_error(SDP_ERR_TOPOLOGY, "no slice descriptors");
-  return SDP_OK;
-}
-
-int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, int n_descs, const int32_t* fwd_maps,
-                      const void* full, void* compact, int64_t compact_total, void* stream) {
-  if (check_descs(descs, n_descs)) return SDP_ERR_TOPOLOGY;
-  if (compact_total <= 0) return SDP_OK;
-  const int grid = grid_for(compact_total);
+int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                      int n_tasks, const int32_t* fwd_maps, const void* full, void* compact,
+                      void* stream) {
+  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
+  if (n_tasks == 0) return SDP_OK;
+  if (!descs || !tasks || !full || !compact) return set_error(SDP_ERR_USAGE, "null device pointer");
   cudaStream_t s = as_stream(stream);
   if (dtype == SDP_DTYPE_F32)
-    k_gather<float><<<grid, kSliceThreads, 0, s>>>(descs, n_descs, fwd_maps, static_cast<const float*>(full),
-                                                   static_cast<float*>(compact), compact_total);
+    k_gather<float><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps, static_cast<const float*>(full),
+                                                      static_cast<float*>(compact));
   else if (dtype == SDP_DTYPE_F64)
-    k_gather<double><<<grid, kSliceThreads, 0, s>>>(descs, n_descs, fwd_maps, static_cast<const double*>(full),
-                                                    static_cast<double*>(compact), compact_total);
+    k_gather<double><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps, static_cast<const double*>(full),
+                                                       static_cast<double*>(compact));
   else
     return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
   SDP_LAUNCH_CHECK();
   return SDP_OK;
 }
 
-int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, int n_descs, const int32_t* inv_maps,
-                       const void* compact, void* full, int64_t full_lo, int64_t full_hi, int flags,
-                       void* stream) {
-  if (check_descs(descs, n_descs)) return SDP_ERR_TOPOLOGY;
-  if (full_hi <= full_lo) return SDP_OK;
-  const int grid = grid_for(full_hi - full_lo, kSliceElems);
+int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                       int n_tasks, const int32_t* inv_maps, const void* compact, void* full,
+                       int flags, void* stream) {
+  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
+  if (n_tasks == 0) return SDP_OK;
+  if (!descs || !tasks || !full) return set_error(SDP_ERR_USAGE, "null device pointer");
   cudaStream_t s = as_stream(stream);
   if (dtype == SDP_DTYPE_F32)
-    k_scatter<float><<<grid, kSliceThreads, 0, s>>>(descs, n_descs, inv_maps, static_cast<const float*>(compact),
-                                                    static_cast<float*>(full), full_lo, full_hi, flags);
+    k_scatter<float><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, inv_maps, static_cast<const float*>(compact),
+                                                       static_cast<float*>(full), flags);
   else if (dtype == SDP_DTYPE_F64)
-    k_scatter<double><<<grid, kSliceThreads, 0, s>>>(descs, n_descs, inv_maps, static_cast<const double*>(compact),
-                                                     static_cast<double*>(full), full_lo, full_hi, flags);
+    k_scatter<double><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, inv_maps, static_cast<const double*>(compact),
+                                                        static_cast<double*>(full), flags);
   else
     return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
   SDP_LAUNCH_CHECK();

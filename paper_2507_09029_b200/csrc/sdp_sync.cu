@@ -223,33 +223,35 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
     int64_t jv[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) jv[k] = s + r0 + (k * kSyncThreads + threadIdx.x) * VN;
+    // Owners in ascending order, K at a time: all K*R 16-B loads of a batch are
+    // issued before the first add (K = 2 for R >= 2, 4 for R = 1: fits the
+    // 64-register budget of 4 resident CTAs per SM without spills).
+    constexpr int K = R >= 2 ? 2 : 4;
     uint64_t b = bits;
     while (b) {
-      const int w0 = __ffsll(static_cast<long long>(b)) - 1;
-      b &= b - 1;
-      const T* g0 = static_cast<const T*>(p.replicas[w0]);
-      Vt a[R], bb[R];
+      const T* g[K];
+      bool on[K];
 #pragma unroll
-      for (int k = 0; k < R; ++k) a[k] = V<T>::ld(g0 + jv[k]);
-      const bool two = b != 0;
-      int w1 = 0;
-      if (two) {
-        w1 = __ffsll(static_cast<long long>(b)) - 1;
-        b &= b - 1;
-        const T* g1 = static_cast<const T*>(p.replicas[w1]);
-#pragma unroll
-        for (int k = 0; k < R; ++k) bb[k] = V<T>::ld(g1 + jv[k]);
+      for (int q = 0; q < K; ++q) {
+        on[q] = b != 0;
+        const int w = on[q] ? __ffsll(static_cast<long long>(b)) - 1 : 0;
+        if (on[q]) b &= b - 1;
+        g[q] = static_cast<const T*>(p.replicas[w]);
       }
+      Vt a[K][R];
 #pragma unroll
-      for (int k = 0; k < R; ++k)
-#pragma unroll
-        for (int e = 0; e < VN; ++e) acc[k].x[e] = add_rn(acc[k].x[e], a[k].x[e]);
-      if (two) {
+      for (int q = 0; q < K; ++q)
 #pragma unroll
         for (int k = 0; k < R; ++k)
+          if (on[q]) a[q][k] = V<T>::ld(g[q] + jv[k]);
 #pragma unroll
-          for (int e = 0; e < VN; ++e) acc[k].x[e] = add_rn(acc[k].x[e], bb[k].x[e]);
-      }
+      for (int q = 0; q < K; ++q)
+        if (on[q]) {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+#pragma unroll
+            for (int e = 0; e < VN; ++e) acc[k].x[e] = add_rn(acc[k].x[e], a[q][k].x[e]);
+        }
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {

@@ -45,6 +45,12 @@ def _sm_count() -> int:
     return int(n.value)
 
 
+def auto_tile(d: int, sms: int) -> int:
+    """2048-element tiles, or 1024 when that leaves fewer than two full waves
+    of resident CTAs (small buffers are latency-bound: more, shorter CTAs)."""
+    return TILE if -(-d // TILE) >= 2 * sms * CTAS_PER_SM else TILE // 2
+
+
 def gpu_of_worker(n_workers: int, world: int) -> np.ndarray:
     """Contiguous placement of N logical workers on `world` GPUs: w -> w*G//N."""
     return np.array([w * world // n_workers for w in range(n_workers)], dtype=np.int64)
@@ -96,12 +102,14 @@ class SyncPlan:
     logical workers to ranks (contiguous placement, SURVEY.md §7 hard part 6).
     """
 
-    def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int = TILE,
+    def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int | None = None,
                  resident: bool = False, max_grid: int | None = None,
                  force_grid: int | None = None):
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
+        if tile is None:
+            tile = auto_tile(d, _sm_count())
         self.tile = tile
         self.world, self.rank = world, rank
         n_tiles = (d + tile - 1) // tile

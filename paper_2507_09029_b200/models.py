@@ -33,7 +33,7 @@ import torch.nn.functional as F
 from . import _native as N
 from ._device import device, ptr, sdp_dtype, stream_ptr
 from .errors import ConfigError, InputError
-from .topology import GlobalModel
+from .topology import GlobalModel, fast_divisor
 from . import zoo
 
 
@@ -224,9 +224,35 @@ def kaiming_fan_out_init(model: GlobalModel, assignment, seed: int) -> torch.Ten
 # compact subnetwork layout (gather / scatter descriptor tables)
 # ---------------------------------------------------------------------------
 
-SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("full_shape", "<i8", 4),
-                        ("compact_shape", "<i8", 4), ("map_offset", "<i4", 4), ("ndim", "<i4"),
+SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("rows", "<i4"),
+                        ("cols", "<i4"), ("inner", "<i4"), ("crows", "<i4"), ("ccols", "<i4"),
+                        ("row_map", "<i4"), ("col_map", "<i4"), ("inner_mul", "<u4"),
+                        ("inner_shr", "<u4"), ("rowlen_mul", "<u4"), ("rowlen_shr", "<u4"),
                         ("pad_", "<i4")])
+TASK_DTYPE = np.dtype([("desc", "<i4"), ("row_begin", "<i4"), ("row_end", "<i4"),
+                       ("elem_begin", "<i4"), ("elem_end", "<i4"), ("pad_", "<i4", 3)])
+TASK_ELEMS = 4096  # elements per gather/scatter CTA (16 per thread, rows flattened)
+
+
+def slice_tasks(descs: np.ndarray, compact: bool, per_task: int = TASK_ELEMS) -> np.ndarray:
+    """Split every tensor into CTA work units of ~per_task elements: runs of
+    whole rows, or pieces of one row when a row is longer (compact rows for
+    gather, full rows for scatter)."""
+    out = []
+    for i, d in enumerate(descs):
+        rows = int(d["crows"] if compact else d["rows"])
+        row_len = int((d["ccols"] if compact else d["cols"]) * d["inner"])
+        if rows == 0 or row_len == 0:
+            continue
+        if row_len >= per_task:
+            for r in range(rows):
+                for e in range(0, row_len, per_task):
+                    out.append((i, r, r + 1, e, min(row_len, e + per_task), (0, 0, 0)))
+        else:
+            k = max(1, per_task // row_len)
+            for r in range(0, rows, k):
+                out.append((i, r, min(rows, r + k), 0, row_len, (0, 0, 0)))
+    return np.array(out, dtype=TASK_DTYPE)
 
 
 class SubnetLayout:
@@ -274,47 +300,61 @@ class SubnetLayout:
         descs = np.zeros(len(topo.params), dtype=SLICE_DTYPE)
         self.shapes: dict[str, tuple[int, ...]] = {}
         self.offsets: dict[str, int] = {}
-        imaps: list[list[int]] = []
+        inv_rows: list[tuple[int, int]] = []   # (row_map, col_map) offsets into the inverse maps
         pos = 0
         for i, p in enumerate(topo.params):
-            shape = list(p.shape)
+            ax = axes[p.name]
+            if any(a > 1 for a in ax):
+                raise ConfigError(f"{p.name}: only axes 0 and 1 may be channel-governed")
+            # canonical [rows, cols, inner]: a 1-D tensor is one row of `cols`;
+            # an ungoverned axis 1 folds into `inner` (contiguous rows)
+            if len(p.shape) == 1:
+                rows, cols, inner = 1, p.shape[0], 1
+                rlid, clid = None, ax.get(0)
+            else:
+                rows, cols = p.shape[0], p.shape[1]
+                inner = int(np.prod(p.shape[2:])) if len(p.shape) > 2 else 1
+                rlid, clid = ax.get(0), ax.get(1)
+                if clid is None:
+                    inner *= cols
+                    cols = 1
+            crows = len(live_ch[rlid]) if rlid else rows
+            ccols = len(live_ch[clid]) if clid else cols
+            if not present[p.name]:
+                crows = 0
             cshape = list(p.shape)
-            fmap, imap = [-1] * 4, [-1] * 4
-            for axis, lid in axes[p.name].items():
+            for axis, lid in ax.items():
                 cshape[axis] = len(live_ch[lid])
-                fmap[axis] = fwd_off[lid]
-                imap[axis] = inv_off[lid]
             if not present[p.name]:
                 cshape[0] = 0
-            n = int(np.prod(cshape)) if cshape else 1
-            nd = len(shape)
-            if nd > 4:
-                raise ConfigError(f"{p.name}: at most 4 dims supported")
-            descs[i]["full_offset"] = p.offset
-            descs[i]["compact_offset"] = pos
-            descs[i]["full_shape"][:nd] = shape
-            descs[i]["full_shape"][nd:] = 1
-            descs[i]["compact_shape"][:nd] = cshape
-            descs[i]["compact_shape"][nd:] = 1
-            descs[i]["ndim"] = nd
-            descs[i]["map_offset"] = fmap
+            mul, shr = fast_divisor(inner)
+            rl_mul, rl_shr = fast_divisor(max(1, ccols * inner))
+            descs[i] = (p.offset, pos, rows, cols, inner, crows, ccols,
+                        fwd_off[rlid] if rlid else -1, fwd_off[clid] if clid else -1, mul, shr,
+                        rl_mul, rl_shr, 0)
+            inv_rows.append((inv_off[rlid] if rlid else -1, inv_off[clid] if clid else -1))
             self.shapes[p.name] = tuple(cshape)
             self.offsets[p.name] = pos
-            pos += n
-            imaps.append(imap)  # the scatter side reads the inverse maps, same axis slots
+            pos += crows * ccols * inner
         self.compact_total = pos
-        self.descs_fwd = descs
         descs_inv = descs.copy()
-        for i, imap in enumerate(imaps):
-            descs_inv[i]["map_offset"] = imap
+        descs_inv["row_map"] = [r for r, _ in inv_rows]
+        descs_inv["col_map"] = [c for _, c in inv_rows]
+        full_rl = [fast_divisor(max(1, int(d["cols"] * d["inner"]))) for d in descs]
+        descs_inv["rowlen_mul"] = [m for m, _ in full_rl]
+        descs_inv["rowlen_shr"] = [s for _, s in full_rl]
         from ._device import upload_struct
+        self.descs = descs
         self.d_fwd = upload_struct(descs, dev)
         self.d_inv = upload_struct(descs_inv, dev)
+        g_tasks = slice_tasks(descs, compact=True)
+        s_tasks = slice_tasks(descs, compact=False)
+        self.t_gather, self.n_gather = upload_struct(g_tasks, dev), len(g_tasks)
+        self.t_scatter, self.n_scatter = upload_struct(s_tasks, dev), len(s_tasks)
         fw = np.concatenate(fwd) if fwd else np.zeros(1, np.int32)
         iv = np.concatenate(inv) if inv else np.zeros(1, np.int32)
         self.fwd_maps = torch.from_numpy(fw.astype(np.int32)).to(dev)
         self.inv_maps = torch.from_numpy(iv.astype(np.int32)).to(dev)
-        self.n_descs = len(descs)
 
     def present(self, name: str) -> bool:
         return self.present_map[name] and int(np.prod(self.shapes[name])) > 0
@@ -334,8 +374,8 @@ class SubnetLayout:
         """Full theta -> compact buffer (sdp_gather_slices)."""
         if out is None:
             out = torch.empty(max(1, self.compact_total), dtype=theta.dtype, device=theta.device)
-        N.call("sdp_gather_slices", sdp_dtype(theta.dtype), ptr(self.d_fwd), self.n_descs,
-               ptr(self.fwd_maps), ptr(theta), ptr(out), self.compact_total, stream_ptr(theta.device))
+        N.call("sdp_gather_slices", sdp_dtype(theta.dtype), ptr(self.d_fwd), ptr(self.t_gather),
+               self.n_gather, ptr(self.fwd_maps), ptr(theta), ptr(out), stream_ptr(theta.device))
         return out
 
     def scatter(self, compact: torch.Tensor, full: torch.Tensor | None = None,
@@ -346,8 +386,9 @@ class SubnetLayout:
             full = torch.empty(d, dtype=compact.dtype, device=compact.device)
             accumulate = False
         flags = N.SCATTER_ACCUMULATE if accumulate else N.SCATTER_ZERO_FILL
-        N.call("sdp_scatter_slices", sdp_dtype(compact.dtype), ptr(self.d_inv), self.n_descs,
-               ptr(self.inv_maps), ptr(compact), ptr(full), 0, d, flags, stream_ptr(compact.device))
+        N.call("sdp_scatter_slices", sdp_dtype(compact.dtype), ptr(self.d_inv), ptr(self.t_scatter),
+               self.n_scatter, ptr(self.inv_maps), ptr(compact), ptr(full), flags,
+               stream_ptr(compact.device))
         return full
 
 

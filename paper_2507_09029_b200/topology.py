@@ -139,7 +139,18 @@ class UnitTable:
 
 
 PARAM_DTYPE = np.dtype([("offset", "<i8"), ("size", "<i8"), ("rule_begin", "<i4"), ("rule_count", "<i4")])
-RULE_DTYPE = np.dtype([("inner", "<i8"), ("dim", "<i8"), ("unit_base", "<i4"), ("pad_", "<i4")])
+RULE_DTYPE = np.dtype([("inner", "<i4"), ("dim", "<i4"), ("unit_base", "<i4"),
+                       ("inner_mul", "<u4"), ("inner_shr", "<u4"), ("dim_mul", "<u4"),
+                       ("dim_shr", "<u4"), ("pad_", "<i4")])
+
+
+def fast_divisor(d: int) -> tuple[int, int]:
+    """(mul, shr) with n // d == umulhi(n, mul) >> shr for 0 <= n < 2**31
+    (mul = 0 encodes d == 1)."""
+    if d == 1:
+        return 0, 0
+    p = 31 + (d - 1).bit_length()
+    return ((1 << p) + d - 1) // d, p - 32
 
 
 def unit_table(topology: ModelTopology, strategy: str) -> UnitTable:
@@ -199,6 +210,7 @@ def unit_table(topology: ModelTopology, strategy: str) -> UnitTable:
         if p.size >= 2**31:
             raise TopologyError(f"parameter {p.name} exceeds 2^31 elements")
         params[i] = (p.offset, p.size, len(rules_list), len(rs))
-        rules_list.extend((inner, dim, base, 0) for inner, dim, base in rs)
-    rules = np.array(rules_list if rules_list else [(1, 1, 0, 0)], dtype=RULE_DTYPE)
+        rules_list.extend((inner, dim, base, *fast_divisor(inner), *fast_divisor(dim), 0)
+                          for inner, dim, base in rs)
+    rules = np.array(rules_list if rules_list else [(1, 1, 0, 0, 0, 0, 0, 0)], dtype=RULE_DTYPE)
     return UnitTable(strategy, keys, layer_base, block_unit, groups, params, rules)

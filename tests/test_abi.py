@@ -74,7 +74,8 @@ int main(void) {
   F(sdp_sync_args, owner_mask) F(sdp_sync_args, replicas) F(sdp_sync_args, shadow_bf16)
   F(sdp_sync_args, lr) F(sdp_sync_args, status) F(sdp_sync_args, signal_pads)
   F(sdp_sync_args, epoch) F(sdp_sync_args, timeout_cycles)
-  F(sdp_slice_desc, map_offset) F(sdp_slice_desc, ndim)
+  F(sdp_slice_desc, rows) F(sdp_slice_desc, col_map) F(sdp_slice_desc, inner_shr)
+  printf("sdp_slice_task %zu\n", sizeof(sdp_slice_task));
   return 0;
 }
 """
@@ -94,6 +95,9 @@ def test_struct_layouts_match_c(tmp_path):
     assert int(out["sdp_param_desc"]) == C.sizeof(N.ParamDesc)
     assert int(out["sdp_rule_desc"]) == C.sizeof(N.RuleDesc)
     assert int(out["sdp_group_desc"]) == C.sizeof(N.GroupDesc)
+    assert int(out["sdp_slice_task"]) == C.sizeof(N.SliceTask) == 32
+    from paper_2507_09029_b200.models import SLICE_DTYPE, TASK_DTYPE
+    assert SLICE_DTYPE.itemsize == C.sizeof(N.SliceDesc) and TASK_DTYPE.itemsize == C.sizeof(N.SliceTask)
     for key, val in out.items():
         if "." in key:
             struct, field = key.split(".")

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--no-shadow", action="store_true")
     ap.add_argument("--no-writeback", action="store_true")
-    ap.add_argument("--tile", type=int, default=4096)
+    ap.add_argument("--tile", type=int, default=None)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     if args.workload == "resnet18":
