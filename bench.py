@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--strategy", default="block")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -325,8 +327,11 @@ def run_ours(args):
 
     e2e = None
     cpu = None
+    train = None
     if rank == 0 and world == 1:
         e2e = run_e2e(args, a, dev, total_bytes)
+        if not args.no_train and args.workload == "resnet18":
+            train = run_train(args, dev)
         if not args.no_cpu_baseline:
             cpu = run_cpu_baseline(args, topo)
     if rank == 0:
@@ -343,6 +348,8 @@ def run_ours(args):
         }
         if e2e:
             line["e2e"] = e2e
+        if train:
+            line["train"] = train
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -381,6 +388,52 @@ def run_e2e(args, a, dev, total_bytes):
             "d2h_bytes_per_step": d * 4, "ms_per_step": dt * 1e3,
             "api": "paper_2507_09029_b200.engine.aggregate(list[np.ndarray pinned], assignment)",
             "timing": "host wall clock around the blocking call (returns numpy)"}
+
+
+def run_train(args, dev):
+    """BASELINE metric parts 2-3: train samples/s/GPU and peak memory per GPU
+    vs full-replica DP (configs[1]: ResNet-18, N=8, P=4, batch 64/worker).
+    Workers are co-resident on this GPU; a step = 8 subnetwork fwd/bwd (bf16
+    autocast, dropped blocks skipped) + one fused sync/Nesterov launch.  The DP
+    comparator is the same loop with P = N (every worker holds the full model)."""
+    import torch
+
+    from paper_2507_09029_b200 import masking, train
+    batch, n = 64, args.n_logical
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    batches = [(torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
+                torch.randint(0, 10, (batch,), generator=gen, device=dev)) for _ in range(n)]
+    out = {"workload": f"ResNet-18 CIFAR-shape, N={n} co-resident workers, batch {batch}/worker, "
+                       "bf16 autocast fwd/bwd, fused sync+Nesterov+bf16 cast", "data": "synthetic"}
+    for tag, p in (("subnet", args.p), ("dp", n)):
+        model = train.build_resnet18(dev)
+        a = masking.build_assignment(model.topology, "block", n, p, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=0.01)
+        out[f"{tag}_loss_first"] = float(tr.step(batches).item())
+        for _ in range(2):
+            tr.step(batches)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.train_steps):
+            loss = tr.step(batches)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / args.train_steps
+        out[f"{tag}_ms_per_step"] = ms
+        out[f"{tag}_samples_per_s_per_gpu"] = n * batch / (ms / 1e3)
+        out[f"{tag}_loss_last"] = float(loss.item())
+        mems = [train.worker_memory(model, a, w if p < n else None, batch, dev)["peak_bytes"]
+                for w in (range(n) if p < n else [0])]
+        out[f"{tag}_peak_mem_per_worker_bytes"] = max(mems)
+        del tr, model, a
+        torch.cuda.empty_cache()
+    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
+    out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
+    out["note"] = ("peak memory = one worker's compact fp32 master + grad + momentum + bf16 copy + "
+                   "activations of its fwd/bwd, i.e. what a GPU holding that worker needs (N = G)")
+    return out
 
 
 def run_cpu_baseline(args, topo):

@@ -1,0 +1,171 @@
+"""Training-step integration: N subnetwork workers + owner-subset sync on B200.
+
+The reference's protocol step (engine.py:202-223) is: every worker runs a
+forward/backward on its subnetwork, the gradients are masked-averaged
+(`aggregate`), and one SGD-Nesterov update is applied.  Here the per-worker
+forward/backward is dense cuDNN/cuBLAS in bf16 autocast (not the optimisation
+target), dropped residual blocks are never executed (models.py:161-163), and
+the sync + update is ONE k_owner_sync launch with the Nesterov epilogue and
+the bf16 weight cast fused (SDP_SYNC_NESTEROV).
+
+`ResNet18Cifar` is the BASELINE configs[1]/[2] model: CIFAR stem, GroupNorm(2),
+torchvision BasicBlock (ReLU after the residual add), the 3 downsampling blocks
+always active.  Its parameter layout is zoo.resnet18_cifar_topology.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from . import engine, masking, zoo
+from .topology import GlobalModel
+
+
+class ResNet18Cifar:
+    def __init__(self, classes: int = 10, norm_groups: int = 2):
+        self.classes, self.norm_groups = classes, norm_groups
+        self.topology = zoo.resnet18_cifar_topology(classes, norm_groups)
+        self.block_plan = []
+        cin = 64
+        for stage, planes in enumerate((64, 128, 256, 512), start=1):
+            for j in range(2):
+                stride = 2 if (stage > 1 and j == 0) else 1
+                self.block_plan.append((f"layer{stage}.{j}", stride, stride != 1 or cin != planes))
+                cin = planes
+
+    def build_topology(self):
+        return self.topology
+
+    def forward(self, params, x, worker=None, block_mode: str = "skip"):
+        g = self.norm_groups
+        h = F.conv2d(x, params["conv1.w"], padding=1)
+        h = F.relu(F.group_norm(h, g, params["gn1.gamma"], params["gn1.beta"]))
+        for bi, (p, stride, down) in enumerate(self.block_plan):
+            live = True if worker is None else bool(worker.block_active[bi])
+            if not live and block_mode == "skip":
+                continue  # a dropped block is the identity and is never executed
+            o = F.conv2d(h, params[f"{p}.conv1.w"], stride=stride, padding=1)
+            o = F.relu(F.group_norm(o, g, params[f"{p}.gn1.gamma"], params[f"{p}.gn1.beta"]))
+            o = F.conv2d(o, params[f"{p}.conv2.w"], padding=1)
+            o = F.group_norm(o, g, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"])
+            if down:
+                sc = F.conv2d(h, params[f"{p}.down.w"], stride=stride)
+                sc = F.group_norm(sc, g, params[f"{p}.down_gn.gamma"], params[f"{p}.down_gn.beta"])
+            else:
+                sc = h
+            if not live:
+                o = o * 0.0
+            h = F.relu(o + sc)
+        return F.linear(h.mean(dim=(2, 3)), params["fc.w"], params["fc.b"])
+
+
+def param_views(topology, flat: torch.Tensor) -> dict:
+    return {p.name: flat[p.offset:p.offset + p.size].view(p.shape) for p in topology.params}
+
+
+@dataclass
+class StepStats:
+    loss_mean: float
+
+
+class SubnetTrainer:
+    """N logical workers co-resident on one GPU (the reference's in-process
+    structure, engine.py:180-245) with the owner-subset sync fused into the
+    optimizer step.
+
+    theta / velocity: canonical fp32 master state (engine.py:223 updates one
+    shared theta); theta_bf16: the training copy every worker's forward reads,
+    written by the sync kernel's epilogue."""
+
+    def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
+                 autocast: bool = True):
+        self.model = model
+        self.assignment = assignment
+        self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
+        d = model.topology.total
+        dev = model.theta.device
+        self.velocity = torch.zeros(d, device=dev)
+        self.theta_bf16 = model.theta.to(torch.bfloat16)
+        self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
+        self.lr, self.momentum, self.autocast = lr, momentum, autocast
+        self.plan = assignment.sync_plan()
+        self._prep = None
+
+    def _sync(self):
+        if self._prep is None:
+            self._prep = engine.PreparedSync(
+                self.grads, self.assignment, writeback=False, plan=self.plan,
+                nesterov={"theta": self.model.theta, "velocity": self.velocity, "lr": self.lr,
+                          "momentum": self.momentum, "theta_bf16": self.theta_bf16})
+        self._prep.args.lr = float(self.lr)
+        self._prep.launch()
+
+    def step(self, batches) -> torch.Tensor:
+        """batches: list of N (x, y) device tensors; returns the mean loss (device)."""
+        topo = self.model.topology
+        losses = []
+        for w, (x, y) in enumerate(batches):
+            # the worker trains on the bf16 weights the previous sync wrote
+            leaf = (self.theta_bf16 if self.autocast else self.model.theta).detach().requires_grad_(True)
+            params = param_views(topo, leaf)
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                logits = self.model.arch.forward(params, x, self.views[w])
+                loss = F.cross_entropy(logits.float(), y)
+            (g,) = torch.autograd.grad(loss, leaf)
+            self.grads[w].copy_(g)  # fp32 gradient replica of worker w
+            losses.append(loss.detach())
+        self._sync()
+        return torch.stack(losses).mean()
+
+
+def build_resnet18(dev, seed: int = 1) -> GlobalModel:
+    arch = ResNet18Cifar()
+    topo = arch.topology
+    theta = torch.zeros(topo.total, device=dev)
+    m = GlobalModel(arch=arch, topology=topo, theta=theta)
+    from .models import kaiming_fan_out_init
+    m.theta = kaiming_fan_out_init(m, None, seed)
+    return m
+
+
+def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int,
+                  dev) -> dict:
+    """Peak device memory of ONE worker's training state and step, as a GPU
+    holding one worker would see it (paper: params, grads, optimizer state and
+    activations all scale with the subnetwork).  worker=None: the full model
+    (a full-replica DP worker).  Parameters/grad/momentum are allocated for
+    the worker's active elements only (compact storage), the forward/backward
+    runs on the subnetwork."""
+    from .models import SubnetLayout
+    topo = model.topology
+    if worker is None:  # full replica = the P = N assignment's worker 0
+        assignment = masking.build_assignment(topo, "block", 1, 1, seed=0)
+        worker = 0
+    sub = SubnetLayout(assignment, worker)
+    view = assignment.worker_view(worker)
+    x = torch.randn(batch, 3, 32, 32, device=dev)
+    y = torch.randint(0, 10, (batch,), device=dev)
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    # compact fp32 master (the leaf) + momentum + bf16 copy; autograd adds the grad
+    master = sub.gather(model.theta).requires_grad_(True)
+    momentum = torch.zeros_like(master)
+    shadow = master.detach().to(torch.bfloat16)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        loss = F.cross_entropy(model.arch.forward(sub.views(master), x, view).float(), y)
+    loss.backward()
+    torch.cuda.synchronize(dev)
+    peak = torch.cuda.max_memory_allocated(dev) - base
+    active = sub.compact_total
+    del master, momentum, shadow, loss
+    return {"active_params": int(active), "peak_bytes": int(peak),
+            "state_bytes": int(active * (4 * 3 + 2))}
+
+
+def build_block_assignment(topo, n=8, p=4, seed=1):
+    return masking.build_assignment(topo, "block", n, p, seed)

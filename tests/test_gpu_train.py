@@ -1,0 +1,41 @@
+"""Training-step integration (engine.py:202-223) on ResNet-18 (configs[1])."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_resnet18_subnet_step_matches_oracle(cuda):
+    from paper_2507_09029_b200 import masking, train
+    model = train.build_resnet18(cuda, seed=3)
+    a = masking.build_assignment(model.topology, "block", 8, 4, seed=1)
+    tr = train.SubnetTrainer(model, a, lr=0.05, autocast=False)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(0)
+    batches = [(torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
+                torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(8)]
+    th0 = model.theta.cpu().numpy().copy()
+    tr.step(batches)
+    grads = [g.cpu().numpy() for g in tr.grads]
+    masks = a.param_masks.cpu().numpy()
+    for w in range(8):  # a worker's gradient is exactly zero outside its subnetwork
+        assert np.all(grads[w][~masks[w]] == 0.0)
+    gbar = O.aggregate_f32_ordered(grads, masks)
+    th1, v1 = O.nesterov_update(th0, np.zeros_like(th0), gbar, 0.05, 0.9)
+    assert np.array_equal(model.theta.cpu().numpy().view(np.uint32), th1.astype(np.float32).view(np.uint32))
+    assert np.array_equal(tr.theta_bf16.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(th1))
+
+
+def test_memory_subnet_below_full_replica(cuda):
+    from paper_2507_09029_b200 import masking, train
+    model = train.build_resnet18(cuda)
+    a = masking.build_assignment(model.topology, "block", 8, 4, seed=1)
+    sub = train.worker_memory(model, a, 0, 64, cuda)
+    full = train.worker_memory(model, a, None, 64, cuda)
+    assert sub["active_params"] == a.worker_view(0).active_params
+    assert full["active_params"] == model.topology.total
+    assert sub["peak_bytes"] < full["peak_bytes"]
