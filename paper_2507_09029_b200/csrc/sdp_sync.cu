@@ -274,36 +274,30 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
   }
 }
 
-// Mixed tile: per-element owner sets from the owner mask.  A vector is loaded
-// from every worker in the union of its VN elements' owner sets; each element
-// adds only its own owners, in ascending order.
+// Mixed tile: per-element owner sets from the owner mask (neuron strategy).
+// Lane-per-element: a warp covers 32 consecutive elements, each thread EL of
+// them at a stride of the CTA width, and the tile's owners (the union over the
+// tile, warp-uniform) are walked in ascending order, two at a time, with
+// per-lane predicates -- every load and store is a coalesced, predicated
+// access that touches only owned elements, and each element adds exactly its
+// own owners in ascending order.
 template <typename T, int MB, int R>
 __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, uint64_t tile_union,
                                                 uint32_t& st) {
-  constexpr int VN = V<T>::N;
-  using Vt = typename V<T>::type;
+  constexpr int EL = 4;  // elements per thread per round
   using M = typename MaskT<MB>::T;
   const M* mask = static_cast<const M*>(p.owner_mask);
-  const int per_round = R * VN * kSyncThreads;
-  for (int r0 = 0; r0 < p.tile; r0 += per_round) {
-    int64_t jv[R];
-    uint64_t m[R][VN];
-    uint64_t vu[R];
-    Vt acc[R];
+  const bool wb = (p.flags & SDP_SYNC_WRITEBACK) != 0;
+  for (int r0 = 0; r0 < p.tile; r0 += EL * kSyncThreads) {
+    int64_t j[EL];
+    uint64_t m[EL];
+    T acc[EL];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      jv[k] = s + r0 + (k * kSyncThreads + threadIdx.x) * VN;
-      vu[k] = 0;
-#pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        m[k][e] = static_cast<uint64_t>(__ldg(mask + jv[k] + e));
-        vu[k] |= m[k][e];
-        acc[k].x[e] = static_cast<T>(0);
-      }
+    for (int u = 0; u < EL; ++u) {
+      j[u] = s + r0 + u * kSyncThreads + threadIdx.x;
+      m[u] = static_cast<uint64_t>(__ldg(mask + j[u]));
+      acc[u] = static_cast<T>(0);
     }
-    // Owners of the whole tile in ascending order, two at a time; a vector is
-    // fetched from worker w only if one of its elements is owned by w, and an
-    // element adds only its own owners -- so the per-element order is exact.
     uint64_t b = tile_union;
     while (b) {
       const int w0 = __ffsll(static_cast<long long>(b)) - 1;
@@ -313,41 +307,47 @@ __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, 
       if (two) b &= b - 1;
       const T* g0 = static_cast<const T*>(p.replicas[w0]);
       const T* g1 = static_cast<const T*>(p.replicas[w1]);
-      Vt a[R], c[R];
+      T a[EL], c[EL];
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        if ((vu[k] >> w0) & 1ull) a[k] = V<T>::ld(g0 + jv[k]);
-        if (two && ((vu[k] >> w1) & 1ull)) c[k] = V<T>::ld(g1 + jv[k]);
+      for (int u = 0; u < EL; ++u) {
+        a[u] = ((m[u] >> w0) & 1ull) ? __ldcs(g0 + j[u]) : static_cast<T>(0);
+        c[u] = (two && ((m[u] >> w1) & 1ull)) ? __ldcs(g1 + j[u]) : static_cast<T>(0);
       }
 #pragma unroll
-      for (int k = 0; k < R; ++k)
-#pragma unroll
-        for (int e = 0; e < VN; ++e) {
-          if ((m[k][e] >> w0) & 1ull) acc[k].x[e] = add_rn(acc[k].x[e], a[k].x[e]);
-          if (two && ((m[k][e] >> w1) & 1ull)) acc[k].x[e] = add_rn(acc[k].x[e], c[k].x[e]);
-        }
+      for (int u = 0; u < EL; ++u) {
+        if ((m[u] >> w0) & 1ull) acc[u] = add_rn(acc[u], a[u]);
+        if (two && ((m[u] >> w1) & 1ull)) acc[u] = add_rn(acc[u], c[u]);
+      }
     }
+    T mean[EL];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      Vt mean;
-      uint64_t inter = ~0ull;
-#pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        const int cnt = __popcll(m[k][e]);
-        mean.x[e] = div_rn(acc[k].x[e], static_cast<T>(cnt > 0 ? cnt : 1));
-        inter &= m[k][e];
-        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
-        if (cnt == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
-          for (int w = 0; w < p.n_workers; ++w)
-            if (!finite(static_cast<const T*>(p.replicas[w])[jv[k] + e])) st |= SDP_STATUS_UNCOVERED_LEAK;
-        }
+    for (int u = 0; u < EL; ++u) {
+      const int cnt = __popcll(m[u]);
+      mean[u] = div_rn(acc[u], static_cast<T>(cnt > 0 ? cnt : 1));
+      if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean[u])) st |= SDP_STATUS_NONFINITE;
+      if (cnt == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+        for (int w = 0; w < p.n_workers; ++w)
+          if (!finite(static_cast<const T*>(p.replicas[w])[j[u]])) st |= SDP_STATUS_UNCOVERED_LEAK;
       }
-      if (inter == vu[k]) {
-        emit_vec<T>(p, jv[k], vu[k], mean);  // the VN elements share one owner set
-      } else {
+      if (p.out) static_cast<T*>(p.out)[j[u]] = mean[u];
+      if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[j[u]] = to_bf16(mean[u]);
+    }
+    if (wb) {
+      for (uint64_t bb = tile_union; bb; bb &= bb - 1) {
+        const int w = __ffsll(static_cast<long long>(bb)) - 1;
+        T* rep = static_cast<T*>(p.replicas[w]);
+        __nv_bfloat16* sh = p.has_shadow ? static_cast<__nv_bfloat16*>(p.shadow[w]) : nullptr;
 #pragma unroll
-        for (int e = 0; e < VN; ++e) emit_scalar<T>(p, jv[k] + e, m[k][e], mean.x[e]);
+        for (int u = 0; u < EL; ++u)
+          if ((m[u] >> w) & 1ull) {
+            rep[j[u]] = mean[u];
+            if (sh) sh[j[u]] = to_bf16(mean[u]);
+          }
       }
+    }
+    if (p.flags & SDP_SYNC_NESTEROV) {
+#pragma unroll
+      for (int u = 0; u < EL; ++u) nesterov_elem<T>(p, j[u], mean[u]);
     }
   }
 }

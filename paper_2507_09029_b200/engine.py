@@ -130,9 +130,13 @@ class SyncPlan:
         self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1)
         if max_grid:
             self.grid = max(1, min(self.grid, max_grid))
+        self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
+        if not (resident or world > 1 or max_grid):
+            # equal tile counts per CTA: shrink the grid to ceil(n / tiles_per_cta)
+            self.grid = max(1, -(-self.n_tiles // self.tiles_per_cta))
         if force_grid:
             self.grid = int(force_grid)  # all ranks launch the same grid (pairwise barrier)
-        self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
+            self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
         self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
         # exact sum of |O_j| over this rank's elements (per-tile coverage sums)
