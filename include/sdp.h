@@ -168,6 +168,7 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
 #define SDP_SYNC_CHECK_UNCOVERED 0x2 /* engine.py:75-78 leak check -> status */
 #define SDP_SYNC_CHECK_FINITE 0x4    /* optim.py:79-80 isfinite(gbar) -> status */
 #define SDP_SYNC_NESTEROV 0x8        /* fused optim.py:81-84 update on theta/vel */
+#define SDP_SYNC_ADAM 0x10           /* fused optim.py:101-109 update on theta/m/v */
 
 /* status word bits written (atomicOr) by the kernel */
 #define SDP_STATUS_UNCOVERED_LEAK 0x1
@@ -204,6 +205,11 @@ typedef struct {
   uint32_t epoch;            /* increments every launch */
   uint32_t pad_;
   int64_t timeout_cycles;    /* spin limit per barrier */
+  /* fused Adam (SDP_SYNC_ADAM, optim.py:90-109): `velocity` holds m, this v;
+   * the host passes 1 - beta (as the reference computes it in float64) and
+   * the bias corrections bias1 = 1 - beta1^t, bias2 = 1 - beta2^t. */
+  void* second_moment;
+  double beta1, beta2, one_minus_beta1, one_minus_beta2, bias1, bias2, eps;
 } sdp_sync_args;
 
 /* Launch the owner-subset sync.  For every element j with owner set O_j:

@@ -28,6 +28,7 @@ SYNC_WRITEBACK = 0x1
 SYNC_CHECK_UNCOVERED = 0x2
 SYNC_CHECK_FINITE = 0x4
 SYNC_NESTEROV = 0x8
+SYNC_ADAM = 0x10
 
 SCATTER_ZERO_FILL = 0x1
 SCATTER_ACCUMULATE = 0x2
@@ -90,6 +91,10 @@ class SyncArgs(C.Structure):
         ("signal_pads", C.c_void_p * 8),
         ("epoch", C.c_uint32), ("pad_", C.c_uint32),
         ("timeout_cycles", C.c_int64),
+        ("second_moment", C.c_void_p),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("one_minus_beta1", C.c_double),
+        ("one_minus_beta2", C.c_double), ("bias1", C.c_double), ("bias2", C.c_double),
+        ("eps", C.c_double),
     ]
 
 

@@ -95,6 +95,8 @@ struct SyncParams {
   uint32_t* status;
   uint32_t* pads[8];
   double lr, momentum;
+  void* second_moment;                                  // Adam v
+  double beta1, beta2, omb1, omb2, bias1, bias2, eps;   // Adam scalars
   int64_t total;
   int64_t timeout_cycles;
   int32_t n_workers, tile, n_tiles, tiles_per_cta, flags, rank, world;
@@ -124,14 +126,39 @@ __device__ bool cross_rank_barrier(const SyncParams& p, uint32_t value) {
   return __syncthreads_and(ok);
 }
 
+__device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
+__device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
+
+// One optimizer step on one element, every operation rounded exactly where
+// numpy rounds it (no FMA contraction):
+//   SGD-Nesterov (optim.py:81-84): v = v*mu + g;  th = th - lr*(g + mu*v)
+//   Adam (optim.py:101-109): m = b1*m + (1-b1)*g;  v = b2*v + ((1-b2)*g)*g;
+//                            th = th - (lr*(m/c1)) / (sqrt(v/c2) + eps)
+template <typename T>
+__device__ __forceinline__ void optim_step(const SyncParams& p, T g, T& th, T& s1, T& s2) {
+  const T lr = static_cast<T>(p.lr);
+  if (p.flags & SDP_SYNC_NESTEROV) {
+    const T mu = static_cast<T>(p.momentum);
+    s1 = add_rn(mul_rn(s1, mu), g);
+    th = sub_rn(th, mul_rn(lr, add_rn(g, mul_rn(mu, s1))));
+  } else {
+    s1 = add_rn(mul_rn(static_cast<T>(p.beta1), s1), mul_rn(static_cast<T>(p.omb1), g));
+    s2 = add_rn(mul_rn(static_cast<T>(p.beta2), s2), mul_rn(mul_rn(static_cast<T>(p.omb2), g), g));
+    const T mh = div_rn(s1, static_cast<T>(p.bias1));
+    const T vh = div_rn(s2, static_cast<T>(p.bias2));
+    th = sub_rn(th, div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), static_cast<T>(p.eps))));
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void nesterov_elem(const SyncParams& p, int64_t j, T g) {
   T* th = static_cast<T*>(p.theta);
-  T* ve = static_cast<T*>(p.velocity);
-  const T mu = static_cast<T>(p.momentum), lr = static_cast<T>(p.lr);
-  const T v = add_rn(mul_rn(ve[j], mu), g);           // velocity *= mu; velocity += g
-  const T t = sub_rn(th[j], mul_rn(lr, add_rn(g, mul_rn(mu, v))));  // theta -= lr*(g + mu*v)
-  ve[j] = v;
+  T* s1 = static_cast<T*>(p.velocity);
+  T* s2 = static_cast<T*>(p.second_moment);
+  T t = th[j], a = s1[j], b = s2 ? s2[j] : static_cast<T>(0);
+  optim_step<T>(p, g, t, a, b);
+  s1[j] = a;
+  if (s2) s2[j] = b;
   th[j] = t;
   if (p.theta_bf16) static_cast<__nv_bfloat16*>(p.theta_bf16)[j] = to_bf16(t);
 }
@@ -169,7 +196,7 @@ __device__ __forceinline__ void emit_scalar(const SyncParams& p, int64_t j, uint
       if (p.has_shadow && p.shadow[w]) static_cast<__nv_bfloat16*>(p.shadow[w])[j] = to_bf16(mean);
     }
   }
-  if (p.flags & SDP_SYNC_NESTEROV) nesterov_elem<T>(p, j, mean);
+  if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) nesterov_elem<T>(p, j, mean);
 }
 
 // Epilogue for one vector of VN consecutive elements with a common owner set.
@@ -186,19 +213,16 @@ __device__ __forceinline__ void emit_vec(const SyncParams& p, int64_t j, uint64_
       if (p.has_shadow && p.shadow[w]) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.shadow[w]) + j, mean);
     }
   }
-  if (p.flags & SDP_SYNC_NESTEROV) {
+  if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
     T* thp = static_cast<T*>(p.theta) + j;
-    T* vep = static_cast<T*>(p.velocity) + j;
-    typename V<T>::type th = V<T>::ld_rw(thp), ve = V<T>::ld_rw(vep);
-    const T mu = static_cast<T>(p.momentum), lr = static_cast<T>(p.lr);
+    T* s1p = static_cast<T*>(p.velocity) + j;
+    T* s2p = p.second_moment ? static_cast<T*>(p.second_moment) + j : nullptr;
+    typename V<T>::type th = V<T>::ld_rw(thp), s1 = V<T>::ld_rw(s1p), s2 = s1;
+    if (s2p) s2 = V<T>::ld_rw(s2p);
 #pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      const T g = mean.x[e];
-      const T v = add_rn(mul_rn(ve.x[e], mu), g);
-      ve.x[e] = v;
-      th.x[e] = sub_rn(th.x[e], mul_rn(lr, add_rn(g, mul_rn(mu, v))));
-    }
-    V<T>::st(vep, ve);
+    for (int e = 0; e < VN; ++e) optim_step<T>(p, mean.x[e], th.x[e], s1.x[e], s2.x[e]);
+    V<T>::st(s1p, s1);
+    if (s2p) V<T>::st(s2p, s2);
     V<T>::st(thp, th);
     if (p.theta_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.theta_bf16) + j, th);
   }
@@ -345,7 +369,7 @@ __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, 
           }
       }
     }
-    if (p.flags & SDP_SYNC_NESTEROV) {
+    if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
 #pragma unroll
       for (int u = 0; u < EL; ++u) nesterov_elem<T>(p, j[u], mean[u]);
     }
@@ -451,9 +475,17 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   }
   if ((a->out && !aligned16(a->out)) || (a->out_bf16 && (reinterpret_cast<uintptr_t>(a->out_bf16) & 7u)))
     return set_error(SDP_ERR_USAGE, "output buffers are not 16-byte aligned");
-  if (a->flags & SDP_SYNC_NESTEROV) {
+  if ((a->flags & SDP_SYNC_NESTEROV) && (a->flags & SDP_SYNC_ADAM))
+    return set_error(SDP_ERR_CONFIG, "choose one fused optimizer: Nesterov or Adam");
+  if (a->flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
     if (!a->theta || !a->velocity || !aligned16(a->theta) || !aligned16(a->velocity))
-      return set_error(SDP_ERR_USAGE, "fused Nesterov needs 16-byte aligned theta and velocity");
+      return set_error(SDP_ERR_USAGE, "fused optimizer needs 16-byte aligned theta and moment buffers");
+  }
+  if (a->flags & SDP_SYNC_ADAM) {
+    if (!a->second_moment || !aligned16(a->second_moment))
+      return set_error(SDP_ERR_USAGE, "fused Adam needs a 16-byte aligned second-moment buffer");
+    if (!(a->bias1 > 0.0) || !(a->bias2 > 0.0))
+      return set_error(SDP_ERR_CONFIG, "Adam bias corrections must be positive (step >= 1)");
   }
   if (a->world > 1) {
     for (int r = 0; r < a->world; ++r)
@@ -478,6 +510,14 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   for (int r = 0; r < 8; ++r) p.pads[r] = r < a->world ? a->signal_pads[r] : nullptr;
   p.lr = a->lr;
   p.momentum = a->momentum;
+  p.second_moment = (a->flags & SDP_SYNC_ADAM) ? a->second_moment : nullptr;
+  p.beta1 = a->beta1;
+  p.beta2 = a->beta2;
+  p.omb1 = a->one_minus_beta1;
+  p.omb2 = a->one_minus_beta2;
+  p.bias1 = a->bias1;
+  p.bias2 = a->bias2;
+  p.eps = a->eps;
   p.total = a->total;
   p.timeout_cycles = a->timeout_cycles > 0 ? a->timeout_cycles : (int64_t)20000000000ll;
   p.n_workers = a->n_workers;

@@ -215,8 +215,8 @@ def owner_sync(replicas, assignment, **kw) -> torch.Tensor | None:
 def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
           out_bf16: torch.Tensor | None = None, writeback: bool = True,
           shadows_bf16=None, check_uncovered: bool = False, check_finite: bool = False,
-          nesterov: dict | None = None, status: torch.Tensor | None = None,
-          plan: SyncPlan | None = None) -> N.SyncArgs:
+          nesterov: dict | None = None, adam: dict | None = None,
+          status: torch.Tensor | None = None, plan: SyncPlan | None = None) -> N.SyncArgs:
     n, d = assignment.n_workers, assignment.topology.total
     reps = _as_replica_list(replicas, n, d)
     dt = reps[0].dtype
@@ -241,6 +241,8 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
             a.shadow_bf16[w] = None if sh is None else sh.data_ptr()
     a.out = None if out is None else out.data_ptr()
     a.out_bf16 = None if out_bf16 is None else out_bf16.data_ptr()
+    if nesterov is not None and adam is not None:
+        raise UsageError("choose one fused optimizer")
     if nesterov is not None:
         flags |= N.SYNC_NESTEROV
         a.theta = nesterov["theta"].data_ptr()
@@ -249,6 +251,21 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
         a.theta_bf16 = None if tb is None else tb.data_ptr()
         a.lr = float(nesterov["lr"])
         a.momentum = float(nesterov.get("momentum", 0.9))
+    if adam is not None:
+        # optim.Adam (optim.py:90-109): t is the step count after increment
+        flags |= N.SYNC_ADAM
+        b1, b2 = float(adam.get("beta1", 0.9)), float(adam.get("beta2", 0.999))
+        t = int(adam["t"])
+        a.theta = adam["theta"].data_ptr()
+        a.velocity = adam["m"].data_ptr()
+        a.second_moment = adam["v"].data_ptr()
+        tb = adam.get("theta_bf16")
+        a.theta_bf16 = None if tb is None else tb.data_ptr()
+        a.lr = float(adam["lr"])
+        a.beta1, a.beta2 = b1, b2
+        a.one_minus_beta1, a.one_minus_beta2 = 1 - b1, 1 - b2
+        a.bias1, a.bias2 = 1 - b1 ** t, 1 - b2 ** t
+        a.eps = float(adam.get("eps", 1e-8))
     a.status = None if status is None else status.data_ptr()
     a.flags = flags
     return a

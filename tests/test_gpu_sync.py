@@ -174,6 +174,40 @@ def test_fused_nesterov_matches_reference_step(cuda, dtype):
             assert np.array_equal(thb.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(t1))
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fused_adam_matches_reference_steps(cuda, dtype):
+    """SDP_SYNC_ADAM epilogue, two steps == reference optim.Adam (optim.py:90-109)."""
+    engine, _ = _pkg()
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    for case in G.cases(with_grads=True)[:6]:
+        a = _build(case)
+        masks = G.case_masks(case)
+        grads, _, _ = G.case_inputs(case, masks)
+        arr = G.arrays()
+        th = torch.from_numpy(arr[f"c{case['id']}_theta1"].astype(npdt)).to(cuda)
+        m = torch.zeros_like(th)
+        v = torch.zeros_like(th)
+        thb = torch.empty(case["d"], dtype=torch.bfloat16, device=cuda)
+        for t, scale in ((1, 1.0), (2, 0.5)):
+            reps = [torch.from_numpy((g * scale).astype(npdt)).to(cuda) for g in grads]
+            engine.owner_sync(reps, a, writeback=False,
+                              adam={"theta": th, "m": m, "v": v, "lr": 0.01, "t": t, "theta_bf16": thb})
+        if dtype == torch.float64:
+            # the scaled gradients aggregate to exactly 0.5 * gbar (power-of-two scaling)
+            assert np.array_equal(th.cpu().numpy().view(np.uint64), arr[f"c{case['id']}_adam_theta2"].view(np.uint64))
+            assert np.array_equal(m.cpu().numpy().view(np.uint64), arr[f"c{case['id']}_adam_m2"].view(np.uint64))
+            assert np.array_equal(v.cpu().numpy().view(np.uint64), arr[f"c{case['id']}_adam_v2"].view(np.uint64))
+        else:
+            g32 = [grads.astype(np.float32), (grads * 0.5).astype(np.float32)]
+            t0 = arr[f"c{case['id']}_theta1"].astype(np.float32)
+            mm, vv = np.zeros_like(t0), np.zeros_like(t0)
+            for t, gs in ((1, g32[0]), (2, g32[1])):
+                gbar = O.aggregate_f32_ordered(list(gs), masks)
+                t0, mm, vv = O.adam_update(t0, mm, vv, gbar, 0.01, t)
+            assert np.array_equal(th.cpu().numpy().view(np.uint32), t0.view(np.uint32))
+            assert np.array_equal(thb.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(t0))
+
+
 def test_standalone_nesterov_and_nonfinite(cuda):
     engine, _ = _pkg()
     from paper_2507_09029_b200.errors import NumericalError

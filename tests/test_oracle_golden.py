@@ -50,6 +50,15 @@ def test_oracle_aggregate_bitexact_f64(case):
     th, v = O.nesterov_update(theta0, vel0, ref, 0.05, 0.9)
     assert np.array_equal(th.view(np.uint64), G.arrays()[f"c{case['id']}_theta1"].view(np.uint64))
     assert np.array_equal(v.view(np.uint64), G.arrays()[f"c{case['id']}_vel1"].view(np.uint64))
+    # Adam (optim.py:90-109): two steps from theta1 with zero moments
+    m = np.zeros_like(th)
+    vv = np.zeros_like(th)
+    th, m, vv = O.adam_update(th, m, vv, ref, 0.01, 1)
+    th, m, vv = O.adam_update(th, m, vv, ref * 0.5, 0.01, 2)
+    arr = G.arrays()
+    assert np.array_equal(th.view(np.uint64), arr[f"c{case['id']}_adam_theta2"].view(np.uint64))
+    assert np.array_equal(m.view(np.uint64), arr[f"c{case['id']}_adam_m2"].view(np.uint64))
+    assert np.array_equal(vv.view(np.uint64), arr[f"c{case['id']}_adam_v2"].view(np.uint64))
 
 
 def test_known_answer_disjoint_masks():
