@@ -290,6 +290,27 @@ int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
                void* out, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Gradient-alignment diagnostic (diagnostics.py:33-78)                      */
+/* ------------------------------------------------------------------------ */
+
+/* A chunk [offset, offset + length) of segment `segment` (one layer's slice). */
+typedef struct {
+  int64_t offset;
+  int64_t length;
+  int32_t segment;
+  int32_t pad_;
+} sdp_reduce_task;
+
+/* Per segment s: out[4s..4s+3] = (sum a*b, sum a*a, sum b*b, count) over the
+ * elements with support[j] != 0 (support = NULL: all), accumulated in float64.
+ * partials: [n_tasks * 4] float64 scratch.  Deterministic (fixed-order
+ * second pass, no float atomics).  The restricted cosine is
+ * ab / (sqrt(aa) * sqrt(bb)) (diagnostics.py:43-47). */
+int sdp_restricted_dots(int dtype, const void* a, const void* b, const uint8_t* support,
+                        const sdp_reduce_task* tasks, int n_tasks, int n_segments,
+                        double* partials, double* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Cross-process peer mapping (multi-GPU owner sync)                         */
 /* ------------------------------------------------------------------------ */
 

@@ -116,6 +116,7 @@ SIGNATURES = {
     "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, VP]),
     "sdp_scatter_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
     "sdp_divide": (C.c_int, [I32, VP, VP, I64, VP, VP]),
+    "sdp_restricted_dots": (C.c_int, [I32, VP, VP, VP, VP, I32, I32, VP, VP, VP]),
     "sdp_ipc_export": (C.c_int, [VP, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
     "sdp_ipc_import": (C.c_int, [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_void_p)]),
     "sdp_ipc_close": (C.c_int, [VP]),

@@ -55,6 +55,13 @@ def main() -> None:
             # multiply mode gives the same loss
             loss_m, _, _ = masked_forward(model, view, xs[w], ys[w], block_mode="multiply")
             arrays[f"m{ci}_lossmul_w{w}"] = np.array([float(loss_m.data)])
+        # gradient alignment (diagnostics.py:50-78) per worker on its first batch
+        from subnetdp.diagnostics import gradient_alignment
+        layers = [p.name for p in model.topology.params if p.kind in ("conv_w", "linear_w")]
+        align = []
+        for w in range(n):
+            samples = gradient_alignment(model, a.worker_view(w), xs[w], ys[w], layers)
+            align.append([[s.layer, s.cosine, s.reason] for s in samples])
         # two protocol steps: worker w uses batch (step*n + w)
         opt = SgdNesterov(model.topology.total, momentum=0.9)
         lrs = [0.1, 0.05]
@@ -73,7 +80,7 @@ def main() -> None:
         manifest["cases"].append({"id": ci, "kind": kind, "kw": {k: (list(v) if isinstance(v, tuple) else v)
                                                                  for k, v in kw.items()},
                                   "strategy": strategy, "n": n, "p": p, "seed": seed, "lrs": lrs,
-                                  "d": model.topology.total})
+                                  "d": model.topology.total, "alignment": align})
     np.savez_compressed(HERE / "models.npz", **arrays)
     (HERE / "models.json").write_text(json.dumps(manifest, indent=1))
     print("ok", {k: v.shape for k, v in list(arrays.items())[:4]})

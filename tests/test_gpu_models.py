@@ -141,6 +141,35 @@ def test_compact_aggregate_bitexact_vs_full_aggregate(cuda, ci):
 
 
 @pytest.mark.parametrize("ci", _case_ids())
+def test_gradient_alignment_matches_reference(cuda, ci):
+    """diagnostics.gradient_alignment (diagnostics.py:50-78) on the GPU reduction:
+    same cosines within 1e-10, same absent-reason where the support is empty."""
+    from paper_2507_09029_b200 import diagnostics
+    c, arr, m, a = _setup(ci, cuda)
+    layers = [p.name for p in m.topology.params if p.kind in ("conv_w", "linear_w")]
+    for w in range(c["n"]):
+        got = diagnostics.gradient_alignment(m, a.worker_view(w), arr[f"m{ci}_x{w}"], arr[f"m{ci}_y{w}"], layers)
+        want = c["alignment"][w]
+        assert [s.layer for s in got] == [x[0] for x in want]
+        for s, (_, cos, reason) in zip(got, want):
+            assert s.reason == reason
+            if cos is None:
+                assert s.cosine is None
+            else:
+                assert abs(s.cosine - cos) <= 1e-10
+
+
+def test_restricted_cosine_edge_cases(cuda):
+    from paper_2507_09029_b200 import diagnostics
+    a = torch.tensor([1.0, 2.0, 0.0], device=cuda, dtype=torch.float64)
+    b = torch.tensor([2.0, 4.0, 5.0], device=cuda, dtype=torch.float64)
+    assert diagnostics.restricted_cosine(a, b, torch.tensor([0, 0, 0], device=cuda)) == (None, "empty-support")
+    assert diagnostics.restricted_cosine(a, b, torch.tensor([0, 0, 1], device=cuda)) == (None, "zero-norm")
+    cos, reason = diagnostics.restricted_cosine(a, b, torch.tensor([1, 1, 0], device=cuda))
+    assert reason is None and abs(cos - 1.0) < 1e-15
+
+
+@pytest.mark.parametrize("ci", _case_ids())
 def test_two_protocol_steps_match_reference(cuda, ci):
     """per-worker masked grads -> owner sync with fused Nesterov, twice
     (engine.py:202-223): theta within 1e-10 of the reference's."""
