@@ -105,9 +105,12 @@ int sdp_ipc_close(void* ptr) {
 }
 
 int sdp_enable_peer(int peer) {
-  int dev = 0;
+  int dev = 0, count = 0;
   SDP_CUDA_CHECK(cudaGetDevice(&dev));
+  SDP_CUDA_CHECK(cudaGetDeviceCount(&count));
   if (peer == dev) return SDP_OK;
+  if (peer < 0 || peer >= count)
+    return sdp::set_error(SDP_ERR_USAGE, "peer device %d outside [0, %d)", peer, count);
   int can = 0;
   SDP_CUDA_CHECK(cudaDeviceCanAccessPeer(&can, dev, peer));
   if (!can) return sdp::set_error(SDP_ERR_CUDA, "device %d cannot access peer %d", dev, peer);

@@ -19,9 +19,11 @@ int set_error(int code, const char* fmt, ...);
 #define SDP_CUDA_CHECK(expr)                                                      \
   do {                                                                            \
     cudaError_t e_ = (expr);                                                      \
-    if (e_ != cudaSuccess)                                                        \
+    if (e_ != cudaSuccess) {                                                      \
+      cudaGetLastError(); /* consume it: a later launch check must not see it */  \
       return ::sdp::set_error(SDP_ERR_CUDA, "%s failed: %s", #expr,               \
                               cudaGetErrorString(e_));                            \
+    }                                                                             \
   } while (0)
 
 #define SDP_LAUNCH_CHECK()                                                        \
