@@ -1,0 +1,35 @@
+"""bench.py's torchrun (N > 1) path end to end on ONE GPU: two ranks share
+device 0 (SDP_BENCH_SAME_DEVICE), plumbing over gloo, data path over CUDA IPC
+with the cross-rank flag barriers.  Timing is meaningless here (the two
+processes' kernels are time-sliced); the test checks the path runs and emits
+the contract's JSON line."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_torchrun_two_ranks_same_device(cuda):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, SDP_BENCH_SAME_DEVICE="1", SDP_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "5", "--warmup", "3"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpu_launches"] == 5 and d["value"] > 0
+    assert "nvlink_frac" in d["roofline"]

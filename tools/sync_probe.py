@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--no-shadow", action="store_true")
     ap.add_argument("--no-writeback", action="store_true")
     ap.add_argument("--tile", type=int, default=None)
+    ap.add_argument("--tpc1", action="store_true", help="one tile per CTA (grid = #tiles)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     if args.workload == "resnet18":
@@ -43,7 +44,10 @@ def main():
     reps = [torch.randn(d, device=dev) * a.param_masks[w] for w in range(args.n)]
     shadows = None if args.no_shadow else [torch.zeros(d, dtype=torch.bfloat16, device=dev) for _ in reps]
     out = torch.empty(d, device=dev) if args.no_writeback else None
-    plan = a.sync_plan(tile=args.tile)
+    kw = {"tile": args.tile}
+    if args.tpc1:
+        kw["force_grid"] = -(-d // (args.tile or engine.auto_tile(d, 148)))  # one tile per CTA
+    plan = a.sync_plan(**kw)
     prep = engine.PreparedSync(reps, a, writeback=not args.no_writeback, shadows_bf16=shadows,
                                out=out, plan=plan)
     per = (4 + (0 if args.no_writeback else 4) + (0 if (args.no_shadow or args.no_writeback) else 2))
