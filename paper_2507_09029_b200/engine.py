@@ -45,10 +45,16 @@ def _sm_count() -> int:
     return int(n.value)
 
 
-def auto_tile(d: int, sms: int) -> int:
-    """2048-element tiles, or 1024 when that leaves fewer than two full waves
-    of resident CTAs (small buffers are latency-bound: more, shorter CTAs)."""
-    return TILE if -(-d // TILE) >= 2 * sms * CTAS_PER_SM else TILE // 2
+def auto_tile(d: int, sms: int, avg_owners: float = 4.0) -> int:
+    """2048-element tiles; 1024 when that leaves fewer than two full waves of
+    resident CTAs (small buffers are latency-bound: more, shorter CTAs); 4096
+    for large buffers with ~2 owners per element, where a 2048-tile CTA moves
+    too few bytes (same-box A/B, 256 MiB P=2: 0.977 vs 0.893-0.95)."""
+    if -(-d // TILE) < 2 * sms * CTAS_PER_SM:
+        return TILE // 2
+    if avg_owners < 2.5 and d * avg_owners * 10 >= BIG_TRAFFIC / 2:
+        return 2 * TILE
+    return TILE
 
 
 def gpu_of_worker(n_workers: int, world: int) -> np.ndarray:
@@ -76,14 +82,26 @@ def tile_leaders(tiles: np.ndarray, gpu_of: np.ndarray, world: int) -> np.ndarra
     return out
 
 
-def plan_grid(n_tiles: int, sms: int, resident: bool) -> int:
-    """Persistent grid for co-residency (cross-rank barrier); otherwise one
-    CTA per tile -- the hardware scheduler then balances the 8 KB-per-replica
-    work units itself (measured: 98% / 101% of the copy peak at 498 MB / 1 GiB,
-    vs 93% / 94% with a capped grid of several tiles per CTA)."""
+BIG_TRAFFIC = 1.5e9  # bytes per launch above which one CTA per tile wins
+
+
+def plan_grid(n_tiles: int, sms: int, resident: bool, traffic: float = 0.0) -> int:
+    """Grid of the sync launch (tools/grid_ab.py, same-box A/B, fraction of the
+    measured copy peak):
+
+        workload (P=4)     traffic   one tile/CTA   capped grid (8 waves)
+        ResNet-18          0.64 GB      0.898           0.947
+        sweep 256 MiB      2.7 GB       1.004           0.949
+        GPT-2 124M         6.5 GB       0.976           0.941
+
+    so one CTA per tile above BIG_TRAFFIC, a grid capped at 8 waves of
+    resident CTAs below it, and a persistent grid for co-residency (the
+    cross-rank barrier)."""
     if resident:
         return max(1, min(n_tiles, sms * CTAS_PER_SM))
-    return max(1, min(n_tiles, 2**31 - 1))
+    if traffic >= BIG_TRAFFIC:
+        return max(1, min(n_tiles, 2**31 - 1))
+    return max(1, min(n_tiles, sms * CTAS_PER_SM * 8))
 
 
 def cta_major(tiles: np.ndarray, grid: int, tiles_per_cta: int) -> np.ndarray:
@@ -112,8 +130,9 @@ class SyncPlan:
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
+        owned_total = assignment.owned_total()
         if tile is None:
-            tile = auto_tile(d, _sm_count())
+            tile = auto_tile(d, _sm_count(), owned_total / max(1, d))
         self.tile = tile
         self.world, self.rank = world, rank
         n_tiles = (d + tile - 1) // tile
@@ -134,13 +153,11 @@ class SyncPlan:
             mine = mine[(mine["tile_index"] >= lo) & (mine["tile_index"] < hi)]
         self.n_tiles = len(mine)
         # every CTA must be co-resident for the cross-rank flag barrier
-        self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1)
+        self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1,
+                              traffic=10.0 * owned_total / world)
         if max_grid:
             self.grid = max(1, min(self.grid, max_grid))
         self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
-        if not (resident or world > 1 or max_grid):
-            # equal tile counts per CTA: shrink the grid to ceil(n / tiles_per_cta)
-            self.grid = max(1, -(-self.n_tiles // self.tiles_per_cta))
         if force_grid:
             self.grid = int(force_grid)  # all ranks launch the same grid (pairwise barrier)
             self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))

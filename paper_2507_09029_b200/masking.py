@@ -347,6 +347,12 @@ class MaskAssignment:
             self._uncovered = int((self.coverage == 0).sum().item())
         return self._uncovered
 
+    def owned_total(self) -> int:
+        """sum_j |O_j| -- replica elements one sync reads (cached)."""
+        if getattr(self, "_owned_total", None) is None:
+            self._owned_total = int(self.coverage.sum().item())
+        return self._owned_total
+
     def host_divisor(self) -> np.ndarray:
         """Read-only numpy copy of `divisor` (cached; the reference's type)."""
         if getattr(self, "_host_divisor", None) is None:

@@ -61,7 +61,8 @@ def test_cta_major_table_covers_every_tile_once():
 def test_plan_grid_residency():
     assert engine.plan_grid(10, 148, True) == 10
     assert engine.plan_grid(10_000, 148, True) == 148 * engine.CTAS_PER_SM
-    assert engine.plan_grid(10_000, 148, False) == 10_000
+    assert engine.plan_grid(10_000, 148, False) == min(10_000, 148 * engine.CTAS_PER_SM * 8)
+    assert engine.plan_grid(100_000, 148, False, traffic=2e9) == 100_000
 
 
 def test_rank_layout_errors():
