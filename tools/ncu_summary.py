@@ -38,7 +38,7 @@ def launches(src, out):
     for r in rows[hi + 1:]:
         if len(r) > vi:
             v = float(r[vi].replace(",", ""))
-            v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(r[ui], 1)
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1)
             agg[r[ki]].append(v)
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# launch list: {Path(src).name}", "",
