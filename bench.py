@@ -442,10 +442,10 @@ def run_train(args, dev):
                 torch.randint(0, 10, (batch,), generator=gen, device=dev)) for _ in range(n)]
     out = {"workload": f"ResNet-18 CIFAR-shape, N={n} co-resident workers, batch {batch}/worker, "
                        "bf16 autocast fwd/bwd, fused sync+Nesterov+bf16 cast", "data": "synthetic"}
-    for tag, p in (("subnet", args.p), ("dp", n)):
+    for tag, p, strategy in (("subnet", args.p, "block"), ("widthwise", args.p, "neuron"), ("dp", n, "block")):
         model = train.build_resnet18(dev)
-        a = masking.build_assignment(model.topology, "block", n, p, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=0.01)
+        a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=0.001)
         out[f"{tag}_loss_first"] = float(tr.step(batches).item())
         for _ in range(2):
             tr.step(batches)
@@ -467,6 +467,11 @@ def run_train(args, dev):
         torch.cuda.empty_cache()
     out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
     out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
+    out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_worker_bytes"]
+                                            / out["dp_peak_mem_per_worker_bytes"])
+    out["configs"] = {"subnet": "configs[1] C2: block dropping P=4", "widthwise": "configs[2] C3: "
+                      "channel-slice compact subnetworks (gather/scatter kernels) P=4",
+                      "dp": "full-replica DP comparator (P=N)"}
     out["note"] = ("peak memory = one worker's compact fp32 master + grad + momentum + bf16 copy + "
                    "activations of its fwd/bwd, i.e. what a GPU holding that worker needs (N = G)")
     return out

@@ -70,8 +70,23 @@ def active_group_norm(x, groups: int, gamma, beta, active: torch.Tensor, eps: fl
     return _group_norm_by_membership(x, member, gamma, beta, eps)
 
 
-def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: float = 1e-5):
-    """Compact channels, each tagged with its original norm group (F4: ragged)."""
+def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: float = 1e-5,
+                      counts: tuple[int, ...] | None = None):
+    """Compact channels, each tagged with its original norm group (F4: ragged).
+
+    Compact channels keep ascending original order, so each group's live
+    channels are contiguous: with the per-group `counts` known, equal counts
+    (the grouped assignment's balanced case) are one fused F.group_norm and
+    unequal ones are a few contiguous F.group_norm(., 1) calls."""
+    if counts is not None:
+        if len(set(counts)) == 1:
+            return F.group_norm(x, len(counts), gamma, beta, eps)
+        outs, pos = [], 0
+        for c in counts:
+            if c:
+                outs.append(F.group_norm(x[:, pos:pos + c], 1, gamma[pos:pos + c], beta[pos:pos + c], eps))
+            pos += c
+        return torch.cat(outs, dim=1)
     member = F.one_hot(group_of.to(torch.long), groups)
     return _group_norm_by_membership(x, member, gamma, beta, eps)
 
@@ -358,6 +373,21 @@ class SubnetLayout:
 
     def present(self, name: str) -> bool:
         return self.present_map[name] and int(np.prod(self.shapes[name])) > 0
+
+    def group_counts(self, layer_id: str, channels: int, groups: int) -> tuple[int, ...]:
+        """Live channels per original norm group (ragged)."""
+        key = (layer_id, channels, groups)
+        if not hasattr(self, "_gcounts"):
+            self._gcounts = {}
+        if key not in self._gcounts:
+            t = self.live_channels.get(layer_id)
+            gsize = channels // groups
+            if t is None:
+                self._gcounts[key] = (gsize,) * groups
+            else:
+                idx = t.cpu().numpy()
+                self._gcounts[key] = tuple(int(v) for v in np.bincount(idx // gsize, minlength=groups))
+        return self._gcounts[key]
 
     def channels(self, layer_id: str, c: int) -> torch.Tensor:
         t = self.live_channels.get(layer_id)

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.nn.functional as F
 
@@ -39,6 +40,16 @@ class ResNet18Cifar:
     def build_topology(self):
         return self.topology
 
+    def _gn(self, x, gamma, beta, worker, layer_id):
+        """GroupNorm; over the worker's live channels only when some are dead
+        (ops.py:140-204: dead channels output exact zeros)."""
+        flags = None if worker is None else worker.channel_active.get(layer_id)
+        if flags is None or bool(np.all(flags)):
+            return F.group_norm(x, self.norm_groups, gamma, beta)
+        from .models import active_group_norm
+        act = torch.as_tensor(np.array(flags, dtype=bool), device=x.device)
+        return active_group_norm(x, self.norm_groups, gamma, beta, act)
+
     def forward(self, params, x, worker=None, block_mode: str = "skip"):
         g = self.norm_groups
         h = F.conv2d(x, params["conv1.w"], padding=1)
@@ -48,9 +59,9 @@ class ResNet18Cifar:
             if not live and block_mode == "skip":
                 continue  # a dropped block is the identity and is never executed
             o = F.conv2d(h, params[f"{p}.conv1.w"], stride=stride, padding=1)
-            o = F.relu(F.group_norm(o, g, params[f"{p}.gn1.gamma"], params[f"{p}.gn1.beta"]))
+            o = F.relu(self._gn(o, params[f"{p}.gn1.gamma"], params[f"{p}.gn1.beta"], worker, f"{p}.conv1"))
             o = F.conv2d(o, params[f"{p}.conv2.w"], padding=1)
-            o = F.group_norm(o, g, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"])
+            o = self._gn(o, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"], worker, f"{p}.conv2")
             if down:
                 sc = F.conv2d(h, params[f"{p}.down.w"], stride=stride)
                 sc = F.group_norm(sc, g, params[f"{p}.down_gn.gamma"], params[f"{p}.down_gn.beta"])
@@ -60,6 +71,36 @@ class ResNet18Cifar:
                 o = o * 0.0
             h = F.relu(o + sc)
         return F.linear(h.mean(dim=(2, 3)), params["fc.w"], params["fc.b"])
+
+    def forward_compact(self, cp, x, sub):
+        """Width-wise subnetwork (config C3): cp holds only the worker's live
+        conv1/conv2 channels (models.SubnetLayout); GroupNorm statistics over
+        the live channels of each original group (ragged); the
+        block output is scattered back into the residual stream's channels."""
+        from .models import ragged_group_norm
+        g = self.norm_groups
+        h = F.conv2d(x, cp["conv1.w"], padding=1)
+        h = F.relu(F.group_norm(h, g, cp["gn1.gamma"], cp["gn1.beta"]))
+        for p, stride, down in self.block_plan:
+            if not sub.present(f"{p}.conv1.w"):
+                continue
+            planes = self.topology.index[f"{p}.conv1.w"].shape[0]
+            gsize = planes // g
+            a1 = sub.channels(f"{p}.conv1", planes)
+            a2 = sub.channels(f"{p}.conv2", planes)
+            o = F.conv2d(h, cp[f"{p}.conv1.w"], stride=stride, padding=1)
+            o = F.relu(ragged_group_norm(o, a1 // gsize, g, cp[f"{p}.gn1.gamma"], cp[f"{p}.gn1.beta"],
+                                         counts=sub.group_counts(f"{p}.conv1", planes, g)))
+            o = F.conv2d(o, cp[f"{p}.conv2.w"], padding=1)
+            o = ragged_group_norm(o, a2 // gsize, g, cp[f"{p}.gn2.gamma"], cp[f"{p}.gn2.beta"],
+                                  counts=sub.group_counts(f"{p}.conv2", planes, g))
+            if down:
+                sc = F.conv2d(h, cp[f"{p}.down.w"], stride=stride)
+                sc = F.group_norm(sc, g, cp[f"{p}.down_gn.gamma"], cp[f"{p}.down_gn.beta"])
+            else:
+                sc = h
+            h = F.relu(sc.index_add(1, a2, o.to(sc.dtype)))
+        return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 
 def param_views(topology, flat: torch.Tensor) -> dict:
@@ -81,10 +122,16 @@ class SubnetTrainer:
     written by the sync kernel's epilogue."""
 
     def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
-                 autocast: bool = True):
+                 autocast: bool = True, compact: bool | None = None):
         self.model = model
         self.assignment = assignment
         self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
+        # width-wise (neuron) workers run their compact subnetwork: gather ->
+        # dense compact fwd/bwd -> scatter into the worker's flat gradient
+        self.compact = assignment.strategy == "neuron" if compact is None else compact
+        if self.compact:
+            from .models import SubnetLayout
+            self.subs = [SubnetLayout(assignment, w) for w in range(assignment.n_workers)]
         d = model.topology.total
         dev = model.theta.device
         self.velocity = torch.zeros(d, device=dev)
@@ -108,6 +155,16 @@ class SubnetTrainer:
         topo = self.model.topology
         losses = []
         for w, (x, y) in enumerate(batches):
+            if self.compact:
+                sub = self.subs[w]
+                leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                    logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
+                    loss = F.cross_entropy(logits.float(), y)
+                (g,) = torch.autograd.grad(loss, leaf)
+                sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
+                losses.append(loss.detach())
+                continue
             # the worker trains on the bf16 weights the previous sync wrote
             leaf = (self.theta_bf16 if self.autocast else self.model.theta).detach().requires_grad_(True)
             params = param_views(topo, leaf)
@@ -157,7 +214,11 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
     momentum = torch.zeros_like(master)
     shadow = master.detach().to(torch.bfloat16)
     with torch.autocast("cuda", dtype=torch.bfloat16):
-        loss = F.cross_entropy(model.arch.forward(sub.views(master), x, view).float(), y)
+        if assignment.strategy == "neuron":
+            logits = model.arch.forward_compact(sub.views(master), x, sub)
+        else:
+            logits = model.arch.forward(sub.views(master), x, view)
+        loss = F.cross_entropy(logits.float(), y)
     loss.backward()
     torch.cuda.synchronize(dev)
     peak = torch.cuda.max_memory_allocated(dev) - base

@@ -30,6 +30,52 @@ def test_resnet18_subnet_step_matches_oracle(cuda):
     assert np.array_equal(tr.theta_bf16.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(th1))
 
 
+def test_resnet18_width_wise_compact_equals_masked_full(cuda):
+    """C3: gather -> compact ResNet-18 fwd/bwd (ragged GN) -> scatter equals the
+    reference semantics (theta*mask through the full model, active-channel GN)."""
+    import torch.nn.functional as F
+    from paper_2507_09029_b200 import masking, models, train
+    model = train.build_resnet18(cuda, seed=2)
+    model.theta = model.theta.double()
+    a = masking.build_assignment(model.topology, "neuron", 8, 4, seed=1)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(3)
+    x = torch.randn(2, 3, 32, 32, generator=gen, device=cuda, dtype=torch.float64)
+    y = torch.randint(0, 10, (2,), generator=gen, device=cuda)
+    for w in (0, 5):
+        view = a.worker_view(w)
+        leaf = models._extract(model.theta, view).requires_grad_(True)
+        loss_f = F.cross_entropy(model.arch.forward(train.param_views(model.topology, leaf), x, view), y)
+        (g_f,) = torch.autograd.grad(loss_f, leaf)
+        sub = models.SubnetLayout(a, w)
+        leaf_c = sub.gather(model.theta).requires_grad_(True)
+        loss_c = F.cross_entropy(model.arch.forward_compact(sub.views(leaf_c), x, sub), y)
+        (g_c,) = torch.autograd.grad(loss_c, leaf_c)
+        g_c = sub.scatter(g_c)
+        assert abs(loss_f.item() - loss_c.item()) <= 1e-12 * abs(loss_f.item())
+        assert torch.max(torch.abs(g_f - g_c)).item() <= 1e-10 * max(1.0, torch.max(torch.abs(g_f)).item())
+        assert torch.all(g_c[~view.param_mask_bool] == 0)
+
+
+def test_resnet18_width_wise_step_matches_oracle(cuda):
+    from paper_2507_09029_b200 import masking, train
+    model = train.build_resnet18(cuda, seed=3)
+    a = masking.build_assignment(model.topology, "neuron", 8, 4, seed=1)
+    tr = train.SubnetTrainer(model, a, lr=0.05, autocast=False)
+    assert tr.compact
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(0)
+    batches = [(torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
+                torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(8)]
+    th0 = model.theta.cpu().numpy().copy()
+    tr.step(batches)
+    grads = [g.cpu().numpy() for g in tr.grads]
+    masks = a.param_masks.cpu().numpy()
+    gbar = O.aggregate_f32_ordered(grads, masks)
+    th1, _ = O.nesterov_update(th0, np.zeros_like(th0), gbar, 0.05, 0.9)
+    assert np.array_equal(model.theta.cpu().numpy().view(np.uint32), th1.astype(np.float32).view(np.uint32))
+
+
 def test_memory_subnet_below_full_replica(cuda):
     from paper_2507_09029_b200 import masking, train
     model = train.build_resnet18(cuda)
