@@ -347,6 +347,7 @@ def run_ours(args):
         e2e = run_e2e(args, a, dev, total_bytes)
         if not args.no_train and args.workload == "resnet18":
             train = run_train(args, dev)
+            train["c4_gpt2"] = run_train_gpt2(args, dev)
         if not args.no_cpu_baseline:
             cpu = run_cpu_baseline(args, topo)
     if rank == 0:
@@ -474,6 +475,50 @@ def run_train(args, dev):
                       "dp": "full-replica DP comparator (P=N)"}
     out["note"] = ("peak memory = one worker's compact fp32 master + grad + momentum + bf16 copy + "
                    "activations of its fwd/bwd, i.e. what a GPU holding that worker needs (N = G)")
+    return out
+
+
+def run_train_gpt2(args, dev, micro_batch: int = 8, seq: int = 1024):
+    """configs[3] C4: GPT-2 small, seq 1024, block dropping P=4, N=8 co-resident
+    workers x micro-batch 8: tokens/s/GPU and peak memory per worker vs DP."""
+    import torch
+
+    from paper_2507_09029_b200 import masking, train
+    n = args.n_logical
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    batches = [(lambda t: (t, t))(torch.randint(0, 50257, (micro_batch, seq), generator=gen, device=dev))
+               for _ in range(n)]
+    out = {"workload": f"GPT-2 small 124M, seq {seq}, N={n} co-resident workers x micro-batch "
+                       f"{micro_batch}, bf16 autocast, flash SDPA, fused sync+Nesterov+bf16", "data": "synthetic tokens"}
+    for tag, p in (("subnet", args.p), ("dp", n)):
+        model = train.build_gpt2(dev)
+        a = masking.build_assignment(model.topology, "block", n, p, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=1e-4, loss_fn=train.lm_loss)
+        out[f"{tag}_loss_first"] = float(tr.step(batches).item())
+        tr.step(batches)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(2, args.train_steps // 2)
+        s.record()
+        for _ in range(steps):
+            loss = tr.step(batches)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / steps
+        out[f"{tag}_ms_per_step"] = ms
+        out[f"{tag}_tokens_per_s_per_gpu"] = n * micro_batch * seq / (ms / 1e3)
+        out[f"{tag}_loss_last"] = float(loss.item())
+        del tr
+        torch.cuda.empty_cache()
+        mk = lambda: (batches[0][0], batches[0][1])  # noqa: E731
+        mems = [train.worker_memory(model, a, w if p < n else None, micro_batch, dev, mk, train.lm_loss)["peak_bytes"]
+                for w in ((0, n - 1) if p < n else (0,))]
+        out[f"{tag}_peak_mem_per_worker_bytes"] = max(mems)
+        del model, a
+        torch.cuda.empty_cache()
+    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
+    out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
     return out
 
 

@@ -103,6 +103,68 @@ class ResNet18Cifar:
         return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 
+class GPT2Small:
+    """BASELINE configs[3] (C4): GPT-2 small over zoo.gpt2_small_topology's flat
+    layout -- pre-LN blocks, HF Conv1D weights ([in, out]), causal flash SDPA,
+    tanh-GELU, tied LM head.  Block dropping skips whole blocks (the residual
+    stream passes through), exactly like models.py:161-163 does for CNN blocks."""
+
+    def __init__(self, vocab=50257, n_ctx=1024, d_model=768, n_layer=12, n_head=12):
+        self.vocab, self.n_ctx, self.d_model, self.n_layer, self.n_head = vocab, n_ctx, d_model, n_layer, n_head
+        self.topology = zoo.gpt2_small_topology(vocab, n_ctx, d_model, n_layer, n_ctx)
+
+    def build_topology(self):
+        return self.topology
+
+    def forward(self, params, tokens, worker=None, block_mode: str = "skip"):
+        b, t = tokens.shape
+        e, nh = self.d_model, self.n_head
+        h = F.embedding(tokens, params["wte"]) + params["wpe"][:t][None]
+        for i in range(self.n_layer):
+            live = True if worker is None else bool(worker.block_active[i])
+            if not live and block_mode == "skip":
+                continue
+            p = f"h{i}"
+            a = F.layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
+            qkv = torch.addmm(params[f"{p}.attn.c_attn.b"], a.reshape(b * t, e), params[f"{p}.attn.c_attn.w"])
+            q, k, v = qkv.view(b, t, 3, nh, e // nh).permute(2, 0, 3, 1, 4)
+            y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+            y = y.transpose(1, 2).reshape(b * t, e)
+            y = torch.addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
+            m = F.layer_norm(h + y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
+            m = F.gelu(torch.addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
+                       approximate="tanh")
+            m = torch.addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
+            o = y + m
+            if not live:
+                o = o * 0.0
+            h = h + o
+        h = F.layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
+        return h @ params["wte"].t()  # tied head: [B, T, vocab]
+
+
+def lm_loss(logits, tokens):
+    """Next-token cross entropy."""
+    return F.cross_entropy(logits[:, :-1].reshape(-1, logits.shape[-1]).float(), tokens[:, 1:].reshape(-1))
+
+
+def build_gpt2(dev, seed: int = 1) -> GlobalModel:
+    arch = GPT2Small()
+    topo = arch.topology
+    m = GlobalModel(arch=arch, topology=topo, theta=torch.zeros(topo.total, device=dev))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    th = torch.zeros(topo.total, device=dev)
+    for spec in topo.params:  # GPT-2 init: N(0, 0.02) weights/embeddings, LN gain 1, biases 0
+        sl = slice(spec.offset, spec.offset + spec.size)
+        if spec.kind in ("linear_w", "embed"):
+            th[sl] = torch.randn(spec.size, generator=gen, device=dev) * 0.02
+        elif spec.kind == "norm_w":
+            th[sl] = 1.0
+    m.theta = th
+    return m
+
+
 def param_views(topology, flat: torch.Tensor) -> dict:
     return {p.name: flat[p.offset:p.offset + p.size].view(p.shape) for p in topology.params}
 
@@ -122,9 +184,10 @@ class SubnetTrainer:
     written by the sync kernel's epilogue."""
 
     def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
-                 autocast: bool = True, compact: bool | None = None):
+                 autocast: bool = True, compact: bool | None = None, loss_fn=None):
         self.model = model
         self.assignment = assignment
+        self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
         self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
         # width-wise (neuron) workers run their compact subnetwork: gather ->
         # dense compact fwd/bwd -> scatter into the worker's flat gradient
@@ -160,7 +223,8 @@ class SubnetTrainer:
                 leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
                     logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
-                    loss = F.cross_entropy(logits.float(), y)
+                    loss = self.loss_fn(logits, y)
+                del logits
                 (g,) = torch.autograd.grad(loss, leaf)
                 sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
                 losses.append(loss.detach())
@@ -170,7 +234,8 @@ class SubnetTrainer:
             params = param_views(topo, leaf)
             with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
                 logits = self.model.arch.forward(params, x, self.views[w])
-                loss = F.cross_entropy(logits.float(), y)
+                loss = self.loss_fn(logits, y)
+            del logits
             (g,) = torch.autograd.grad(loss, leaf)
             self.grads[w].copy_(g)  # fp32 gradient replica of worker w
             losses.append(loss.detach())
@@ -189,7 +254,7 @@ def build_resnet18(dev, seed: int = 1) -> GlobalModel:
 
 
 def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int,
-                  dev) -> dict:
+                  dev, make_batch=None, loss_fn=None) -> dict:
     """Peak device memory of ONE worker's training state and step, as a GPU
     holding one worker would see it (paper: params, grads, optimizer state and
     activations all scale with the subnetwork).  worker=None: the full model
@@ -203,8 +268,12 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
         worker = 0
     sub = SubnetLayout(assignment, worker)
     view = assignment.worker_view(worker)
-    x = torch.randn(batch, 3, 32, 32, device=dev)
-    y = torch.randint(0, 10, (batch,), device=dev)
+    if make_batch is None:
+        x = torch.randn(batch, 3, 32, 32, device=dev)
+        y = torch.randint(0, 10, (batch,), device=dev)
+    else:
+        x, y = make_batch()
+    loss_fn = loss_fn or (lambda logits, yy: F.cross_entropy(logits.float(), yy))
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()
     base = torch.cuda.memory_allocated(dev)
@@ -218,7 +287,8 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
             logits = model.arch.forward_compact(sub.views(master), x, sub)
         else:
             logits = model.arch.forward(sub.views(master), x, view)
-        loss = F.cross_entropy(logits.float(), y)
+        loss = loss_fn(logits, y)
+    del logits
     loss.backward()
     torch.cuda.synchronize(dev)
     peak = torch.cuda.max_memory_allocated(dev) - base

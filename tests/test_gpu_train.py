@@ -76,6 +76,28 @@ def test_resnet18_width_wise_step_matches_oracle(cuda):
     assert np.array_equal(model.theta.cpu().numpy().view(np.uint32), th1.astype(np.float32).view(np.uint32))
 
 
+def test_gpt2_block_dropping_skip_equals_multiply(cuda):
+    """C4: a dropped GPT-2 block is the identity (skip == multiply-by-zero)
+    and leaves exactly-zero gradients on its parameters."""
+    from paper_2507_09029_b200 import masking, train
+    model = train.build_gpt2(cuda)
+    model.theta = model.theta.double()
+    a = masking.build_assignment(model.topology, "block", 8, 4, seed=1)
+    view = a.worker_view(3)
+    tok = torch.randint(0, 50257, (2, 64), device=cuda)
+    losses, grads = [], []
+    for mode in ("skip", "multiply"):
+        leaf = model.theta.detach().clone().requires_grad_(True)
+        loss = train.lm_loss(model.arch.forward(train.param_views(model.topology, leaf), tok, view, mode), tok)
+        (g,) = torch.autograd.grad(loss, leaf)
+        losses.append(loss.item())
+        grads.append(g)
+    assert abs(losses[0] - losses[1]) <= 1e-12 * abs(losses[0])
+    mask = view.param_mask_bool
+    assert torch.all(grads[0][~mask] == 0) and torch.all(grads[1][~mask] == 0)
+    assert torch.max(torch.abs(grads[0] - grads[1])).item() < 1e-12
+
+
 def test_memory_subnet_below_full_replica(cuda):
     from paper_2507_09029_b200 import masking, train
     model = train.build_resnet18(cuda)
