@@ -269,10 +269,16 @@ typedef struct {
   int32_t pad_[3];
 } sdp_slice_task;
 
-/* compact[...] = full[...] over every task (one CTA per task). */
+/* compact[...] = full[...] over every task (one CTA per task).
+ * flags & SDP_GATHER_REVERSE: full[...] = compact[...] through the same
+ * forward maps (only mapped full elements are written) -- the inverse of a
+ * gather whose descriptors tile the full tensor, e.g. leaving the
+ * window-class-major sync layout.  dtype SDP_DTYPE_U8 moves owner masks. */
+#define SDP_GATHER_REVERSE 0x1
+#define SDP_DTYPE_U8 2
 int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
                       int n_tasks, const int32_t* fwd_maps, const void* full,
-                      void* compact, void* stream);
+                      void* compact, int flags, void* stream);
 
 #define SDP_SCATTER_ZERO_FILL 0x1  /* full[j] = 0 where no compact element maps */
 #define SDP_SCATTER_ACCUMULATE 0x2 /* full[j] += compact[...] instead of = */

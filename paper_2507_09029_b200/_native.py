@@ -35,6 +35,8 @@ SCATTER_ACCUMULATE = 0x2
 
 DTYPE_F32 = 0
 DTYPE_F64 = 1
+DTYPE_U8 = 2
+GATHER_REVERSE = 0x1
 
 TILE_UNIFORM = 0x80000000
 TILE_LEN_MASK = 0x00FFFFFF
@@ -113,7 +115,7 @@ SIGNATURES = {
     "sdp_owner_sync": (C.c_int, [C.POINTER(SyncArgs), VP]),
     "sdp_nesterov_update": (C.c_int, [I32, I64, VP, VP, VP, DBL, DBL, VP, VP, VP]),
     "sdp_masked_extract": (C.c_int, [I32, VP, VP, I32, I64, I32, VP, VP]),
-    "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, VP]),
+    "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
     "sdp_scatter_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
     "sdp_divide": (C.c_int, [I32, VP, VP, I64, VP, VP]),
     "sdp_restricted_dots": (C.c_int, [I32, VP, VP, VP, VP, I32, I32, VP, VP, VP]),

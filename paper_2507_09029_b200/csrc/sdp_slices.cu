@@ -30,10 +30,10 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
   return mul ? (__umulhi(n, mul) >> shr) : n;
 }
 
-template <typename T>
+template <typename T, bool REVERSE>
 __global__ void __launch_bounds__(kSliceThreads)
 k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks,
-         const int32_t* __restrict__ fwd, const T* __restrict__ full, T* __restrict__ compact) {
+         const int32_t* __restrict__ fwd, T* full, T* compact) {
   const sdp_slice_task tk = tasks[blockIdx.x];
   const sdp_slice_desc d = descs[tk.desc];
   const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
@@ -55,7 +55,9 @@ k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restr
       const uint32_t b = fast_div(t, d.inner_mul, d.inner_shr);
       src += static_cast<int64_t>(__ldg(fwd + d.col_map + b)) * d.inner + (t - b * d.inner);
     }
-    compact[d.compact_offset + static_cast<int64_t>(r) * row_len + t] = full[src];
+    const int64_t c = d.compact_offset + static_cast<int64_t>(r) * row_len + t;
+    if (REVERSE) full[src] = compact[c];
+    else compact[c] = full[src];
   }
 }
 
@@ -147,19 +149,27 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask, int
 
 int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
                       int n_tasks, const int32_t* fwd_maps, const void* full, void* compact,
-                      void* stream) {
+                      int flags, void* stream) {
   if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
   if (n_tasks == 0) return SDP_OK;
   if (!descs || !tasks || !full || !compact) return set_error(SDP_ERR_USAGE, "null device pointer");
   cudaStream_t s = as_stream(stream);
-  if (dtype == SDP_DTYPE_F32)
-    k_gather<float><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps, static_cast<const float*>(full),
-                                                      static_cast<float*>(compact));
-  else if (dtype == SDP_DTYPE_F64)
-    k_gather<double><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps, static_cast<const double*>(full),
-                                                       static_cast<double*>(compact));
-  else
-    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  const bool rev = (flags & SDP_GATHER_REVERSE) != 0;
+  void* fu = const_cast<void*>(full);
+#define SDP_GATHER(TT)                                                                          \
+  do {                                                                                          \
+    if (rev)                                                                                    \
+      k_gather<TT, true><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps,              \
+                                                           static_cast<TT*>(fu), static_cast<TT*>(compact)); \
+    else                                                                                        \
+      k_gather<TT, false><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps,             \
+                                                            static_cast<TT*>(fu), static_cast<TT*>(compact)); \
+  } while (0)
+  if (dtype == SDP_DTYPE_F32) SDP_GATHER(float);
+  else if (dtype == SDP_DTYPE_F64) SDP_GATHER(double);
+  else if (dtype == SDP_DTYPE_U8) SDP_GATHER(uint8_t);
+  else return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32, SDP_DTYPE_F64 or SDP_DTYPE_U8");
+#undef SDP_GATHER
   SDP_LAUNCH_CHECK();
   return SDP_OK;
 }

@@ -126,7 +126,7 @@ class SyncPlan:
     def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int | None = None,
                  resident: bool = False, max_grid: int | None = None,
                  force_grid: int | None = None, tile_lo: int | None = None,
-                 tile_hi: int | None = None):
+                 tile_hi: int | None = None, owner_mask: torch.Tensor | None = None):
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
@@ -135,9 +135,11 @@ class SyncPlan:
             tile = auto_tile(d, _sm_count(), owned_total / max(1, d))
         self.tile = tile
         self.world, self.rank = world, rank
+        # a permuted layout (layout.SyncLayout) brings its own per-element owner mask
+        self.owner_mask = assignment.owner_mask if owner_mask is None else owner_mask
         n_tiles = (d + tile - 1) // tile
         raw = torch.empty(max(1, n_tiles) * TILE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        N.call("sdp_plan_tiles", ptr(assignment.owner_mask), assignment.mask_bytes, d, tile,
+        N.call("sdp_plan_tiles", ptr(self.owner_mask), assignment.mask_bytes, d, tile,
                ptr(raw), stream_ptr(dev))
         tiles = raw.cpu().numpy().view(TILE_DTYPE)[:n_tiles].copy()
         self.all_tiles = tiles
@@ -165,7 +167,11 @@ class SyncPlan:
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
         # exact sum of |O_j| over this rank's elements (per-tile coverage sums)
         padded = torch.zeros(max(1, n_tiles) * tile, dtype=torch.int64, device=dev)
-        padded[:d] = assignment.coverage
+        if owner_mask is None:
+            padded[:d] = assignment.coverage
+        else:  # popcount of the permuted mask
+            m = self.owner_mask.to(torch.int64) & ((1 << assignment.n_workers) - 1)
+            padded[:d] = sum((m >> w) & 1 for w in range(assignment.n_workers))
         self.tile_owned = padded.view(-1, tile).sum(dim=1).cpu().numpy()
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
@@ -197,7 +203,7 @@ class SyncPlan:
         s.mask_bytes = a.mask_bytes
         s.tile = self.tile
         s.total = a.topology.total
-        s.owner_mask = a.owner_mask.data_ptr()
+        s.owner_mask = self.owner_mask.data_ptr()
         s.tiles = self.table.data_ptr()
         s.n_tiles = self.grid * self.tiles_per_cta
         s.tiles_per_cta = self.tiles_per_cta

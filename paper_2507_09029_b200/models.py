@@ -405,7 +405,7 @@ class SubnetLayout:
         if out is None:
             out = torch.empty(max(1, self.compact_total), dtype=theta.dtype, device=theta.device)
         N.call("sdp_gather_slices", sdp_dtype(theta.dtype), ptr(self.d_fwd), ptr(self.t_gather),
-               self.n_gather, ptr(self.fwd_maps), ptr(theta), ptr(out), stream_ptr(theta.device))
+               self.n_gather, ptr(self.fwd_maps), ptr(theta), ptr(out), 0, stream_ptr(theta.device))
         return out
 
     def scatter(self, compact: torch.Tensor, full: torch.Tensor | None = None,

@@ -184,7 +184,8 @@ class SubnetTrainer:
     written by the sync kernel's epilogue."""
 
     def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
-                 autocast: bool = True, compact: bool | None = None, loss_fn=None):
+                 autocast: bool = True, compact: bool | None = None, loss_fn=None,
+                 sync_layout: bool = False):
         self.model = model
         self.assignment = assignment
         self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
@@ -197,12 +198,24 @@ class SubnetTrainer:
             self.subs = [SubnetLayout(assignment, w) for w in range(assignment.n_workers)]
         d = model.topology.total
         dev = model.theta.device
+        # sync_layout: keep theta / velocity / gradient replicas permuted into the
+        # window-class-major layout (layout.py) so the sync sees uniform tiles
+        self.slayout = None
+        if sync_layout and self.compact:
+            from .layout import SyncLayout, WorkerTransfer
+            self.slayout = SyncLayout(assignment)
+            self.transfers = [WorkerTransfer(self.slayout, s) for s in self.subs]
+            model.theta = self.slayout.to_sync(model.theta)
         self.velocity = torch.zeros(d, device=dev)
         self.theta_bf16 = model.theta.to(torch.bfloat16)
         self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
         self.lr, self.momentum, self.autocast = lr, momentum, autocast
-        self.plan = assignment.sync_plan()
+        self.plan = self.slayout.plan() if self.slayout else assignment.sync_plan()
         self._prep = None
+
+    def theta(self) -> torch.Tensor:
+        """theta in the reference's flat layout."""
+        return self.slayout.from_sync(self.model.theta) if self.slayout else self.model.theta
 
     def _sync(self):
         if self._prep is None:
@@ -220,13 +233,19 @@ class SubnetTrainer:
         for w, (x, y) in enumerate(batches):
             if self.compact:
                 sub = self.subs[w]
-                leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
+                if self.slayout:  # the worker's blocks of the permuted theta
+                    leaf = self.transfers[w].to_compact(self.model.theta).requires_grad_(True)
+                else:
+                    leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
                     logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
                     loss = self.loss_fn(logits, y)
                 del logits
                 (g,) = torch.autograd.grad(loss, leaf)
-                sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
+                if self.slayout:
+                    self.transfers[w].from_compact(g, self.grads[w])
+                else:
+                    sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
                 losses.append(loss.detach())
                 continue
             # the worker trains on the bf16 weights the previous sync wrote
