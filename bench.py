@@ -446,7 +446,7 @@ def run_train(args, dev):
     for tag, p, strategy in (("subnet", args.p, "block"), ("widthwise", args.p, "neuron"), ("dp", n, "block")):
         model = train.build_resnet18(dev)
         a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=0.001)
+        tr = train.SubnetTrainer(model, a, lr=0.02, sync_layout=(strategy == "neuron"))
         out[f"{tag}_loss_first"] = float(tr.step(batches).item())
         for _ in range(2):
             tr.step(batches)

@@ -106,7 +106,7 @@ class PeerGroup:
 
     def __init__(self, assignment, rank: int, world: int, device, all_gather,
                  dtype=torch.float32, shadows: bool = True, max_grid: int | None = None,
-                 timeout_cycles: int = 20_000_000_000):
+                 timeout_cycles: int = 20_000_000_000, owner_mask: torch.Tensor | None = None):
         self.assignment = assignment
         self.layout = rank_layout(assignment.n_workers, world, rank)
         self.device = torch.device(device)
@@ -114,12 +114,15 @@ class PeerGroup:
         self.replicas = {w: torch.zeros(d, dtype=dtype, device=self.device) for w in self.layout.local_workers}
         self.shadows = ({w: torch.zeros(d, dtype=torch.bfloat16, device=self.device)
                          for w in self.layout.local_workers} if shadows else {})
-        self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True, max_grid=max_grid)
+        # owner_mask: the sync-space mask of a layout.SyncLayout when replicas are
+        # kept window-class-major (width-wise assignments)
+        self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True, max_grid=max_grid,
+                             owner_mask=owner_mask)
         # every rank must launch the same grid for the pairwise per-CTA barrier
         self.grid = max(all_gather(self.plan.grid))
         if self.plan.grid != self.grid:
             self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True,
-                                 force_grid=self.grid)
+                                 force_grid=self.grid, owner_mask=owner_mask)
         self.pad = torch.zeros(self.grid * PAD_WORDS_PER_CTA, dtype=torch.int32, device=self.device)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._imported: list[int] = []

@@ -269,6 +269,8 @@ def build_resnet18(dev, seed: int = 1) -> GlobalModel:
     m = GlobalModel(arch=arch, topology=topo, theta=theta)
     from .models import kaiming_fan_out_init
     m.theta = kaiming_fan_out_init(m, None, seed)
+    fc = topo.index["fc.w"]
+    m.theta[fc.offset:fc.offset + fc.size] = 0.0  # zero-init classifier: initial loss ln(10)
     return m
 
 

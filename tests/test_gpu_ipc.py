@@ -30,19 +30,24 @@ CHILD = textwrap.dedent(r"""
         return out
     topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32))
     a = masking.build_assignment(topo, os.environ["STRATEGY"], 4, 2, seed=1)
+    lay = None
+    if os.environ.get("LAYOUT") == "sync":
+        from paper_2507_09029_b200.layout import SyncLayout
+        lay = SyncLayout(a)
     g = comm.PeerGroup(a, rank, world, torch.device("cuda", 0), all_gather, max_grid=4,
-                       timeout_cycles=10_000_000_000)
+                       timeout_cycles=10_000_000_000, owner_mask=None if lay is None else lay.owner_mask)
     gen = torch.Generator(device="cuda")
     for w, t in g.replicas.items():
         gen.manual_seed(50 + w)
-        t.copy_(torch.randn(t.numel(), generator=gen, device="cuda") * a.param_masks[w])
+        x = torch.randn(t.numel(), generator=gen, device="cuda") * a.param_masks[w]
+        t.copy_(x if lay is None else lay.to_sync(x))
     torch.cuda.synchronize()
     dist.barrier()
     g.launch()
     torch.cuda.synchronize()
     dist.barrier()
     st = int(g.status.item())
-    out = {w: t.cpu().numpy() for w, t in g.replicas.items()}
+    out = {w: (t if lay is None else lay.from_sync(t)).cpu().numpy() for w, t in g.replicas.items()}
     np.savez(os.path.join(os.environ["OUT"], f"rank{rank}.npz"), status=st, **{f"w{w}": v for w, v in out.items()})
     g.close()
     dist.destroy_process_group()
@@ -57,8 +62,8 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("strategy", ["block", "neuron"])
-def test_two_process_ipc_owner_sync(cuda, tmp_path, strategy):
+@pytest.mark.parametrize("strategy,layout", [("block", "ref"), ("neuron", "ref"), ("neuron", "sync")])
+def test_two_process_ipc_owner_sync(cuda, tmp_path, strategy, layout):
     import torch
     from oracle import oracle as O
     from paper_2507_09029_b200 import masking, zoo
@@ -67,7 +72,8 @@ def test_two_process_ipc_owner_sync(cuda, tmp_path, strategy):
     procs = []
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy)
+                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy,
+                   LAYOUT=layout)
         procs.append(subprocess.Popen([sys.executable, "-c", CHILD], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []

@@ -60,7 +60,8 @@ def emit(kernel, config, us, us_min, nbytes, **extra):
                       **extra}), flush=True)
 
 
-def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None, reps=20):
+def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None, reps=20,
+              sync_layout=False):
     a = masking.build_assignment(topo, strategy, n, p, seed=1)
     d = topo.total
     pm = a.param_masks
@@ -72,7 +73,13 @@ def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None
     del pm
     sh = [torch.zeros(d, dtype=torch.bfloat16, device=DEV) for _ in range(n)] if shadows else None
     out = None if writeback else torch.empty(d, device=DEV)
-    plan = a.sync_plan(tile=tile)
+    if sync_layout:
+        from paper_2507_09029_b200.layout import SyncLayout
+        lay = SyncLayout(a)
+        reps_t = [lay.to_sync(r) for r in reps_t]
+        plan = lay.plan(tile=tile)
+    else:
+        plan = a.sync_plan(tile=tile)
     prep = engine.PreparedSync(reps_t, a, writeback=writeback, shadows_bf16=sh, out=out, plan=plan)
     us, us_min = timed(prep.launch, reps=reps)
     own = plan.owned_elems
@@ -164,7 +171,9 @@ def main():
     sync_case(r18, "C2 resnet18", "block", 8, 4)
     sync_case(r18, "C2 resnet18", "block", 8, 4, writeback=False, shadows=False)
     sync_case(r18, "C3 resnet18", "neuron", 8, 4)
+    sync_case(r18, "C3 resnet18 (sync layout)", "neuron", 8, 4, sync_layout=True)
     sync_case(gpt2, "C4 gpt2", "block", 8, 4)
+    sync_case(gpt2, "C4 gpt2 width-wise (sync layout)", "neuron", 8, 4, sync_layout=True)
     sizes = [1, 16, 256] if args.quick else [1, 4, 16, 64, 256, 1024]
     for mib in sizes:
         for p in (2, 4, 8):
