@@ -256,12 +256,17 @@ typedef struct {
   uint32_t inner_shr;
   uint32_t rowlen_mul;  /* fast division by the row length the kernel walks: */
   uint32_t rowlen_shr;  /* ccols*inner (gather table), cols*inner (scatter) */
-  int32_t pad_;
+  int32_t col_tab;      /* offset in the map buffer of the expanded column table
+                         * (one int32 per element of a walked row: the element's
+                         * offset in the other side's row, -1 = not held), or -1
+                         * for the identity; required when col_map >= 0 and the
+                         * walked row has >= 256 elements */
 } sdp_slice_desc;
 
 /* A unit of work of the gather/scatter kernels: rows [row_begin, row_end) of
  * descriptor `desc` (compact rows for gather, full rows for scatter), and
- * within each of those rows the elements [elem_begin, elem_end). */
+ * within each of those rows the elements [elem_begin, elem_end).  Rows of
+ * fewer than 256 elements must be whole (elem_begin = 0, elem_end = row length). */
 typedef struct {
   int32_t desc;
   int32_t row_begin, row_end;
@@ -269,7 +274,8 @@ typedef struct {
   int32_t pad_[3];
 } sdp_slice_task;
 
-/* compact[...] = full[...] over every task (one CTA per task).
+/* compact[...] = full[...] over every task (persistent CTAs walk the task list;
+ * a tensor holds fewer than 2^31 elements).
  * flags & SDP_GATHER_REVERSE: full[...] = compact[...] through the same
  * forward maps (only mapped full elements are written) -- the inverse of a
  * gather whose descriptors tile the full tensor, e.g. leaving the

@@ -68,7 +68,7 @@ class SliceDesc(C.Structure):
                 ("crows", C.c_int32), ("ccols", C.c_int32),
                 ("row_map", C.c_int32), ("col_map", C.c_int32),
                 ("inner_mul", C.c_uint32), ("inner_shr", C.c_uint32),
-                ("rowlen_mul", C.c_uint32), ("rowlen_shr", C.c_uint32), ("pad_", C.c_int32)]
+                ("rowlen_mul", C.c_uint32), ("rowlen_shr", C.c_uint32), ("col_tab", C.c_int32)]
 
 
 class SliceTask(C.Structure):

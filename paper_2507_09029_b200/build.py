@@ -57,12 +57,19 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = LIBDIR / "obj"
     objdir.mkdir(parents=True, exist_ok=True)
 
+    headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
+
     def compile_one(src: Path) -> tuple[Path, str]:
         obj = objdir / (src.stem + ".o")
+        log = objdir / (src.stem + ".ptxas")
+        if not force and obj.exists() and log.exists() and \
+                all(p.stat().st_mtime <= obj.stat().st_mtime for p in [src, *headers]):
+            return obj, log.read_text()  # object is current: incremental rebuild
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
+        log.write_text(r.stderr)
         return obj, r.stderr
 
     with concurrent.futures.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:

@@ -30,72 +30,281 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
   return mul ? (__umulhi(n, mul) >> shr) : n;
 }
 
+// Persistent CTAs (a few per SM) walk the task list interleaved (task
+// blockIdx.x + i * gridDim.x).  Per stage, kStage task records and their
+// descriptors are loaded in parallel into shared memory: the task -> descriptor
+// chain costs one round trip per kStage tasks instead of one per task.
+//
+// A task is either
+//  * tiled (the walked row length >= kSliceThreads): elements
+//    [elem_begin, elem_end) of every row in [row_begin, row_end).  A thread
+//    owns the row positions tid + k * kSliceThreads; it resolves their column
+//    offsets ONCE (the descriptor's expanded column table, col_tab) and reuses
+//    them for every row, so a row costs one uniform row-map load plus one load
+//    and one store per element -- no per-element division or map chain; or
+//  * flat (short rows): whole rows [row_begin, row_end) flattened over the
+//    CTA with a multiply-high division per element (small tensors only).
+// Data loads of a batch are all issued before its first store.  The
+// contiguous side (compact rows for gather, full rows for scatter) is
+// accessed at consecutive thread positions (coalesced).  Offsets inside one
+// tensor fit in 32 bits (rows * cols * inner < 2^31, checked on the host).
+constexpr int kSliceBatch = 8;
+template <typename T> constexpr int rows_per_iter() { return sizeof(T) == 8 ? 1 : 2; }
+constexpr int kStage = 32;
+constexpr int kSliceCtasPerSm = 3;  // <= 80 registers: 16 elements in flight per thread without spills
+
+struct SliceStage {
+  sdp_slice_task task[kStage];
+  sdp_slice_desc desc[kStage];
+};
+
+__device__ __forceinline__ int stage_tasks(SliceStage& st, const sdp_slice_desc* __restrict__ descs,
+                                           const sdp_slice_task* __restrict__ tasks, int n_tasks,
+                                           int first) {
+  const int stride = gridDim.x;
+  const int n = min(kStage, (n_tasks - first + stride - 1) / stride);
+  __syncthreads();  // the previous stage is consumed
+  if (threadIdx.x < n) {
+    const sdp_slice_task tk = tasks[first + threadIdx.x * stride];
+    st.task[threadIdx.x] = tk;
+    st.desc[threadIdx.x] = descs[tk.desc];
+  }
+  __syncthreads();
+  return n;
+}
+
 template <typename T, bool REVERSE>
-__global__ void __launch_bounds__(kSliceThreads)
-k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks,
-         const int32_t* __restrict__ fwd, T* full, T* compact) {
-  const sdp_slice_task tk = tasks[blockIdx.x];
-  const sdp_slice_desc d = descs[tk.desc];
-  const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
-  // (row, element) pairs of the task flattened over the CTA: independent
-  // loads across rows instead of one dependent round trip per row.
-  const uint32_t seg = static_cast<uint32_t>(tk.elem_end - tk.elem_begin);
-  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * seg;
-  const int64_t row_stride = static_cast<int64_t>(d.cols) * d.inner;
-#pragma unroll 4
-  for (uint32_t idx = threadIdx.x; idx < n_el; idx += kSliceThreads) {
-    const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);  // 0 for single-row tasks
-    const uint32_t r = tk.row_begin + rr;
-    const uint32_t t = tk.elem_begin + (idx - rr * row_len);
-    const int64_t fr = d.row_map >= 0 ? __ldg(fwd + d.row_map + r) : r;
-    int64_t src = d.full_offset + fr * row_stride;
-    if (d.col_map < 0) {
-      src += t;
-    } else {
-      const uint32_t b = fast_div(t, d.inner_mul, d.inner_shr);
-      src += static_cast<int64_t>(__ldg(fwd + d.col_map + b)) * d.inner + (t - b * d.inner);
+__device__ __forceinline__ void gather_tiled(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                             const int32_t* __restrict__ fwd, T* __restrict__ full,
+                                             T* __restrict__ compact, uint32_t row_len) {
+  constexpr int kRowsPerIter = rows_per_iter<T>();
+  const uint32_t row_stride = static_cast<uint32_t>(d.cols) * d.inner;
+  T* const fbase = full + d.full_offset;
+  T* const cbase = compact + d.compact_offset;
+  for (uint32_t eb = tk.elem_begin + threadIdx.x; eb < static_cast<uint32_t>(tk.elem_end);
+       eb += kSliceThreads * kSliceBatch) {
+    int32_t co[kSliceBatch];  // offset of my element inside the full row, -1 = past the task
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      const uint32_t t = eb + k * kSliceThreads;
+      co[k] = t < static_cast<uint32_t>(tk.elem_end)
+                  ? (d.col_tab >= 0 ? __ldg(fwd + d.col_tab + t) : static_cast<int32_t>(t)) : -1;
     }
-    const int64_t c = d.compact_offset + static_cast<int64_t>(r) * row_len + t;
-    if (REVERSE) full[src] = compact[c];
-    else compact[c] = full[src];
+    for (int r0 = tk.row_begin; r0 < tk.row_end; r0 += kRowsPerIter) {
+      T* fr[kRowsPerIter];
+      T* cr[kRowsPerIter];
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j) {
+        const int r = min(r0 + j, tk.row_end - 1);  // a duplicated last row rewrites identical values
+        const uint32_t f = d.row_map >= 0 ? __ldg(fwd + d.row_map + r) : static_cast<uint32_t>(r);
+        fr[j] = fbase + f * row_stride;
+        cr[j] = cbase + static_cast<uint32_t>(r) * row_len + eb;
+      }
+      T v[kRowsPerIter][kSliceBatch];
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j)
+#pragma unroll
+        for (int k = 0; k < kSliceBatch; ++k)
+          if (co[k] >= 0) v[j][k] = REVERSE ? cr[j][k * kSliceThreads] : __ldg(fr[j] + co[k]);
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j)
+#pragma unroll
+        for (int k = 0; k < kSliceBatch; ++k) {
+          if (co[k] < 0) continue;
+          if (REVERSE) fr[j][co[k]] = v[j][k];
+          else cr[j][k * kSliceThreads] = v[j][k];
+        }
+    }
+  }
+}
+
+template <typename T, bool REVERSE>
+__device__ __forceinline__ void gather_flat(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                            const int32_t* __restrict__ fwd, T* __restrict__ full,
+                                            T* __restrict__ compact, uint32_t row_len) {
+  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * row_len;
+  const uint32_t row_stride = static_cast<uint32_t>(d.cols) * d.inner;
+  T* const fbase = full + d.full_offset;
+  T* const cbase = compact + d.compact_offset + static_cast<int64_t>(tk.row_begin) * row_len;
+  for (uint32_t base = threadIdx.x; base < n_el; base += kSliceThreads * kSliceBatch) {
+    int32_t src[kSliceBatch];  // element of the full tensor, -1 past the task
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      const uint32_t idx = base + k * kSliceThreads;
+      src[k] = -1;
+      if (idx < n_el) {
+        const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);
+        const uint32_t r = tk.row_begin + rr;
+        const uint32_t t = idx - rr * row_len;
+        const uint32_t fr = d.row_map >= 0 ? __ldg(fwd + d.row_map + r) : r;
+        uint32_t e = fr * row_stride;
+        if (d.col_map < 0) {
+          e += t;
+        } else {
+          const uint32_t b = fast_div(t, d.inner_mul, d.inner_shr);
+          e += static_cast<uint32_t>(__ldg(fwd + d.col_map + b)) * d.inner + (t - b * d.inner);
+        }
+        src[k] = static_cast<int32_t>(e);
+      }
+    }
+    T v[kSliceBatch];
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k)
+      if (src[k] >= 0) v[k] = REVERSE ? cbase[base + k * kSliceThreads] : __ldg(fbase + src[k]);
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      if (src[k] < 0) continue;
+      if (REVERSE) fbase[src[k]] = v[k];
+      else cbase[base + k * kSliceThreads] = v[k];
+    }
+  }
+}
+
+template <typename T, bool REVERSE>
+__global__ void __launch_bounds__(kSliceThreads, kSliceCtasPerSm)
+k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks, int n_tasks,
+         const int32_t* __restrict__ fwd, T* __restrict__ full, T* __restrict__ compact) {
+  __shared__ SliceStage st;
+  for (int first = blockIdx.x; first < n_tasks; first += kStage * gridDim.x) {
+    const int n = stage_tasks(st, descs, tasks, n_tasks, first);
+    for (int i = 0; i < n; ++i) {
+      const sdp_slice_task& tk = st.task[i];
+      const sdp_slice_desc& d = st.desc[i];
+      const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
+      if (row_len >= kSliceThreads) gather_tiled<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+      else gather_flat<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+    }
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSliceThreads)
-k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks,
-          const int32_t* __restrict__ inv, const T* __restrict__ compact, T* __restrict__ full,
-          int flags) {
-  const bool zero_fill = (flags & SDP_SCATTER_ZERO_FILL) && !(flags & SDP_SCATTER_ACCUMULATE);
-  const bool accumulate = (flags & SDP_SCATTER_ACCUMULATE) != 0;
-  const sdp_slice_task tk = tasks[blockIdx.x];
-  const sdp_slice_desc d = descs[tk.desc];
-  const int64_t crow_len = static_cast<int64_t>(d.ccols) * d.inner;
-  const uint32_t row_len = static_cast<uint32_t>(d.cols) * d.inner;
-  const uint32_t seg = static_cast<uint32_t>(tk.elem_end - tk.elem_begin);
-  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * seg;
-#pragma unroll 4
-  for (uint32_t idx = threadIdx.x; idx < n_el; idx += kSliceThreads) {
-    const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);  // 0 for single-row tasks
-    const uint32_t f = tk.row_begin + rr;
-    const uint32_t t = tk.elem_begin + (idx - rr * row_len);
-    T* dst = full + d.full_offset + static_cast<int64_t>(f) * row_len + t;
-    const int32_t a = d.crows == 0 ? -1 : (d.row_map >= 0 ? __ldg(inv + d.row_map + f) : static_cast<int32_t>(f));
-    int64_t src = -1;
-    if (a >= 0) {
-      if (d.col_map < 0) {
-        src = a * crow_len + t;
-      } else {
-        const uint32_t fb = fast_div(t, d.inner_mul, d.inner_shr);
-        const int32_t cb = __ldg(inv + d.col_map + fb);
-        if (cb >= 0) src = a * crow_len + static_cast<int64_t>(cb) * d.inner + (t - fb * d.inner);
+__device__ __forceinline__ void scatter_tiled(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                              const int32_t* __restrict__ inv, const T* __restrict__ compact,
+                                              T* __restrict__ full, uint32_t row_len, bool zero_fill,
+                                              bool accumulate) {
+  constexpr int kRowsPerIter = rows_per_iter<T>();
+  const uint32_t crow_len = static_cast<uint32_t>(d.ccols) * d.inner;
+  const T* const cbase = compact + d.compact_offset;
+  T* const fbase = full + d.full_offset;
+  for (uint32_t eb = tk.elem_begin + threadIdx.x; eb < static_cast<uint32_t>(tk.elem_end);
+       eb += kSliceThreads * kSliceBatch) {
+    int32_t co[kSliceBatch];  // compact column offset, -1 = not held, -2 = past the task
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      const uint32_t t = eb + k * kSliceThreads;
+      co[k] = t < static_cast<uint32_t>(tk.elem_end)
+                  ? (d.col_tab >= 0 ? __ldg(inv + d.col_tab + t) : static_cast<int32_t>(t)) : -2;
+    }
+    for (int r0 = tk.row_begin; r0 < tk.row_end; r0 += kRowsPerIter) {
+      T* fr[kRowsPerIter];
+      int32_t a[kRowsPerIter];  // compact row, -1 = row not held
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j) {
+        const int f = min(r0 + j, tk.row_end - 1);  // a duplicated last row rewrites identical values
+        a[j] = d.crows == 0 ? -1 : (d.row_map >= 0 ? __ldg(inv + d.row_map + f) : f);
+        fr[j] = fbase + static_cast<uint32_t>(f) * row_len + eb;
+      }
+      T v[kRowsPerIter][kSliceBatch];
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j) {
+        const T* crow = cbase + static_cast<uint32_t>(max(a[j], 0)) * crow_len;
+#pragma unroll
+        for (int k = 0; k < kSliceBatch; ++k) {
+          v[j][k] = T(0);
+          if (a[j] >= 0 && co[k] >= 0) v[j][k] = __ldg(crow + co[k]);
+        }
+      }
+      if (accumulate) {
+        // not idempotent: never apply a duplicated last row twice
+#pragma unroll
+        for (int j = 0; j < kRowsPerIter; ++j)
+#pragma unroll
+          for (int k = 0; k < kSliceBatch; ++k)
+            if (r0 + j < tk.row_end && a[j] >= 0 && co[k] >= 0)
+              v[j][k] = static_cast<T>(fr[j][k * kSliceThreads] + v[j][k]);
+      }
+#pragma unroll
+      for (int j = 0; j < kRowsPerIter; ++j) {
+        if (accumulate && r0 + j >= tk.row_end) continue;
+#pragma unroll
+        for (int k = 0; k < kSliceBatch; ++k) {
+          const bool held = a[j] >= 0 && co[k] >= 0;
+          if (held || (zero_fill && co[k] != -2)) fr[j][k * kSliceThreads] = v[j][k];
+        }
       }
     }
-    if (src >= 0) {
-      const T v = compact[d.compact_offset + src];
-      *dst = accumulate ? static_cast<T>(*dst + v) : v;
-    } else if (zero_fill) {
-      *dst = T(0);  // the worker does not hold this element
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void scatter_flat(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                             const int32_t* __restrict__ inv, const T* __restrict__ compact,
+                                             T* __restrict__ full, uint32_t row_len, bool zero_fill,
+                                             bool accumulate) {
+  const uint32_t crow_len = static_cast<uint32_t>(d.ccols) * d.inner;
+  const uint32_t n_el = static_cast<uint32_t>(tk.row_end - tk.row_begin) * row_len;
+  const T* const cbase = compact + d.compact_offset;
+  T* const f0 = full + d.full_offset + static_cast<int64_t>(tk.row_begin) * row_len;
+  for (uint32_t base = threadIdx.x; base < n_el; base += kSliceThreads * kSliceBatch) {
+    int32_t src[kSliceBatch];  // compact element, -1 = not held, -2 = past the task
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      const uint32_t idx = base + k * kSliceThreads;
+      src[k] = -2;
+      if (idx < n_el) {
+        const uint32_t rr = fast_div(idx, d.rowlen_mul, d.rowlen_shr);
+        const uint32_t f = tk.row_begin + rr;
+        const uint32_t t = idx - rr * row_len;
+        const int32_t a = d.crows == 0 ? -1
+                          : (d.row_map >= 0 ? __ldg(inv + d.row_map + f) : static_cast<int32_t>(f));
+        int32_t s = -1;
+        if (a >= 0) {
+          if (d.col_map < 0) {
+            s = static_cast<int32_t>(a * crow_len + t);
+          } else {
+            const uint32_t fb = fast_div(t, d.inner_mul, d.inner_shr);
+            const int32_t cb = __ldg(inv + d.col_map + fb);
+            if (cb >= 0) s = static_cast<int32_t>(a * crow_len + cb * d.inner + (t - fb * d.inner));
+          }
+        }
+        src[k] = s;
+      }
+    }
+    T v[kSliceBatch];
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      v[k] = T(0);
+      if (src[k] >= 0) v[k] = __ldg(cbase + src[k]);
+    }
+    if (accumulate) {
+#pragma unroll
+      for (int k = 0; k < kSliceBatch; ++k)
+        if (src[k] >= 0) v[k] = static_cast<T>(f0[base + k * kSliceThreads] + v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kSliceBatch; ++k) {
+      // zero fill: the worker does not hold this element (v stays 0)
+      if (src[k] >= 0 || (src[k] == -1 && zero_fill)) f0[base + k * kSliceThreads] = v[k];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSliceThreads, kSliceCtasPerSm)
+k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks, int n_tasks,
+          const int32_t* __restrict__ inv, const T* __restrict__ compact, T* __restrict__ full,
+          int flags) {
+  __shared__ SliceStage st;
+  const bool zero_fill = (flags & SDP_SCATTER_ZERO_FILL) && !(flags & SDP_SCATTER_ACCUMULATE);
+  const bool accumulate = (flags & SDP_SCATTER_ACCUMULATE) != 0;
+  for (int first = blockIdx.x; first < n_tasks; first += kStage * gridDim.x) {
+    const int n = stage_tasks(st, descs, tasks, n_tasks, first);
+    for (int i = 0; i < n; ++i) {
+      const sdp_slice_task& tk = st.task[i];
+      const sdp_slice_desc& d = st.desc[i];
+      const uint32_t row_len = static_cast<uint32_t>(d.cols) * d.inner;
+      if (row_len >= kSliceThreads) scatter_tiled<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
+      else scatter_flat<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
     }
   }
 }
@@ -106,6 +315,10 @@ __global__ void k_divide(const T* __restrict__ acc, const double* __restrict__ d
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[j] = acc[j] / static_cast<T>(divisor[j]);
+}
+
+static int slice_grid(int n_tasks) {
+  return std::max(1, std::min(n_tasks, sm_count() * kSliceCtasPerSm));
 }
 
 static int grid_for(int64_t n) {
@@ -155,14 +368,15 @@ int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_ta
   if (!descs || !tasks || !full || !compact) return set_error(SDP_ERR_USAGE, "null device pointer");
   cudaStream_t s = as_stream(stream);
   const bool rev = (flags & SDP_GATHER_REVERSE) != 0;
+  const int grid = slice_grid(n_tasks);
   void* fu = const_cast<void*>(full);
 #define SDP_GATHER(TT)                                                                          \
   do {                                                                                          \
     if (rev)                                                                                    \
-      k_gather<TT, true><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps,              \
+      k_gather<TT, true><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps,        \
                                                            static_cast<TT*>(fu), static_cast<TT*>(compact)); \
     else                                                                                        \
-      k_gather<TT, false><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, fwd_maps,             \
+      k_gather<TT, false><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps,       \
                                                             static_cast<TT*>(fu), static_cast<TT*>(compact)); \
   } while (0)
   if (dtype == SDP_DTYPE_F32) SDP_GATHER(float);
@@ -181,11 +395,12 @@ int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_t
   if (n_tasks == 0) return SDP_OK;
   if (!descs || !tasks || !full) return set_error(SDP_ERR_USAGE, "null device pointer");
   cudaStream_t s = as_stream(stream);
+  const int grid = slice_grid(n_tasks);
   if (dtype == SDP_DTYPE_F32)
-    k_scatter<float><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, inv_maps, static_cast<const float*>(compact),
+    k_scatter<float><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, static_cast<const float*>(compact),
                                                        static_cast<float*>(full), flags);
   else if (dtype == SDP_DTYPE_F64)
-    k_scatter<double><<<n_tasks, kSliceThreads, 0, s>>>(descs, tasks, inv_maps, static_cast<const double*>(compact),
+    k_scatter<double><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, static_cast<const double*>(compact),
                                                         static_cast<double*>(full), flags);
   else
     return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");

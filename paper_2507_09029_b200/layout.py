@@ -61,19 +61,23 @@ class _DescBuilder:
         return off
 
     def add(self, full_off, comp_off, rows, cols, inner, rmap, cmap):
+        if rows * cols * inner >= 1 << 31:
+            raise ConfigError("a tensor of 2^31 or more elements exceeds the slice kernels' "
+                              "32-bit in-tensor offsets")
         crows = len(rmap) if rmap is not None else rows
         ccols = len(cmap) if cmap is not None else cols
         mul, shr = fast_divisor(inner)
         rl_mul, rl_shr = fast_divisor(max(1, ccols * inner))
         self.rows.append((full_off, comp_off, rows, cols, inner, crows, ccols, self.map_offset(rmap),
-                          self.map_offset(cmap), mul, shr, rl_mul, rl_shr, 0))
+                          self.map_offset(cmap), mul, shr, rl_mul, rl_shr, -1))
         return crows * ccols * inner
 
     def upload(self, dev):
-        from .models import slice_tasks
+        from .models import add_col_tables, slice_tasks
         descs = np.array(self.rows, dtype=self.dtype)
         tasks = slice_tasks(descs, compact=True)
         maps = np.concatenate(self.maps) if self.maps else np.zeros(1, np.int32)
+        maps = add_col_tables(descs, maps, inverse=False)
         return (upload_struct(descs, dev), upload_struct(tasks, dev), len(tasks),
                 torch.from_numpy(maps.astype(np.int32)).to(dev))
 

@@ -243,31 +243,66 @@ SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("row
                         ("cols", "<i4"), ("inner", "<i4"), ("crows", "<i4"), ("ccols", "<i4"),
                         ("row_map", "<i4"), ("col_map", "<i4"), ("inner_mul", "<u4"),
                         ("inner_shr", "<u4"), ("rowlen_mul", "<u4"), ("rowlen_shr", "<u4"),
-                        ("pad_", "<i4")])
+                        ("col_tab", "<i4")])
 TASK_DTYPE = np.dtype([("desc", "<i4"), ("row_begin", "<i4"), ("row_end", "<i4"),
                        ("elem_begin", "<i4"), ("elem_end", "<i4"), ("pad_", "<i4", 3)])
-TASK_ELEMS = 4096  # elements per gather/scatter CTA (16 per thread, rows flattened)
+TASK_ELEMS = 4096   # elements per gather/scatter task
+TILE_ELEMS = 2048   # max row elements a tiled task walks (256 threads x 8)
+TILED_MIN = 256     # walked rows at least this long are tiled (sdp_slices.cu)
 
 
 def slice_tasks(descs: np.ndarray, compact: bool, per_task: int = TASK_ELEMS) -> np.ndarray:
-    """Split every tensor into CTA work units of ~per_task elements: runs of
-    whole rows, or pieces of one row when a row is longer (compact rows for
-    gather, full rows for scatter)."""
+    """Split every tensor into work units of ~per_task elements (compact rows
+    for gather, full rows for scatter): rows of >= TILED_MIN elements are cut
+    into balanced, warp-aligned column chunks of <= TILE_ELEMS, and a task
+    takes that chunk of several rows (the kernel resolves the chunk's column
+    offsets once per task); shorter rows are grouped whole."""
     out = []
     for i, d in enumerate(descs):
         rows = int(d["crows"] if compact else d["rows"])
         row_len = int((d["ccols"] if compact else d["cols"]) * d["inner"])
         if rows == 0 or row_len == 0:
             continue
-        if row_len >= per_task:
-            for r in range(rows):
-                for e in range(0, row_len, per_task):
-                    out.append((i, r, r + 1, e, min(row_len, e + per_task), (0, 0, 0)))
+        if row_len >= TILED_MIN:
+            n_chunks = -(-row_len // TILE_ELEMS)
+            chunk = min(TILE_ELEMS, -(-(-(-row_len // n_chunks)) // 32) * 32)
+            k = max(1, per_task // chunk)
+            for e in range(0, row_len, chunk):
+                for r in range(0, rows, k):
+                    out.append((i, r, min(rows, r + k), e, min(row_len, e + chunk), (0, 0, 0)))
         else:
             k = max(1, per_task // row_len)
             for r in range(0, rows, k):
                 out.append((i, r, min(rows, r + k), 0, row_len, (0, 0, 0)))
     return np.array(out, dtype=TASK_DTYPE)
+
+
+def add_col_tables(descs: np.ndarray, maps: np.ndarray, inverse: bool) -> np.ndarray:
+    """Append each column-mapped descriptor's expanded column table to `maps`
+    and point `col_tab` at it (sdp.h): one int32 per element of the walked row
+    -- gather: the element's offset in the full row, fwd[col_map + t // inner]
+    * inner + t % inner over ccols * inner; inverse (scatter): its offset in
+    the compact row or -1, over cols * inner.  Identical tables are shared."""
+    parts, pos, seen = [maps.astype(np.int32)], len(maps), {}
+    tabs = np.full(len(descs), -1, dtype=np.int32)
+    for i, d in enumerate(descs):
+        cm = int(d["col_map"])
+        if cm < 0:
+            continue
+        inner = int(d["inner"])
+        n_cols = int(d["cols"] if inverse else d["ccols"])
+        key = (cm, inner, n_cols)
+        if key not in seen:
+            cmap = maps[cm:cm + n_cols].astype(np.int64)
+            tab = (cmap[:, None] * inner + np.arange(inner)[None, :])
+            if inverse:
+                tab[cmap < 0] = -1
+            seen[key] = pos
+            parts.append(tab.reshape(-1).astype(np.int32))
+            pos += tab.size
+        tabs[i] = seen[key]
+    descs["col_tab"] = tabs
+    return np.concatenate(parts)
 
 
 class SubnetLayout:
@@ -333,6 +368,9 @@ class SubnetLayout:
                 if clid is None:
                     inner *= cols
                     cols = 1
+            if rows * cols * inner >= 1 << 31:
+                raise ConfigError(f"{p.name}: 2^31 or more elements exceed the slice kernels' "
+                                  "32-bit in-tensor offsets")
             crows = len(live_ch[rlid]) if rlid else rows
             ccols = len(live_ch[clid]) if clid else cols
             if not present[p.name]:
@@ -359,6 +397,10 @@ class SubnetLayout:
         descs_inv["rowlen_mul"] = [m for m, _ in full_rl]
         descs_inv["rowlen_shr"] = [s for _, s in full_rl]
         from ._device import upload_struct
+        fw = np.concatenate(fwd) if fwd else np.zeros(1, np.int32)
+        iv = np.concatenate(inv) if inv else np.zeros(1, np.int32)
+        fw = add_col_tables(descs, fw, inverse=False)
+        iv = add_col_tables(descs_inv, iv, inverse=True)
         self.descs = descs
         self.d_fwd = upload_struct(descs, dev)
         self.d_inv = upload_struct(descs_inv, dev)
@@ -366,8 +408,6 @@ class SubnetLayout:
         s_tasks = slice_tasks(descs, compact=False)
         self.t_gather, self.n_gather = upload_struct(g_tasks, dev), len(g_tasks)
         self.t_scatter, self.n_scatter = upload_struct(s_tasks, dev), len(s_tasks)
-        fw = np.concatenate(fwd) if fwd else np.zeros(1, np.int32)
-        iv = np.concatenate(inv) if inv else np.zeros(1, np.int32)
         self.fwd_maps = torch.from_numpy(fw.astype(np.int32)).to(dev)
         self.inv_maps = torch.from_numpy(iv.astype(np.int32)).to(dev)
 

@@ -133,6 +133,22 @@ def slices_case(topo, tag, strategy, n, p):
     us, us_min = timed(lambda: N.call("sdp_masked_extract", 0, ptr(theta), ptr(view.param_mask_bool), 1,
                                       topo.total, 0, ptr(out), stream_ptr(DEV)))
     emit("k_masked_extract", tag, us, us_min, topo.total * 9, d=topo.total)
+    if strategy == "neuron":
+        # what width-wise training runs: flat <-> sync layout, compact <-> sync blocks
+        from paper_2507_09029_b200.layout import SyncLayout, WorkerTransfer
+        lay = SyncLayout(a)
+        ts = torch.empty_like(theta)
+        us, us_min = timed(lambda: lay.to_sync(theta, ts))
+        emit("k_gather(to_sync)", tag, us, us_min, topo.total * 8, d=topo.total)
+        us, us_min = timed(lambda: lay.from_sync(ts, theta))
+        emit("k_gather(from_sync, reverse)", tag, us, us_min, topo.total * 8, d=topo.total)
+        tr = WorkerTransfer(lay, sub)
+        us, us_min = timed(lambda: tr.to_compact(ts, comp))
+        emit("k_gather(to_compact, reverse)", tag, us, us_min, sub.compact_total * 8,
+             compact=sub.compact_total, d=topo.total)
+        us, us_min = timed(lambda: tr.from_compact(comp, ts))
+        emit("k_gather(from_compact)", tag, us, us_min, sub.compact_total * 8,
+             compact=sub.compact_total, d=topo.total)
 
 
 def cpu_case(topo, tag, n, p, budget=3.0):
@@ -157,32 +173,37 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only", default="build,sync,sweep,slices,cpu",
+                    help="comma-separated sections to run")
     args = ap.parse_args()
+    only = set(args.only.split(","))
     N.load()
     FLUSH_W = torch.empty(64 << 20, device=DEV)
     FLUSH_R = torch.zeros(64 << 20, device=DEV)
     r18, gpt2 = zoo.resnet18_cifar_topology(), zoo.gpt2_small_topology()
-    # mask builder
-    build_case(r18, "C2 resnet18", "block", 8, 4)
-    build_case(r18, "C2 resnet18 +[N,d]", "block", 8, 4, with_pm=True)
-    build_case(r18, "C3 resnet18", "neuron", 8, 4)
-    build_case(gpt2, "C4 gpt2", "block", 8, 4)
-    # sync
-    sync_case(r18, "C2 resnet18", "block", 8, 4)
-    sync_case(r18, "C2 resnet18", "block", 8, 4, writeback=False, shadows=False)
-    sync_case(r18, "C3 resnet18", "neuron", 8, 4)
-    sync_case(r18, "C3 resnet18 (sync layout)", "neuron", 8, 4, sync_layout=True)
-    sync_case(gpt2, "C4 gpt2", "block", 8, 4)
-    sync_case(gpt2, "C4 gpt2 width-wise (sync layout)", "neuron", 8, 4, sync_layout=True)
-    sizes = [1, 16, 256] if args.quick else [1, 4, 16, 64, 256, 1024]
-    for mib in sizes:
-        for p in (2, 4, 8):
-            sync_case(zoo.sweep_topology(mib * (1 << 20) // 4), f"C5 sweep {mib} MiB", "block", 8, p)
-            torch.cuda.empty_cache()
-    # width-wise extraction / write-back
-    slices_case(r18, "C3 resnet18", "neuron", 8, 4)
-    slices_case(gpt2, "C4 gpt2 (mlp units)", "neuron", 8, 4)
-    if not args.no_cpu:
+    if "build" in only:  # mask builder
+        build_case(r18, "C2 resnet18", "block", 8, 4)
+        build_case(r18, "C2 resnet18 +[N,d]", "block", 8, 4, with_pm=True)
+        build_case(r18, "C3 resnet18", "neuron", 8, 4)
+        build_case(gpt2, "C4 gpt2", "block", 8, 4)
+        build_case(gpt2, "C4 gpt2 neuron", "neuron", 8, 4)
+    if "sync" in only:
+        sync_case(r18, "C2 resnet18", "block", 8, 4)
+        sync_case(r18, "C2 resnet18", "block", 8, 4, writeback=False, shadows=False)
+        sync_case(r18, "C3 resnet18", "neuron", 8, 4)
+        sync_case(r18, "C3 resnet18 (sync layout)", "neuron", 8, 4, sync_layout=True)
+        sync_case(gpt2, "C4 gpt2", "block", 8, 4)
+        sync_case(gpt2, "C4 gpt2 width-wise (sync layout)", "neuron", 8, 4, sync_layout=True)
+    if "sweep" in only:
+        sizes = [1, 16, 256] if args.quick else [1, 4, 16, 64, 256, 1024]
+        for mib in sizes:
+            for p in (2, 4, 8):
+                sync_case(zoo.sweep_topology(mib * (1 << 20) // 4), f"C5 sweep {mib} MiB", "block", 8, p)
+                torch.cuda.empty_cache()
+    if "slices" in only:  # width-wise extraction / write-back
+        slices_case(r18, "C3 resnet18", "neuron", 8, 4)
+        slices_case(gpt2, "C4 gpt2 (mlp units)", "neuron", 8, 4)
+    if "cpu" in only and not args.no_cpu:
         for mib in (1, 16, 64):
             cpu_case(zoo.sweep_topology(mib * (1 << 20) // 4), f"C5 sweep {mib} MiB P=4", 8, 4)
 
