@@ -407,8 +407,9 @@ def run_e2e(args, a, dev, total_bytes):
         t.copy_(torch.randn(d, generator=gen, device=dev) * pm[w])
         host.append(t.numpy())
     del pm
-    for _ in range(3):
-        engine.aggregate(host, a)
+    out = None
+    for _ in range(3):  # warm-up exactly like the timed loop (the previous result is held)
+        out = engine.aggregate(host, a)
     torch.cuda.synchronize()
     ts = []
     for _ in range(args.e2e_steps):
@@ -416,6 +417,7 @@ def run_e2e(args, a, dev, total_bytes):
         out = engine.aggregate(host, a)
         ts.append(time.perf_counter() - t0)
     assert out.gbar.shape == (d,)
+    print("e2e per-call ms:", " ".join(f"{t * 1e3:.2f}" for t in ts), file=sys.stderr)
     dt = float(np.mean(ts))
     plan = a.sync_plan()
     h2d = sum(ln for w in range(n) for _, ln in plan.worker_ranges(w)) * 4 \

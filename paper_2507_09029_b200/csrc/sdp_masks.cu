@@ -175,8 +175,8 @@ __global__ void k_permutation(SeedWords seed, const int32_t* skip_sizes_dev, int
 // element expansion
 // ---------------------------------------------------------------------------
 constexpr int kBuildThreads = 256;
-constexpr int kLaneElems = 16;                  // elements per lane per warp chunk
-constexpr int kWarpChunk = 32 * kLaneElems;     // 512 consecutive elements per warp
+constexpr int kPairIters = 16;                  // pair iterations per warp chunk
+constexpr int kWarpChunk = 64 * kPairIters;     // 1024 consecutive elements per warp
 
 __device__ __forceinline__ int find_param(const sdp_param_desc* __restrict__ p, int n, int64_t j) {
   int lo = 0, hi = n - 1;  // last param with offset <= j
@@ -191,9 +191,69 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t mul, uint32_t shr)
   return mul ? (__umulhi(n, mul) >> shr) : n;
 }
 
-// A warp owns 512 consecutive elements; lane l takes elements l, l+32, ... so
-// every store instruction writes 32 consecutive elements (fully coalesced for
-// the 8-B coverage / divisor / governor arrays and the 1-B masks alike).
+// The parameter an element falls in, with its owner set precomputed when no
+// rule varies along the parameter (block rules, dim == 1: the whole block
+// strategy and every ungoverned tensor) -- then an element costs no rule walk.
+struct ParamCursor {
+  int pi;
+  int64_t lo, hi;       // [offset, offset + size)
+  int32_t rule_begin, rule_count;
+  bool uniform;
+  uint64_t bits;
+
+  __device__ void load(const sdp_param_desc* __restrict__ params, const sdp_rule_desc* __restrict__ rules,
+                       const uint64_t* __restrict__ unit_bits, uint64_t full, int i) {
+    const sdp_param_desc pd = params[i];
+    pi = i;
+    lo = pd.offset;
+    hi = pd.offset + pd.size;
+    rule_begin = pd.rule_begin;
+    rule_count = pd.rule_count;
+    uniform = true;
+    bits = full;
+    for (int r = 0; r < rule_count; ++r) {
+      const sdp_rule_desc rd = rules[rule_begin + r];
+      if (rd.dim != 1) {
+        uniform = false;
+        break;
+      }
+      bits &= __ldg(unit_bits + rd.unit_base);
+    }
+  }
+
+  __device__ __forceinline__ uint64_t owners(const sdp_rule_desc* __restrict__ rules,
+                                             const uint64_t* __restrict__ unit_bits, uint64_t full,
+                                             int64_t j) const {
+    if (uniform) return bits;
+    const uint32_t le = static_cast<uint32_t>(j - lo);
+    uint64_t b = full;
+    for (int r = 0; r < rule_count; ++r) {
+      const sdp_rule_desc rd = rules[rule_begin + r];
+      const uint32_t q = fdiv(le, rd.inner_mul, rd.inner_shr);
+      const uint32_t u = q - fdiv(q, rd.dim_mul, rd.dim_shr) * static_cast<uint32_t>(rd.dim);
+      b &= __ldg(unit_bits + static_cast<uint32_t>(rd.unit_base) + u);
+    }
+    return b;
+  }
+};
+
+template <typename M>
+__device__ __forceinline__ void st_mask_pair(M* p, uint64_t b0, uint64_t b1) {
+  if constexpr (sizeof(M) == 1) {
+    *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>((b0 & 0xff) | ((b1 & 0xff) << 8));
+  } else if constexpr (sizeof(M) == 2) {
+    *reinterpret_cast<uint32_t*>(p) = static_cast<uint32_t>((b0 & 0xffff) | ((b1 & 0xffff) << 16));
+  } else if constexpr (sizeof(M) == 4) {
+    *reinterpret_cast<uint64_t*>(p) = (b0 & 0xffffffffull) | (b1 << 32);
+  } else {
+    *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(b0, b1);
+  }
+}
+
+// A warp owns 1024 consecutive elements; per iteration lane l takes the pair
+// (2l, 2l + 1) of the next 64, so every store instruction writes 64
+// consecutive elements with 16-B (8-B arrays) or 2..16-B (masks) vectors.
+// Output buffers are 16-B aligned (checked by sdp_build_masks).
 template <int MB>
 __global__ void __launch_bounds__(kBuildThreads)
 k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
@@ -208,43 +268,78 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
   const int64_t n_chunks = (total + kWarpChunk - 1) / kWarpChunk;
   const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  ParamCursor cur;
+  cur.pi = -1;
   for (int64_t c = warp0; c < n_chunks; c += n_warps) {  // warp-uniform trip count
-    const int64_t base = c * kWarpChunk;
-    int pi = find_param(params, n_params, min(base + lane, total - 1));
-    sdp_param_desc pd = params[pi];
-    uint64_t bits[kLaneElems];
-#pragma unroll
-    for (int e = 0; e < kLaneElems; ++e) {
-      const int64_t j = base + e * 32 + lane;
-      bits[e] = 0;
-      if (j >= total) continue;
-      while (j >= pd.offset + pd.size) pd = params[++pi];
-      const uint32_t le = static_cast<uint32_t>(j - pd.offset);
-      uint64_t b = full;
-      for (int r = 0; r < pd.rule_count; ++r) {
-        const sdp_rule_desc rd = rules[pd.rule_begin + r];
-        const uint32_t q = fdiv(le, rd.inner_mul, rd.inner_shr);
-        const uint32_t u = q - fdiv(q, rd.dim_mul, rd.dim_shr) * static_cast<uint32_t>(rd.dim);
-        b &= __ldg(unit_bits + static_cast<uint32_t>(rd.unit_base) + u);
+    const int64_t base = c * kWarpChunk + 2 * lane;
+    if (cur.pi < 0 || base < cur.lo || base >= cur.hi)
+      cur.load(params, rules, unit_bits, full, find_param(params, n_params, min(base, total - 1)));
+    // per-worker held counts of this lane: N <= 8 packs one 8-bit counter per
+    // worker into a register (<= 32 elements per lane per chunk); more
+    // workers use a local array
+    uint64_t packed = 0;
+    unsigned cnt[64];
+    if (active_counts && n_workers > 8)
+      for (int w = 0; w < n_workers; ++w) cnt[w] = 0;
+#pragma unroll 4
+    for (int it = 0; it < kPairIters; ++it) {
+      const int64_t j = base + it * 64;
+      if (j >= total) break;
+      const bool two = j + 1 < total;
+      while (j >= cur.hi) cur.load(params, rules, unit_bits, full, cur.pi + 1);
+      const uint64_t b0 = cur.owners(rules, unit_bits, full, j);
+      const int32_t g0 = cur.rule_count;
+      uint64_t b1 = 0;
+      int32_t g1 = 0;
+      if (two) {
+        while (j + 1 >= cur.hi) cur.load(params, rules, unit_bits, full, cur.pi + 1);
+        b1 = cur.owners(rules, unit_bits, full, j + 1);
+        g1 = cur.rule_count;
       }
-      bits[e] = b;
-      const int cnt = __popcll(b);
-      if (owner_mask) owner_mask[j] = static_cast<M>(b);
-      if (coverage) coverage[j] = cnt;
-      if (divisor) divisor[j] = static_cast<double>(cnt > 0 ? cnt : 1);
-      if (governors) governors[j] = pd.rule_count;
-      if (param_masks)
-        for (int w = 0; w < n_workers; ++w)
-          param_masks[static_cast<int64_t>(w) * total + j] = static_cast<uint8_t>((b >> w) & 1ull);
+      const int c0 = __popcll(b0), c1 = __popcll(b1);
+      if (two) {
+        if (owner_mask) st_mask_pair<M>(owner_mask + j, b0, b1);
+        if (coverage) *reinterpret_cast<longlong2*>(coverage + j) = make_longlong2(c0, c1);
+        if (divisor) *reinterpret_cast<double2*>(divisor + j) = make_double2(c0 > 0 ? c0 : 1, c1 > 0 ? c1 : 1);
+        if (governors) *reinterpret_cast<longlong2*>(governors + j) = make_longlong2(g0, g1);
+        if (param_masks)
+          for (int w = 0; w < n_workers; ++w) {
+            uint8_t* pm = param_masks + static_cast<int64_t>(w) * total + j;
+            if (total & 1) {  // odd d: row w starts at an odd byte for odd w
+              pm[0] = static_cast<uint8_t>((b0 >> w) & 1ull);
+              pm[1] = static_cast<uint8_t>((b1 >> w) & 1ull);
+            } else {
+              *reinterpret_cast<uint16_t*>(pm) =
+                  static_cast<uint16_t>(((b0 >> w) & 1ull) | (((b1 >> w) & 1ull) << 8));
+            }
+          }
+      } else {
+        if (owner_mask) owner_mask[j] = static_cast<M>(b0);
+        if (coverage) coverage[j] = c0;
+        if (divisor) divisor[j] = static_cast<double>(c0 > 0 ? c0 : 1);
+        if (governors) governors[j] = g0;
+        if (param_masks)
+          for (int w = 0; w < n_workers; ++w)
+            param_masks[static_cast<int64_t>(w) * total + j] = static_cast<uint8_t>((b0 >> w) & 1ull);
+      }
+      if (active_counts) {
+        if (n_workers <= 8) {
+          constexpr uint64_t kSpread = 0x0002040810204081ull, kLow = 0x0101010101010101ull;
+          // bit w -> byte w: bits 0-6 by one multiply (no carries), bit 7 by a shift
+          packed += (((b0 & 0x7f) * kSpread) & kLow) | ((b0 & 0x80) << 49);
+          packed += (((b1 & 0x7f) * kSpread) & kLow) | ((b1 & 0x80) << 49);
+        } else {
+          for (int w = 0; w < n_workers; ++w)
+            cnt[w] += static_cast<unsigned>(((b0 >> w) & 1ull) + ((b1 >> w) & 1ull));
+        }
+      }
     }
     if (active_counts) {
       // held-parameter count per worker: warp-shuffle reduce, one atomic per warp
       for (int w = 0; w < n_workers; ++w) {
-        unsigned cnt = 0;
-#pragma unroll
-        for (int e = 0; e < kLaneElems; ++e) cnt += static_cast<unsigned>((bits[e] >> w) & 1ull);
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0 && cnt) atomicAdd(active_counts + w, static_cast<unsigned long long>(cnt));
+        const unsigned mine = n_workers <= 8 ? static_cast<unsigned>((packed >> (8 * w)) & 0xff) : cnt[w];
+        const unsigned t = __reduce_add_sync(0xffffffffu, mine);
+        if (lane == 0 && t) atomicAdd(active_counts + w, static_cast<unsigned long long>(t));
       }
     }
   }
@@ -372,6 +467,11 @@ int sdp_build_masks(const sdp_param_desc* params, int n_params, const sdp_rule_d
   if (owner_mask && (check_mask_bytes(mask_bytes) || mask_bytes * 8 < n_workers))
     return set_error(SDP_ERR_CONFIG, "mask_bytes=%d cannot hold %d workers", mask_bytes, n_workers);
   if (n_params < 1 || total < 1) return set_error(SDP_ERR_TOPOLOGY, "empty topology");
+  for (const void* p : {static_cast<const void*>(owner_mask), static_cast<const void*>(param_masks),
+                        static_cast<const void*>(coverage), static_cast<const void*>(divisor),
+                        static_cast<const void*>(governors)})
+    if (reinterpret_cast<uintptr_t>(p) % 16)
+      return set_error(SDP_ERR_USAGE, "sdp_build_masks outputs must be 16-byte aligned");
   const int64_t n_chunks = (total + kWarpChunk - 1) / kWarpChunk;
   const int64_t want = (n_chunks + kBuildThreads / 32 - 1) / (kBuildThreads / 32);
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 8));

@@ -62,6 +62,67 @@ def test_aggregate_f32_bitexact_vs_restatement_and_tolerance(cuda, case):
     assert np.all(np.abs(out - ref) <= REL_TOL_F32 * scale)
 
 
+def _pinned(arr):
+    t = torch.empty(arr.shape, dtype=torch.from_numpy(arr).dtype, pin_memory=True)
+    t.copy_(torch.from_numpy(arr))
+    return t.numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_host_paths_bitexact(cuda, dtype):
+    """engine.aggregate on numpy inputs: pinned (zero-copy kernel reads over
+    PCIe, writes the mean into pinned memory), pageable (pipelined copies) and
+    device inputs give the same bits, and the reference's bits in float64."""
+    engine, _ = _pkg()
+    for case in G.cases(with_grads=True)[:6]:
+        a = _build(case)
+        masks = G.case_masks(case)
+        grads, _, _ = G.case_inputs(case, masks)
+        g = grads.astype(dtype)
+        pinned = engine.aggregate([_pinned(x) for x in g], a).gbar
+        pageable = engine.aggregate(list(g), a).gbar
+        dev = engine.aggregate([torch.from_numpy(x).to(cuda) for x in g], a).gbar.cpu().numpy()
+        view = np.uint64 if dtype == np.float64 else np.uint32
+        assert np.array_equal(pinned.view(view), dev.view(view))
+        assert np.array_equal(pageable.view(view), dev.view(view))
+        if dtype == np.float64:
+            ref = G.arrays()[f"c{case['id']}_gbar"]
+            assert np.array_equal(pinned.view(np.uint64), ref.view(np.uint64))
+
+
+def test_host_results_are_fresh(cuda):
+    """The pinned result pool never hands out a buffer the caller still holds
+    (engine.py:60-79 returns a fresh gbar every call)."""
+    engine, _ = _pkg()
+    case = G.cases(with_grads=True)[0]
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    g1 = [_pinned(x) for x in grads.astype(np.float32)]
+    g2 = [_pinned(x * 2) for x in grads.astype(np.float32)]
+    r1 = engine.aggregate(g1, a).gbar
+    keep = r1.copy()
+    sub = r1[1:]  # a view keeps the buffer in use too
+    del r1
+    r2 = engine.aggregate(g2, a).gbar
+    assert np.array_equal(sub, keep[1:])
+    assert np.shares_memory(sub, r2) is False
+    assert np.array_equal(r2, keep * 2)
+
+
+def test_uncovered_leak_pinned_host(cuda):
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import ProtocolError
+    case = next(c for c in G.cases(with_grads=True) if c["uncovered_params"] > 0)
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    unc = np.nonzero(~masks.any(0))[0]
+    grads[1, unc[0]] = np.nan
+    with pytest.raises(ProtocolError, match="zero mask coverage"):
+        engine.aggregate([_pinned(x) for x in grads], a)
+
+
 def test_disjoint_known_answer(cuda):
     """SPEC.md:298: m1=[1,0], m2=[0,1], g1=[2,0], g2=[0,4] -> [2,4]."""
     engine, masking = _pkg()

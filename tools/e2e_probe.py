@@ -1,26 +1,105 @@
-import time, torch, numpy as np, sys
-sys.path.insert(0, '.')
-from paper_2507_09029_b200 import masking, zoo, engine
+"""Break down the host-buffer aggregate (bench.py's e2e leg) on one B200.
+
+    python tools/e2e_probe.py
+
+Raw pinned H2D / D2H / bidirectional copy bandwidth, the owned-range H2D the
+aggregate issues, and engine.aggregate at several pipeline depths.
+"""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2507_09029_b200 import engine, masking, zoo  # noqa: E402
+
 dev = torch.device('cuda', 0)
-topo = zoo.resnet18_cifar_topology(); d = topo.total
+topo = zoo.resnet18_cifar_topology()
+d = topo.total
 a = masking.build_assignment(topo, 'block', 8, 4, seed=1)
 host = []
 for w in range(8):
-    t = torch.empty(d, pin_memory=True); t.normal_(); host.append(t.numpy())
-h = torch.from_numpy(host[0]); print('from_numpy pinned:', h.is_pinned())
+    t = torch.empty(d, pin_memory=True)
+    t.normal_()
+    host.append(t.numpy())
 dst = [torch.empty(d, device=dev) for _ in range(8)]
-def tm(f, n=5):
-    f(); torch.cuda.synchronize(); t0=time.perf_counter()
-    for _ in range(n): f()
-    torch.cuda.synchronize(); return (time.perf_counter()-t0)/n*1e3
-print('8 full H2D ms', tm(lambda: [dst[w].copy_(torch.from_numpy(host[w]), non_blocking=True) for w in range(8)]))
+
+
+def tm(f, n=10):
+    f()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        f()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / n * 1e3
+
+
+big_h = torch.empty(64 << 20, pin_memory=True)
+big_d = torch.empty(64 << 20, device=dev)
+ms = tm(lambda: big_d.copy_(big_h, non_blocking=True))
+print(f'H2D 256 MiB one copy: {ms:.3f} ms  {256 * 2**20 / ms / 1e6:.1f} GB/s')
+ms = tm(lambda: big_h.copy_(big_d, non_blocking=True))
+print(f'D2H 256 MiB one copy: {ms:.3f} ms  {256 * 2**20 / ms / 1e6:.1f} GB/s')
+s2 = torch.cuda.Stream(dev)
+big_h2 = torch.empty(64 << 20, pin_memory=True)
+big_d2 = torch.empty(64 << 20, device=dev)
+
+
+def bidir():
+    big_d.copy_(big_h, non_blocking=True)
+    with torch.cuda.stream(s2):
+        big_h2.copy_(big_d2, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s2)
+
+
+ms = tm(bidir)
+print(f'bidirectional 256+256 MiB: {ms:.3f} ms  {512 * 2**20 / ms / 1e6:.1f} GB/s total')
 plan = a.sync_plan()
-print('ranges per worker', [len(plan.worker_ranges(w)) for w in range(8)])
-print('range H2D ms', tm(lambda: [dst[w][s:s+l].copy_(torch.from_numpy(host[w])[s:s+l], non_blocking=True) for w in range(8) for s,l in plan.worker_ranges(w)]))
-out = torch.empty(d, pin_memory=True); g = torch.empty(d, device=dev)
-print('D2H ms', tm(lambda: out.copy_(g, non_blocking=True)))
-print('aggregate ms', tm(lambda: engine.aggregate(host, a)))
-engine.HOST_CHUNKS = 1
-print('aggregate 1 chunk ms', tm(lambda: engine.aggregate(host, a)))
-engine.HOST_CHUNKS = 4
-print('aggregate 4 chunk ms', tm(lambda: engine.aggregate(host, a)))
+rng = [plan.worker_ranges(w) for w in range(8)]
+owned = sum(ln for r in rng for _, ln in r) * 4
+print('ranges per worker', [len(r) for r in rng], 'owned H2D bytes', owned)
+ms = tm(lambda: [dst[w].copy_(torch.from_numpy(host[w]), non_blocking=True) for w in range(8)])
+print(f'8 full H2D: {ms:.3f} ms  {8 * d * 4 / ms / 1e6:.1f} GB/s')
+ms = tm(lambda: [dst[w][s:s + ln].copy_(torch.from_numpy(host[w])[s:s + ln], non_blocking=True)
+                 for w in range(8) for s, ln in rng[w]])
+print(f'owned-range H2D: {ms:.3f} ms  {owned / ms / 1e6:.1f} GB/s')
+for k in (1, 2, 4, 8, 16):
+    engine.HOST_CHUNKS = k
+    ms = tm(lambda: engine.aggregate(host, a))
+    print(f'aggregate {k:2d} chunks: {ms:.3f} ms  e2e {plan.owned_elems * 4 / ms / 1e6:.1f} GB/s')
+engine.HOST_CHUNKS = 8
+t0 = time.perf_counter()
+for _ in range(10):
+    engine.aggregate(host, a)
+print('host-side per call (incl. sync) ms', (time.perf_counter() - t0) / 10 * 1e3)
+
+# zero-copy experiment: k_owner_sync reads the pinned host gradients over PCIe
+# and writes the mean straight into pinned host memory (no staging copies)
+import ctypes as C  # noqa: E402
+
+from paper_2507_09029_b200 import _native as N  # noqa: E402
+
+hp = [torch.from_numpy(h) for h in host]
+print('inputs pinned:', all(t.is_pinned() for t in hp))
+out_h = torch.empty(d, pin_memory=True)
+for tl in (2048, 8192):
+    zplan = a.sync_plan(tile=tl)
+    args = zplan.args(N.DTYPE_F32)
+    for w in range(8):
+        args.replicas[w] = hp[w].data_ptr()
+    args.out = out_h.data_ptr()
+    args.flags = 0
+    fn = N.lib().sdp_owner_sync
+
+    def zc():
+        rc = fn(C.byref(args), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0, N.lib().sdp_last_error()
+        torch.cuda.current_stream().synchronize()
+
+    ms = tm(zc)
+    ref = engine.aggregate(host, a).gbar
+    print(f'zero-copy sync tile {tl} grid {zplan.grid}: {ms:.3f} ms  e2e {plan.owned_elems * 4 / ms / 1e6:.1f} GB/s',
+          'bit-exact' if np.array_equal(out_h.numpy().view(np.uint32), ref.view(np.uint32)) else 'MISMATCH')
