@@ -1,8 +1,9 @@
 // Block-assignment and mask builder (masking.py:56-359) on the device.
 //
-//   k_assign       one warp: SeedSequence -> PCG64 -> per-group Fisher-Yates,
-//                  cyclic windows (masking.py:56-117).  Sequential by nature
-//                  (O(units)); bit-exact with numpy default_rng.
+//   k_assign       one CTA: SeedSequence -> PCG64 stream generated in parallel
+//                  (affine jump-ahead) -> per-group Fisher-Yates on one thread
+//                  (sequential by definition) -> cyclic windows
+//                  (masking.py:56-117); bit-exact with numpy default_rng.
 //   k_build_masks  HBM-bound expansion: every element ANDs the owner sets of
 //                  the units that govern it (masking.py:131-149, 160-169) and
 //                  emits owner mask / [N,d] bool / coverage / divisor /
@@ -122,33 +123,119 @@ __device__ __forceinline__ uint64_t window_bits(uint64_t slot, int n, int p) {
   return ((low << start) | (low >> (n - start))) & full;
 }
 
-// One CTA.  Thread 0 runs the inherently sequential Fisher-Yates draws of each
-// group (one generator across groups, masking.py:107-116); the whole CTA then
-// writes that group's window masks.
-__global__ void k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups,
-                         int n_groups, int n_units, int n_workers, int replication,
-                         uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch,
-                         int smem_cap) {
-  extern __shared__ int32_t s_perm[];
+// ---- PCG64 stream generated in parallel ------------------------------------
+// The LCG step x -> M x + inc (mod 2^128) is affine, so k steps are the affine
+// map (M^k, inc (M^(k-1) + ... + 1)): every thread jumps to its own offset by
+// binary exponentiation and then steps through its slice of the stream.
+struct Affine128 {
+  u128 a, c;  // x -> a x + c
+};
+
+__device__ __forceinline__ Affine128 compose(const Affine128& f, const Affine128& g) {  // f after g
+  return {f.a * g.a, f.a * g.c + f.c};
+}
+
+__device__ __forceinline__ u128 pcg_mult() {
+  return (static_cast<u128>(0x2360ED051FC65DA4ull) << 64) | 0x4385DF649FCCF645ull;
+}
+
+__device__ __forceinline__ u128 jump(u128 x, u128 inc, uint64_t k) {
+  Affine128 r{1, 0}, b{pcg_mult(), inc};
+  while (k) {
+    if (k & 1) r = compose(b, r);
+    b = compose(b, b);
+    k >>= 1;
+  }
+  return r.a * x + r.c;
+}
+
+__device__ __forceinline__ uint64_t pcg_output(u128 state) {  // XSL-RR
+  const uint64_t hi = static_cast<uint64_t>(state >> 64), lo = static_cast<uint64_t>(state);
+  const uint32_t rot = static_cast<uint32_t>(hi >> 58);
+  const uint64_t x = hi ^ lo;
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+constexpr int kAssignThreads = 256;
+constexpr int kAssignWords = 8192;               // 32-bit words per refill (4096 raw draws)
+constexpr int kRawPerThread = kAssignWords / 2 / kAssignThreads;
+
+// words[2k], words[2k+1] = low, high half of the k-th next 64-bit output after
+// *state (numpy's buffered 32-bit draws consume them in exactly this order);
+// *state advances by kAssignWords / 2 steps.  Whole CTA.
+__device__ void refill_words(uint32_t* words, u128* state, u128 inc) {
+  const u128 base = *state;
+  u128 x = jump(base, inc, static_cast<uint64_t>(threadIdx.x) * kRawPerThread);
+  const u128 m = pcg_mult();
+  for (int s = 0; s < kRawPerThread; ++s) {
+    x = m * x + inc;
+    const uint64_t out = pcg_output(x);
+    const int k = threadIdx.x * kRawPerThread + s;
+    words[2 * k] = static_cast<uint32_t>(out);
+    words[2 * k + 1] = static_cast<uint32_t>(out >> 32);
+  }
+  __syncthreads();  // everyone has read *state
+  if (threadIdx.x == kAssignThreads - 1) *state = x;
+  __syncthreads();
+}
+
+// One CTA.  The PCG64 stream is generated cooperatively, kAssignWords 32-bit
+// draws at a time, into shared memory (affine jump-ahead per thread); thread 0
+// then runs the inherently sequential Fisher-Yates of each group
+// (Generator.shuffle, one generator across groups, masking.py:107-116) on
+// plain shared-memory reads -- the 128-bit LCG chain is off its critical path
+// (~80 ns per unit on B200, shared-memory latency bound; splitting draws and
+// swaps into two concurrent warps measured no faster) -- and the whole CTA
+// writes the group's window masks.
+__global__ void __launch_bounds__(kAssignThreads)
+k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups, int n_units,
+         int n_workers, int replication, uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch,
+         int perm_cap) {
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t* words = s_dyn;
+  int32_t* s_perm = reinterpret_cast<int32_t*>(s_dyn + kAssignWords);
+  __shared__ u128 s_state, s_inc;
+  __shared__ int s_p, s_i;
   const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
   for (int u = threadIdx.x; u < n_units; u += blockDim.x) unit_bits[u] = full;
-  Pcg64 g;
-  if (threadIdx.x == 0) seed_pcg(g, seed.w, seed.n);
+  if (threadIdx.x == 0) {
+    Pcg64 g;
+    seed_pcg(g, seed.w, seed.n);
+    s_state = g.state;
+    s_inc = g.inc;
+    s_p = 0;
+  }
+  __syncthreads();
+  const u128 inc = s_inc;
+  refill_words(words, &s_state, inc);
   uint64_t slot = 0;
   for (int gi = 0; gi < n_groups; ++gi) {
     const int first = groups[gi].first_unit, size = groups[gi].size;
-    int32_t* a = size <= smem_cap ? s_perm : scratch;
+    int32_t* a = size <= perm_cap ? s_perm : scratch;
     __syncthreads();  // previous group's readers are done with a[]
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < size; ++i) a[i] = i;
-      for (int i = size - 1; i > 0; --i) {  // Generator.shuffle (Fisher-Yates)
-        const int j = static_cast<int>(g.interval(static_cast<uint64_t>(i)));
-        const int32_t t = a[i];
-        a[i] = a[j];
-        a[j] = t;
-      }
-    }
+    for (int k = threadIdx.x; k < size; k += blockDim.x) a[k] = k;
+    if (threadIdx.x == 0) s_i = size - 1;
     __syncthreads();
+    while (true) {
+      if (threadIdx.x == 0) {  // Generator.shuffle (Fisher-Yates), masked rejection draws
+        int i = s_i, p = s_p;
+        while (i > 0 && p < kAssignWords) {
+          const uint32_t v = words[p++] & (0xffffffffu >> __clz(i));
+          if (v > static_cast<uint32_t>(i)) continue;
+          const int32_t t = a[i];
+          a[i] = a[v];
+          a[v] = t;
+          --i;
+        }
+        s_i = i;
+        s_p = p;
+      }
+      __syncthreads();
+      if (s_i == 0) break;
+      refill_words(words, &s_state, inc);  // the stream ran out mid-group
+      if (threadIdx.x == 0) s_p = 0;
+      __syncthreads();
+    }
     for (int k = threadIdx.x; k < size; k += blockDim.x)
       unit_bits[first + a[k]] = window_bits(slot + k, n_workers, replication);
     slot += size;
@@ -464,11 +551,14 @@ int sdp_assign_units(const uint32_t* seed_words, int n_seed_words, const sdp_gro
   if (!seed_words || n_seed_words < 1 || n_seed_words > 8)
     return set_error(SDP_ERR_CONFIG, "seed must be given as 1..8 uint32 words");
   if (!unit_bits || !groups) return set_error(SDP_ERR_USAGE, "null device pointer");
-  const int smem_cap = 48 * 1024 / 4;
+  const int smem_cap = 12288;  // units per group held in shared memory
   const int smem_elems = max_group <= smem_cap ? max_group : 0;
   if (max_group > smem_cap && !scratch)
     return set_error(SDP_ERR_USAGE, "group of %d units needs a scratch buffer", max_group);
-  k_assign<<<1, 256, smem_elems * sizeof(int32_t), as_stream(stream)>>>(
+  const size_t smem = (kAssignWords + static_cast<size_t>(smem_elems)) * sizeof(uint32_t);
+  SDP_CUDA_CHECK(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+  k_assign<<<1, kAssignThreads, smem, as_stream(stream)>>>(
       make_seed(seed_words, n_seed_words), groups, n_groups, n_units, n_workers, replication,
       unit_bits, scratch, smem_elems);
   SDP_LAUNCH_CHECK();

@@ -238,3 +238,24 @@ def test_large_topologies_match_oracle(cuda):
     cov = a.coverage.cpu().numpy()
     assert cov.size == 124_439_808
     assert int((cov == 4).sum()) == 12 * 7_087_872 and int((cov == 8).sum()) == 39_385_344
+
+
+@pytest.mark.parametrize("sizes", [[20000], [5000, 7000, 3000, 9000, 1, 2]],
+                         ids=["scratch-group", "multi-refill"])
+def test_device_assign_long_streams(cuda, sizes):
+    """k_assign over groups that outrun one refill of the parallel PCG64 stream
+    (8192 words) and a group too large for shared memory: the unit owner bits
+    equal numpy's default_rng permutations (masking.py:107-116) drawn in order."""
+    masking = _m()
+    groups, pos = [], 0
+    for s in sizes:
+        groups.append((pos, s))
+        pos += s
+    got = masking._device_assign(groups, pos, 8, 3, 7, cuda).cpu().numpy().view(np.uint64)
+    rng = np.random.default_rng(7)
+    want, slot = np.zeros(pos, dtype=np.uint64), 0
+    for first, s in groups:
+        for k, u in enumerate(rng.permutation(s)):
+            want[first + int(u)] = O.window_bits(slot + k, 8, 3)
+        slot += s
+    assert np.array_equal(got, want)
