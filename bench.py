@@ -444,11 +444,12 @@ def run_train(args, dev):
     batches = [(torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
                 torch.randint(0, 10, (batch,), generator=gen, device=dev)) for _ in range(n)]
     out = {"workload": f"ResNet-18 CIFAR-shape, N={n} co-resident workers, batch {batch}/worker, "
-                       "bf16 autocast fwd/bwd, fused sync+Nesterov+bf16 cast", "data": "synthetic"}
+                       "bf16 autocast fwd/bwd, fused sync+Nesterov+bf16 cast, whole step in one CUDA graph",
+           "data": "synthetic"}
     for tag, p, strategy in (("subnet", args.p, "block"), ("widthwise", args.p, "neuron"), ("dp", n, "block")):
         model = train.build_resnet18(dev)
         a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=0.02, sync_layout=(strategy == "neuron"))
+        tr = train.SubnetTrainer(model, a, lr=0.02, sync_layout=(strategy == "neuron"), graphed=True)
         out[f"{tag}_loss_first"] = float(tr.step(batches).item())
         for _ in range(2):
             tr.step(batches)
@@ -492,11 +493,12 @@ def run_train_gpt2(args, dev, micro_batch: int = 8, seq: int = 1024):
     batches = [(lambda t: (t, t))(torch.randint(0, 50257, (micro_batch, seq), generator=gen, device=dev))
                for _ in range(n)]
     out = {"workload": f"GPT-2 small 124M, seq {seq}, N={n} co-resident workers x micro-batch "
-                       f"{micro_batch}, bf16 autocast, flash SDPA, fused sync+Nesterov+bf16", "data": "synthetic tokens"}
+                       f"{micro_batch}, bf16 autocast, flash SDPA, fused sync+Nesterov+bf16, whole step in one "
+                       "CUDA graph", "data": "synthetic tokens"}
     for tag, p in (("subnet", args.p), ("dp", n)):
         model = train.build_gpt2(dev)
         a = masking.build_assignment(model.topology, "block", n, p, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=1e-4, loss_fn=train.lm_loss)
+        tr = train.SubnetTrainer(model, a, lr=1e-4, loss_fn=train.lm_loss, graphed=True)
         out[f"{tag}_loss_first"] = float(tr.step(batches).item())
         tr.step(batches)
         torch.cuda.synchronize()

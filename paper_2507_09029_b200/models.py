@@ -436,8 +436,12 @@ class SubnetLayout:
         return t
 
     def views(self, compact: torch.Tensor) -> dict:
-        return {p.name: compact[self.offsets[p.name]:self.offsets[p.name] + int(np.prod(self.shapes[p.name]))]
-                .view(self.shapes[p.name]) for p in self.topology.params}
+        """Per-parameter views of the compact buffer: one split (backward = one
+        concatenation, not a [compact] zero-fill + accumulate per parameter)."""
+        sizes = [int(np.prod(self.shapes[p.name])) for p in self.topology.params]
+        flat = compact if compact.numel() == sum(sizes) else compact[:sum(sizes)]
+        parts = flat.split(sizes)
+        return {p.name: t.view(self.shapes[p.name]) for p, t in zip(self.topology.params, parts)}
 
     # -- kernels --------------------------------------------------------------
     def gather(self, theta: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -63,7 +63,7 @@ class ResNet18Cifar:
             o = F.conv2d(o, params[f"{p}.conv2.w"], padding=1)
             o = self._gn(o, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"], worker, f"{p}.conv2")
             if down:
-                sc = F.conv2d(h, params[f"{p}.down.w"], stride=stride)
+                sc = downsample(h, params[f"{p}.down.w"], stride)
                 sc = F.group_norm(sc, g, params[f"{p}.down_gn.gamma"], params[f"{p}.down_gn.beta"])
             else:
                 sc = h
@@ -95,7 +95,7 @@ class ResNet18Cifar:
             o = ragged_group_norm(o, a2 // gsize, g, cp[f"{p}.gn2.gamma"], cp[f"{p}.gn2.beta"],
                                   counts=sub.group_counts(f"{p}.conv2", planes, g))
             if down:
-                sc = F.conv2d(h, cp[f"{p}.down.w"], stride=stride)
+                sc = downsample(h, cp[f"{p}.down.w"], stride)
                 sc = F.group_norm(sc, g, cp[f"{p}.down_gn.gamma"], cp[f"{p}.down_gn.beta"])
             else:
                 sc = h
@@ -166,7 +166,23 @@ def build_gpt2(dev, seed: int = 1) -> GlobalModel:
 
 
 def param_views(topology, flat: torch.Tensor) -> dict:
-    return {p.name: flat[p.offset:p.offset + p.size].view(p.shape) for p in topology.params}
+    """Per-parameter views of the flat vector.  One split (the parameters tile
+    [0, d) in order, topology.py:66-74): its backward is ONE concatenation of
+    the parameter gradients, where per-parameter slicing would zero-fill and
+    accumulate a [d] gradient once per parameter (62 x 2 x 44 MB per ResNet-18
+    worker step)."""
+    parts = flat.split([p.size for p in topology.params])
+    return {p.name: t.view(p.shape) for p, t in zip(topology.params, parts)}
+
+
+def downsample(h: torch.Tensor, w: torch.Tensor, stride: int) -> torch.Tensor:
+    """1x1 convolution with stride s == subsample then 1x1 stride-1 convolution
+    (the strided 1x1 kernel reads only every s-th position).  cuDNN's strided
+    1x1 data-gradient falls back to a direct kernel (~0.44 ms per ResNet-18
+    layer4 worker step on B200); the stride-1 form runs on the GEMM path."""
+    if stride == 1:
+        return F.conv2d(h, w)
+    return F.conv2d(h[:, :, ::stride, ::stride], w)
 
 
 @dataclass
@@ -185,8 +201,13 @@ class SubnetTrainer:
 
     def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
                  autocast: bool = True, compact: bool | None = None, loss_fn=None,
-                 sync_layout: bool = False):
+                 sync_layout: bool = False, graphed: bool = False):
+        """graphed: capture the whole protocol step (N worker fwd/bwd, gather /
+        scatter, the fused sync) in one CUDA graph and replay it -- the eager
+        step is host-bound (thousands of small launches), see step()."""
         self.model = model
+        self.graphed = graphed
+        self._graph = None
         self.assignment = assignment
         self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
         self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
@@ -227,7 +248,44 @@ class SubnetTrainer:
         self._prep.launch()
 
     def step(self, batches) -> torch.Tensor:
-        """batches: list of N (x, y) device tensors; returns the mean loss (device)."""
+        """batches: list of N (x, y) device tensors; returns the mean loss (device).
+
+        graphed: the first call (and any call after `lr` changed) captures the
+        step into a CUDA graph -- after warm-up steps on a side stream whose
+        effect on theta / velocity is rolled back -- and every call copies the
+        batches into the graph's static inputs and replays it.  Same math, same
+        kernels, same order as the eager step."""
+        if not self.graphed:
+            return self._step_eager(batches)
+        if self._graph is None or self._graph_lr != self.lr:
+            self._capture(batches)
+        for (sx, sy), (x, y) in zip(self._static, batches):
+            if sx.data_ptr() != x.data_ptr():
+                sx.copy_(x)
+            if sy.data_ptr() != y.data_ptr():
+                sy.copy_(y)
+        self._graph.replay()
+        return self._static_loss
+
+    def _capture(self, batches, warmup: int = 2) -> None:
+        self._static = [(x.clone(), y.clone()) for x, y in batches]
+        state = [self.model.theta, self.velocity, self.theta_bf16]
+        saved = [t.clone() for t in state]
+        side = torch.cuda.Stream(self.model.theta.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # autograd / cuDNN warm-up outside the capture
+            for _ in range(warmup):
+                self._step_eager(self._static, cache=False)
+        torch.cuda.current_stream().wait_stream(side)
+        for t, v in zip(state, saved):  # the warm-up steps never happened
+            t.copy_(v)
+        del saved
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self._static_loss = self._step_eager(self._static, cache=False)
+        self._graph_lr = self.lr
+
+    def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
         topo = self.model.topology
         losses = []
         for w, (x, y) in enumerate(batches):
@@ -237,7 +295,7 @@ class SubnetTrainer:
                     leaf = self.transfers[w].to_compact(self.model.theta).requires_grad_(True)
                 else:
                     leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                     logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
                     loss = self.loss_fn(logits, y)
                 del logits
@@ -251,7 +309,7 @@ class SubnetTrainer:
             # the worker trains on the bf16 weights the previous sync wrote
             leaf = (self.theta_bf16 if self.autocast else self.model.theta).detach().requires_grad_(True)
             params = param_views(topo, leaf)
-            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                 logits = self.model.arch.forward(params, x, self.views[w])
                 loss = self.loss_fn(logits, y)
             del logits

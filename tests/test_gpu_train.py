@@ -107,3 +107,31 @@ def test_memory_subnet_below_full_replica(cuda):
     assert sub["active_params"] == a.worker_view(0).active_params
     assert full["active_params"] == model.topology.total
     assert sub["peak_bytes"] < full["peak_bytes"]
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_graphed_step_equals_eager(cuda, strategy):
+    """The CUDA-graph step (train.SubnetTrainer(graphed=True)) replays exactly
+    the eager step: same theta after three steps (deterministic cuDNN, fp32),
+    and the capture's warm-up steps leave no trace."""
+    from paper_2507_09029_b200 import masking, train
+    prev = torch.backends.cudnn.deterministic
+    torch.backends.cudnn.deterministic = True
+    try:
+        gen = torch.Generator(device=cuda)
+        gen.manual_seed(4)
+        steps = [[(torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
+                   torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(8)]
+                 for _ in range(3)]
+        out = []
+        for graphed in (False, True):
+            model = train.build_resnet18(cuda, seed=5)
+            a = masking.build_assignment(model.topology, strategy, 8, 4, seed=1)
+            tr = train.SubnetTrainer(model, a, lr=0.05, autocast=False, graphed=graphed,
+                                     sync_layout=strategy == "neuron")
+            losses = [float(tr.step(b).item()) for b in steps]
+            out.append((tr.theta().cpu().numpy(), losses))
+        assert out[0][1] == out[1][1]
+        assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
+    finally:
+        torch.backends.cudnn.deterministic = prev
