@@ -333,7 +333,7 @@ def build_resnet18(dev, seed: int = 1) -> GlobalModel:
 
 
 def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int,
-                  dev, make_batch=None, loss_fn=None) -> dict:
+                  dev, make_batch=None, loss_fn=None, return_grad: bool = False) -> dict:
     """Peak device memory of ONE worker's training state and step, as a GPU
     holding one worker would see it (paper: params, grads, optimizer state and
     activations all scale with the subnetwork).  worker=None: the full model
@@ -357,24 +357,49 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
     torch.cuda.empty_cache()
     base = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
-    # compact fp32 master (the leaf) + momentum + bf16 copy; autograd adds the grad
-    master = sub.gather(model.theta).requires_grad_(True)
+    # compact fp32 master + fp32 gradient (what the sync reads) + momentum + bf16
+    # training copy.  The step mirrors SubnetTrainer's: block workers run on
+    # the bf16 copy, width-wise workers on the fp32 compact master under
+    # autocast (no weight-cast cache, as in the graphed step).  Every
+    # parameter is a leaf view whose gradient is written into its slot of the
+    # fp32 flat gradient the moment autograd finishes it and then freed
+    # (post-accumulate hook): no second gradient-sized buffer and no
+    # all-parameter gradient set alive at once.
+    master = sub.gather(model.theta)
+    grad = torch.zeros_like(master)
     momentum = torch.zeros_like(master)
-    shadow = master.detach().to(torch.bfloat16)
-    with torch.autocast("cuda", dtype=torch.bfloat16):
+    shadow = master.to(torch.bfloat16)
+    gviews = sub.views(grad)
+    weights = sub.views(master if assignment.strategy == "neuron" else shadow)
+    leaves = {}
+    for name, v in weights.items():
+        if v.numel() == 0:
+            leaves[name] = v
+            continue
+        t = v.detach().requires_grad_(True)
+
+        def _to_flat(param, slot=gviews[name]):
+            slot.copy_(param.grad)
+            param.grad = None
+
+        t.register_post_accumulate_grad_hook(_to_flat)
+        leaves[name] = t
+    with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
         if assignment.strategy == "neuron":
-            logits = model.arch.forward_compact(sub.views(master), x, sub)
+            logits = model.arch.forward_compact(leaves, x, sub)
         else:
-            logits = model.arch.forward(sub.views(master), x, view)
+            logits = model.arch.forward(leaves, x, view)
         loss = loss_fn(logits, y)
     del logits
     loss.backward()
     torch.cuda.synchronize(dev)
     peak = torch.cuda.max_memory_allocated(dev) - base
     active = sub.compact_total
-    del master, momentum, shadow, loss
-    return {"active_params": int(active), "peak_bytes": int(peak),
-            "state_bytes": int(active * (4 * 3 + 2))}
+    out = {"active_params": int(active), "peak_bytes": int(peak), "state_bytes": int(active * (4 * 3 + 2))}
+    if return_grad:
+        out["grad"] = grad
+    del master, grad, momentum, shadow, loss, leaves
+    return out
 
 
 def build_block_assignment(topo, n=8, p=4, seed=1):

@@ -110,6 +110,34 @@ def test_memory_subnet_below_full_replica(cuda):
 
 
 @pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_memory_step_gradient_is_the_worker_gradient(cuda, strategy):
+    """worker_memory's hooked per-parameter backward produces the same compact
+    gradient as autograd on the gathered compact leaf."""
+    import torch.nn.functional as F
+    from paper_2507_09029_b200 import masking, models, train
+    model = train.build_resnet18(cuda, seed=6)
+    a = masking.build_assignment(model.topology, strategy, 8, 4, seed=1)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(2)
+    x = torch.randn(8, 3, 32, 32, generator=gen, device=cuda)
+    y = torch.randint(0, 10, (8,), generator=gen, device=cuda)
+    got = train.worker_memory(model, a, 3, 8, cuda, make_batch=lambda: (x, y), return_grad=True)["grad"]
+    sub = models.SubnetLayout(a, 3)
+    leaf = sub.gather(model.theta)
+    if strategy == "block":  # block workers train on the bf16 copy
+        leaf = leaf.to(torch.bfloat16)
+    leaf.requires_grad_(True)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        if strategy == "neuron":
+            logits = model.arch.forward_compact(sub.views(leaf), x, sub)
+        else:
+            logits = model.arch.forward(sub.views(leaf), x, a.worker_view(3))
+        loss = F.cross_entropy(logits.float(), y)
+    (want,) = torch.autograd.grad(loss, leaf)
+    assert torch.allclose(got, want.float(), rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
 def test_graphed_step_equals_eager(cuda, strategy):
     """The CUDA-graph step (train.SubnetTrainer(graphed=True)) replays exactly
     the eager step: same theta after three steps (deterministic cuDNN, fp32),
