@@ -29,7 +29,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
-def launches(src, out):
+def launches(src, out, split=None):
+    """split = (substring, threshold_us, label): launches of a kernel whose name
+    contains `substring` and that run longer than the threshold are listed
+    separately (bench.py's zero-copy e2e sync launches read host memory over
+    PCIe and take milliseconds; the device-resident ones ~100 us)."""
     rows = list(csv.reader(open(src)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
@@ -39,12 +43,16 @@ def launches(src, out):
         if len(r) > vi:
             v = float(r[vi].replace(",", ""))
             v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1)
-            agg[r[ki]].append(v)
+            key = r[ki]
+            if split and split[0] in key and v > split[1]:
+                key = f"{key} [{split[2]}]"
+            agg[key].append(v)
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# launch list: {Path(src).name}", "",
              "| launches | total us | share | avg us | kernel |", "|---:|---:|---:|---:|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-        lines.append(f"| {len(v)} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% | {sum(v) / len(v):.2f} | `{k[:110]}` |")
+        name = k if len(k) <= 110 else (k[:110] + (k[k.rindex(" ["):] if k.endswith("]") else ""))
+        lines.append(f"| {len(v)} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% | {sum(v) / len(v):.2f} | `{name}` |")
     Path(out).write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 
@@ -80,7 +88,11 @@ def full(src, out, traffic_key=None):
 if __name__ == "__main__":
     mode, src, out = sys.argv[1:4]
     if mode == "launches":
-        launches(src, out)
+        sp = None
+        if "--split" in sys.argv:  # --split SUBSTRING THRESHOLD_US LABEL
+            i = sys.argv.index("--split")
+            sp = (sys.argv[i + 1], float(sys.argv[i + 2]), sys.argv[i + 3])
+        launches(src, out, sp)
     else:
         key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
         full(src, out, key)
