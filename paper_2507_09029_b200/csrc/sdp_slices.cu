@@ -118,6 +118,64 @@ __device__ __forceinline__ void gather_tiled(const sdp_slice_task& tk, const sdp
   }
 }
 
+// Row copies (no column map): whole rows move as 16-B vectors -- a gather is
+// a typeless copy -- when every row start on both sides is 16-B aligned.
+constexpr int kVecPerThread = 2;   // 16-B vectors per thread per row
+constexpr int kVecRows = 2;        // rows per iteration: 4 vectors (64 B) in flight per thread
+
+template <typename T>
+__device__ __forceinline__ bool rows_vectorizable(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                                  const T* full, const T* compact, uint32_t row_len) {
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint32_t row_stride = static_cast<uint32_t>(d.cols) * d.inner;
+  return d.col_tab < 0 && d.col_map < 0 &&
+         ((static_cast<uint64_t>(d.full_offset) | static_cast<uint64_t>(d.compact_offset) | row_stride | row_len |
+           static_cast<uint32_t>(tk.elem_begin) | static_cast<uint32_t>(tk.elem_end)) % VE) == 0 &&
+         (reinterpret_cast<uintptr_t>(full) | reinterpret_cast<uintptr_t>(compact)) % 16 == 0;
+}
+
+template <typename T, bool REVERSE>
+__device__ __forceinline__ void gather_rows_vec(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                                const int32_t* __restrict__ fwd, T* __restrict__ full,
+                                                T* __restrict__ compact, uint32_t row_len) {
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint32_t row_stride = static_cast<uint32_t>(d.cols) * d.inner;
+  const uint32_t v0 = tk.elem_begin / VE, v1 = tk.elem_end / VE;
+  T* const fbase = full + d.full_offset;
+  T* const cbase = compact + d.compact_offset;
+  for (uint32_t vb = v0 + threadIdx.x; vb < v1; vb += kSliceThreads * kVecPerThread) {
+    for (int r0 = tk.row_begin; r0 < tk.row_end; r0 += kVecRows) {
+      uint4* fr[kVecRows];
+      uint4* cr[kVecRows];
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j) {
+        const int r = min(r0 + j, tk.row_end - 1);  // a duplicated last row rewrites identical values
+        const uint32_t f = d.row_map >= 0 ? __ldg(fwd + d.row_map + r) : static_cast<uint32_t>(r);
+        fr[j] = reinterpret_cast<uint4*>(fbase + f * row_stride);
+        cr[j] = reinterpret_cast<uint4*>(cbase + static_cast<uint32_t>(r) * row_len);
+      }
+      uint4 v[kVecRows][kVecPerThread];
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j)
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) {
+          const uint32_t q = vb + k * kSliceThreads;
+          if (q < v1) v[j][k] = REVERSE ? __ldg(cr[j] + q) : __ldg(fr[j] + q);
+        }
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j)
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) {
+          const uint32_t q = vb + k * kSliceThreads;
+          if (q < v1) {
+            if (REVERSE) fr[j][q] = v[j][k];
+            else cr[j][q] = v[j][k];
+          }
+        }
+    }
+  }
+}
+
 template <typename T, bool REVERSE>
 __device__ __forceinline__ void gather_flat(const sdp_slice_task& tk, const sdp_slice_desc& d,
                                             const int32_t* __restrict__ fwd, T* __restrict__ full,
@@ -171,8 +229,14 @@ k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restr
       const sdp_slice_task& tk = st.task[i];
       const sdp_slice_desc& d = st.desc[i];
       const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
-      if (row_len >= kSliceThreads) gather_tiled<T, REVERSE>(tk, d, fwd, full, compact, row_len);
-      else gather_flat<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+      if (row_len >= kSliceThreads) {
+        if (rows_vectorizable<T>(tk, d, full, compact, row_len))
+          gather_rows_vec<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+        else
+          gather_tiled<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+      } else {
+        gather_flat<T, REVERSE>(tk, d, fwd, full, compact, row_len);
+      }
     }
   }
 }
@@ -232,6 +296,65 @@ __device__ __forceinline__ void scatter_tiled(const sdp_slice_task& tk, const sd
           if (held || (zero_fill && co[k] != -2)) fr[j][k * kSliceThreads] = v[j][k];
         }
       }
+    }
+  }
+}
+
+// Row write-back (no column map) as 16-B vectors: held rows are copied (or
+// added elementwise in ACCUMULATE mode), rows the worker does not hold are
+// zero-filled in ZERO_FILL mode.
+template <typename T>
+__device__ __forceinline__ void scatter_rows_vec(const sdp_slice_task& tk, const sdp_slice_desc& d,
+                                                 const int32_t* __restrict__ inv, const T* __restrict__ compact,
+                                                 T* __restrict__ full, uint32_t row_len, bool zero_fill,
+                                                 bool accumulate) {
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint32_t v0 = tk.elem_begin / VE, v1 = tk.elem_end / VE;
+  const T* const cbase = compact + d.compact_offset;
+  T* const fbase = full + d.full_offset;
+  for (uint32_t vb = v0 + threadIdx.x; vb < v1; vb += kSliceThreads * kVecPerThread) {
+    for (int r0 = tk.row_begin; r0 < tk.row_end; r0 += kVecRows) {
+      uint4* fr[kVecRows];
+      const uint4* cr[kVecRows];
+      bool held[kVecRows], live[kVecRows];
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j) {
+        const int f = min(r0 + j, tk.row_end - 1);
+        live[j] = r0 + j < tk.row_end;  // never apply a duplicated row twice (accumulate)
+        const int32_t a = d.crows == 0 ? -1 : (d.row_map >= 0 ? __ldg(inv + d.row_map + f) : f);
+        held[j] = a >= 0;
+        fr[j] = reinterpret_cast<uint4*>(fbase + static_cast<uint32_t>(f) * row_len);
+        cr[j] = reinterpret_cast<const uint4*>(cbase + static_cast<uint32_t>(max(a, 0)) * row_len);
+      }
+      uint4 v[kVecRows][kVecPerThread], o[kVecRows][kVecPerThread];
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j)
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) {
+          const uint32_t q = vb + k * kSliceThreads;
+          v[j][k] = make_uint4(0, 0, 0, 0);
+          if (q < v1 && held[j]) {
+            v[j][k] = __ldg(cr[j] + q);
+            if (accumulate && live[j]) o[j][k] = fr[j][q];
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < kVecRows; ++j)
+#pragma unroll
+        for (int k = 0; k < kVecPerThread; ++k) {
+          const uint32_t q = vb + k * kSliceThreads;
+          if (q >= v1 || !live[j]) continue;
+          if (accumulate) {
+            if (!held[j]) continue;
+            T* a = reinterpret_cast<T*>(&o[j][k]);
+            const T* b = reinterpret_cast<const T*>(&v[j][k]);
+#pragma unroll
+            for (uint32_t e = 0; e < VE; ++e) a[e] = static_cast<T>(a[e] + b[e]);
+            fr[j][q] = o[j][k];
+          } else if (held[j] || zero_fill) {
+            fr[j][q] = v[j][k];  // zeros for a row the worker does not hold
+          }
+        }
     }
   }
 }
@@ -303,8 +426,14 @@ k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __rest
       const sdp_slice_task& tk = st.task[i];
       const sdp_slice_desc& d = st.desc[i];
       const uint32_t row_len = static_cast<uint32_t>(d.cols) * d.inner;
-      if (row_len >= kSliceThreads) scatter_tiled<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
-      else scatter_flat<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
+      if (row_len >= kSliceThreads) {
+        if (rows_vectorizable<T>(tk, d, full, compact, row_len))
+          scatter_rows_vec<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
+        else
+          scatter_tiled<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
+      } else {
+        scatter_flat<T>(tk, d, inv, compact, full, row_len, zero_fill, accumulate);
+      }
     }
   }
 }

@@ -187,3 +187,28 @@ def test_two_protocol_steps_match_reference(cuda, ci):
         ref = arr[f"m{ci}_theta_step{t + 1}"]
         err = np.max(np.abs(m.theta.cpu().numpy() - ref))
         assert err <= TOL_G * max(1.0, np.abs(ref).max()), err
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_gather_scatter_all_paths_full_size(cuda, strategy, dtype):
+    """ResNet-18 (C2/C3) through every slice-kernel path (16-B row copies,
+    tiled column tables, flattened short rows, dropped tensors): gather then
+    zero-fill scatter == theta on the worker's mask, 0 elsewhere; accumulate
+    scatter == base + theta on the mask, base elsewhere (bit-exact)."""
+    from paper_2507_09029_b200 import masking, models, zoo
+    topo = zoo.resnet18_cifar_topology()
+    a = masking.build_assignment(topo, strategy, 8, 4, seed=1)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(9)
+    theta = torch.randn(topo.total, generator=gen, device=cuda, dtype=dtype)
+    base = torch.randn(topo.total, generator=gen, device=cuda, dtype=dtype)
+    for w in (0, 5):
+        sub = models.SubnetLayout(a, w)
+        mask = a.worker_view(w).param_mask_bool
+        comp = sub.gather(theta)
+        assert comp.numel() >= sub.compact_total and int(mask.sum()) == sub.compact_total
+        full = sub.scatter(comp)
+        assert torch.equal(full, torch.where(mask, theta, torch.zeros((), dtype=dtype, device=cuda)))
+        acc = sub.scatter(comp, base.clone(), accumulate=True)
+        assert torch.equal(acc, torch.where(mask, base + theta, base))

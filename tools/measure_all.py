@@ -200,6 +200,11 @@ def main():
             for p in (2, 4, 8):
                 sync_case(zoo.sweep_topology(mib * (1 << 20) // 4), f"C5 sweep {mib} MiB", "block", 8, p)
                 torch.cuda.empty_cache()
+    if "sweep" in only:  # neuron variant, fragmented / uncovered owner sets
+        mr = zoo.mini_resnet_topology(512, 8, 10, 2, 3, (8, 8))
+        for p in (2, 4, 8):
+            sync_case(mr, "C5 neuron mini-ResNet c=512 K=8", "neuron", 8, p)
+            sync_case(mr, "C5 neuron mini-ResNet c=512 K=8 (sync layout)", "neuron", 8, p, sync_layout=True)
     if "slices" in only:  # width-wise extraction / write-back
         slices_case(r18, "C3 resnet18", "neuron", 8, 4)
         slices_case(gpt2, "C4 gpt2 (mlp units)", "neuron", 8, 4)
