@@ -63,6 +63,12 @@ const char* sdp_last_error(void);
 /* Number of SMs of the current device (grid sizing helper). */
 int sdp_device_sm_count(int* out);
 
+/* *out = 1 iff ptr is page-locked host memory the current device reads and
+ * writes through the SAME address (unified addressing): the zero-copy form of
+ * engine.aggregate's host-buffer path (engine.py:60-79 on numpy inputs) hands
+ * such pointers to sdp_owner_sync directly. */
+int sdp_host_ptr_on_device(const void* ptr, int* out);
+
 /* ------------------------------------------------------------------------ */
 /* Mask builder                                                              */
 /* ------------------------------------------------------------------------ */

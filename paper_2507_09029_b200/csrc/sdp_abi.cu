@@ -62,6 +62,20 @@ int sdp_device_sm_count(int* out) {
   return SDP_OK;
 }
 
+int sdp_host_ptr_on_device(const void* ptr, int* out) {
+  if (!out) return sdp::set_error(SDP_ERR_USAGE, "null out");
+  *out = 0;
+  if (!ptr) return SDP_OK;
+  cudaPointerAttributes at;
+  const cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {  // unregistered pageable memory on older drivers
+    cudaGetLastError();
+    return SDP_OK;
+  }
+  *out = at.type == cudaMemoryTypeHost && at.devicePointer == ptr ? 1 : 0;
+  return SDP_OK;
+}
+
 int sdp_ipc_export(const void* ptr, uint8_t* handle_out, uint64_t* offset_out) {
   if (!ptr || !handle_out || !offset_out) return sdp::set_error(SDP_ERR_USAGE, "null argument");
   uint64_t base = 0;

@@ -228,6 +228,16 @@ def _aligned(t: torch.Tensor) -> bool:
     return t.is_contiguous() and t.data_ptr() % 16 == 0
 
 
+def _device_readable(t: torch.Tensor) -> bool:
+    """Host tensor in page-locked memory mapped at the same address on the
+    device (libsdp sdp_host_ptr_on_device)."""
+    if t.device.type != "cpu" or t.numel() == 0:
+        return False
+    ok = C.c_int(0)
+    N.call("sdp_host_ptr_on_device", C.c_void_p(t.data_ptr()), C.byref(ok))
+    return bool(ok.value)
+
+
 class PreparedSync:
     """A fully bound k_owner_sync launch (args built once): the steady-state
     form used by training loops and the benchmark -- one ctypes call per step."""
@@ -277,7 +287,7 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     dev = assignment.device
 
     def placed(t):
-        return t.device == dev or (zero_copy and t.device.type == "cpu" and t.is_pinned())
+        return t.device == dev or (zero_copy and _device_readable(t))
 
     for r in reps:
         if r.dtype != dt or r.numel() != d or not placed(r) or not _aligned(r):
@@ -348,7 +358,7 @@ def aggregate(grads, assignment) -> AggregatedGradient:
     if host:
         dt = torch.float64 if grads[0].dtype == np.float64 else torch.float32
         hosts = [torch.from_numpy(np.ascontiguousarray(g, dtype=dt_np(dt))) for g in grads]
-        if all(h.numel() == d and _aligned(h) and h.is_pinned() for h in hosts):
+        if all(h.numel() == d and _aligned(h) and _device_readable(h) for h in hosts):
             return _aggregate_host_zero_copy(hosts, assignment, check)
     if host and not check:
         return _aggregate_host_pipelined(grads, assignment)

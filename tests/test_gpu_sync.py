@@ -90,6 +90,16 @@ def test_host_paths_bitexact(cuda, dtype):
             assert np.array_equal(pinned.view(np.uint64), ref.view(np.uint64))
 
 
+def test_zero_copy_eligibility(cuda):
+    """Only page-locked host memory mapped at the same device address takes the
+    zero-copy path; pageable numpy and device tensors do not."""
+    engine, _ = _pkg()
+    pinned = torch.from_numpy(_pinned(np.zeros(64, dtype=np.float32)))
+    assert engine._device_readable(pinned)
+    assert not engine._device_readable(torch.from_numpy(np.zeros(64, dtype=np.float32)))
+    assert not engine._device_readable(torch.zeros(64, device=cuda))
+
+
 def test_host_results_are_fresh(cuda):
     """The pinned result pool never hands out a buffer the caller still holds
     (engine.py:60-79 returns a fresh gbar every call)."""
