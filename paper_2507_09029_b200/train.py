@@ -15,13 +15,16 @@ always active.  Its parameter layout is zoo.resnet18_cifar_topolog
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 import torch.nn.functional as F
 
+from . import _native as N
 from . import engine, masking, zoo
+from ._device import ptr, stream_ptr
 from .topology import GlobalModel
 
 
@@ -140,12 +143,96 @@ class GPT2Small:
                 o = o * 0.0
             h = h + o
         h = F.layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
-        return h @ params["wte"].t()  # tied head: [B, T, vocab]
+        return LMHead(h, params["wte"])  # tied head, logits h @ wte.T left to lm_loss
 
 
-def lm_loss(logits, tokens):
-    """Next-token cross entropy."""
-    return F.cross_entropy(logits[:, :-1].reshape(-1, logits.shape[-1]).float(), tokens[:, 1:].reshape(-1))
+@dataclass
+class LMHead:
+    """Final hidden states [B, T, E] and the tied embedding [V, E].  The
+    [B, T, V] logits are never materialised whole: lm_loss fuses the head GEMM
+    with the cross-entropy chunk by chunk (logits() builds them for callers
+    that want them)."""
+    h: torch.Tensor
+    wte: torch.Tensor
+
+    def logits(self) -> torch.Tensor:
+        return self.h @ self.wte.t()
+
+
+class _LinearCrossEntropy(torch.autograd.Function):
+    """mean_i CE(h_i @ w.T, t_i) without the [n, V] logits in memory: the
+    forward keeps only each row's log-sum-exp, the backward recomputes a chunk
+    of logits at a time and feeds the two gradient GEMMs.  Under autocast
+    (bf16) the GEMMs write bf16 logit chunks and libsdp's k_ce_fwd / k_ce_bwd
+    make one fp32-accumulating pass over each (log-sum-exp; softmax - onehot,
+    scaled); other dtypes use torch ops in at least fp32."""
+
+    CHUNK = 2048
+
+    @staticmethod
+    def _cdt(h):
+        return torch.get_autocast_dtype("cuda") if torch.is_autocast_enabled("cuda") else h.dtype
+
+    @staticmethod
+    def forward(ctx, h, w, t):
+        cdt = _LinearCrossEntropy._cdt(h)
+        hc, wc = h.to(cdt), w.to(cdt)
+        t = t.contiguous()
+        n = h.shape[0]
+        acc = torch.float64 if cdt == torch.float64 else torch.float32
+        lse = torch.empty(n, dtype=acc, device=h.device)
+        rows = torch.empty(n, dtype=acc, device=h.device)
+        with torch.autocast("cuda", enabled=False):
+            for s in range(0, n, _LinearCrossEntropy.CHUNK):
+                e = min(n, s + _LinearCrossEntropy.CHUNK)
+                lg = hc[s:e] @ wc.t()
+                if cdt == torch.bfloat16:  # libsdp k_ce_fwd: one pass over the bf16 chunk
+                    N.call("sdp_ce_rows_fwd", ptr(lg), e - s, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
+                           ptr(rows[s:e]), stream_ptr(h.device))
+                else:
+                    lg = lg.to(acc)
+                    lse[s:e] = torch.logsumexp(lg, dim=1)
+                    rows[s:e] = lse[s:e] - lg.gather(1, t[s:e, None]).squeeze(1)
+        ctx.save_for_backward(h, w, t, lse)
+        ctx.cdt = cdt
+        return rows.sum() / n
+
+    @staticmethod
+    def backward(ctx, g):
+        h, w, t, lse = ctx.saved_tensors
+        cdt = ctx.cdt
+        hc, wc = h.to(cdt), w.to(cdt)
+        n = h.shape[0]
+        acc = lse.dtype
+        gh = torch.empty(h.shape, dtype=cdt, device=h.device)
+        gw = torch.zeros(w.shape, dtype=acc, device=w.device)
+        g32 = g.detach().to(torch.float32).reshape(1).contiguous()
+        with torch.autocast("cuda", enabled=False):
+            for s in range(0, n, _LinearCrossEntropy.CHUNK):
+                e = min(n, s + _LinearCrossEntropy.CHUNK)
+                lg = hc[s:e] @ wc.t()
+                if cdt == torch.bfloat16:  # libsdp k_ce_bwd: softmax - onehot, scaled, in one pass
+                    dl = torch.empty_like(lg)
+                    N.call("sdp_ce_rows_bwd", ptr(lg), e - s, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
+                           ptr(g32), C.c_float(1.0 / n), ptr(dl), stream_ptr(h.device))
+                else:
+                    p = torch.exp(lg.to(acc) - lse[s:e, None])
+                    p[torch.arange(e - s, device=h.device), t[s:e]] -= 1.0
+                    dl = (p * (g.to(acc) / n)).to(cdt)
+                del lg
+                gh[s:e] = dl @ wc
+                gw += (dl.t() @ hc[s:e]).to(acc)
+        return gh.to(h.dtype), gw.to(w.dtype), None
+
+
+def lm_loss(out, tokens):
+    """Next-token cross entropy over the tied LM head (fused, chunked), or over
+    given logits [B, T, V]."""
+    if isinstance(out, LMHead):
+        e = out.h.shape[-1]
+        return _LinearCrossEntropy.apply(out.h[:, :-1].reshape(-1, e), out.wte, tokens[:, 1:].reshape(-1))
+    acc = torch.promote_types(out.dtype, torch.float32)  # fp32, or fp64 for fp64 logits
+    return F.cross_entropy(out[:, :-1].reshape(-1, out.shape[-1]).to(acc), tokens[:, 1:].reshape(-1))
 
 
 def build_gpt2(dev, seed: int = 1) -> GlobalModel:

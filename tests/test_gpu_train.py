@@ -163,3 +163,24 @@ def test_graphed_step_equals_eager(cuda, strategy):
         assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
     finally:
         torch.backends.cudnn.deterministic = prev
+
+
+def test_fused_lm_head_cross_entropy_matches_unfused(cuda):
+    """train.lm_loss on the tied head (chunked, logits never whole) == the
+    unfused F.cross_entropy over materialised logits: float64 to 1e-12, and
+    under bf16 autocast to bf16 rounding."""
+    from paper_2507_09029_b200 import train
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(1)
+    tok = torch.randint(0, 50257, (3, 1500), generator=gen, device=cuda)  # 4497 rows: 3 chunks
+    for dtype, autocast, tol in ((torch.float64, False, 1e-12), (torch.float32, True, 2e-2)):
+        h = (torch.randn(3, 1500, 64, generator=gen, device=cuda) * 0.5).to(dtype).requires_grad_(True)
+        w = (torch.randn(50257, 64, generator=gen, device=cuda) * 0.05).to(dtype).requires_grad_(True)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=autocast):
+            fused = train.lm_loss(train.LMHead(h, w), tok)
+            plain = train.lm_loss(train.LMHead(h, w).logits(), tok)
+        gf = torch.autograd.grad(fused, (h, w))
+        gp = torch.autograd.grad(plain, (h, w))
+        assert abs(fused.item() - plain.item()) <= tol * abs(plain.item())
+        for a, b in zip(gf, gp):
+            assert torch.allclose(a.double(), b.double(), rtol=tol, atol=tol * b.abs().max().item())
