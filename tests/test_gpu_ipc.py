@@ -1,4 +1,4 @@
-"""The real N > 1 path across PROCESSES on one GPU: two ranks export their
+"""The real N > 1 path across PROCESSES on one GPU: the ranks export their
 replicas + signal pads with CUDA IPC, exchange handles over gloo, open each
 other's buffers and run k_owner_sync with the cross-rank flag barriers.
 
@@ -62,16 +62,18 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("strategy,layout", [("block", "ref"), ("neuron", "ref"), ("neuron", "sync")])
-def test_two_process_ipc_owner_sync(cuda, tmp_path, strategy, layout):
+@pytest.mark.parametrize("strategy,layout,world", [("block", "ref", 2), ("neuron", "ref", 2), ("neuron", "sync", 2),
+                                                   ("block", "ref", 4), ("neuron", "sync", 4)])
+def test_multi_process_ipc_owner_sync(cuda, tmp_path, strategy, layout, world):
+    """world = 4 is one worker per rank (N = G = 4), the real deployment shape."""
     import torch
     from oracle import oracle as O
     from paper_2507_09029_b200 import masking, zoo
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     port = _port()
     procs = []
-    for r in range(2):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy,
                    LAYOUT=layout)
         procs.append(subprocess.Popen([sys.executable, "-c", CHILD], env=env,
@@ -95,10 +97,10 @@ def test_two_process_ipc_owner_sync(cuda, tmp_path, strategy, layout):
         host.append((torch.randn(topo.total, generator=gen, device="cuda") * a.param_masks[w]).cpu().numpy())
     masks = a.param_masks.cpu().numpy()
     want = O.aggregate_f32_ordered(host, masks)
-    for r in range(2):
+    for r in range(world):
         z = np.load(tmp_path / f"rank{r}.npz")
         assert int(z["status"]) == 0, f"rank {r} status {int(z['status'])}"
-        for w in (0, 1) if r == 0 else (2, 3):
+        for w in [w for w in range(4) if w * world // 4 == r]:
             got = z[f"w{w}"]
             m = masks[w]
             assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32))
