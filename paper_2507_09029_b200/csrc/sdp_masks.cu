@@ -385,13 +385,50 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
   const int64_t n_steps = (total + kStepElems - 1) / kStepElems;
   const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  // per-worker held counts of this lane: 16-bit counters, four per register
-  uint64_t packed[16];
+  // per-worker held counts of this lane: 16-bit counters, four per register;
+  // MB mask bytes bound the workers (8 * MB), so only 2 * MB registers exist
+  // (a 16-register loop with runtime predicates cost ~70 issued instructions
+  // per element at N = 8)
+  constexpr int kGroups = 2 * MB;
+  uint64_t packed[kGroups];
 #pragma unroll
-  for (int g = 0; g < 16; ++g) packed[g] = 0;
+  for (int g = 0; g < kGroups; ++g) packed[g] = 0;
   ParamCursor cur;
   cur.pi = -1;
   for (int64_t k = warp0; k < n_steps; k += n_warps) {  // warp-uniform trip count
+    // Whole step inside one parameter with one owner set (block rules or no
+    // rule: the block strategy almost everywhere): constant fills, no
+    // per-element work.  The cursor is loaded from the step start, so it is
+    // warp-uniform here.
+    const int64_t jb = k * kStepElems;
+    if (cur.pi < 0 || jb < cur.lo || jb >= cur.hi)
+      cur.load(params, rules, unit_bits, full, find_param(params, n_params, jb));
+    if (cur.uniform && jb + kStepElems <= cur.hi && jb + kStepElems <= total && !(param_masks && (total & 1))) {
+      const uint64_t b = cur.bits;
+      const int c = __popcll(b);
+      const longlong2 cv = make_longlong2(c, c);
+      const double dv = static_cast<double>(c > 0 ? c : 1);
+      const double2 dvv = make_double2(dv, dv);
+      const longlong2 gv = make_longlong2(cur.rule_count, cur.rule_count);
+#pragma unroll
+      for (int it = 0; it < kStepElems / 64; ++it) {
+        const int64_t j = jb + it * 64 + 2 * lane;
+        if (owner_mask) st_mask_pair<M>(owner_mask + j, b, b);
+        if (coverage) *reinterpret_cast<longlong2*>(coverage + j) = cv;
+        if (divisor) *reinterpret_cast<double2*>(divisor + j) = dvv;
+        if (governors) *reinterpret_cast<longlong2*>(governors + j) = gv;
+        if (param_masks)
+          for (int w = 0; w < n_workers; ++w)
+            *reinterpret_cast<uint16_t*>(param_masks + static_cast<int64_t>(w) * total + j) =
+                static_cast<uint16_t>(((b >> w) & 1ull) * 0x0101u);
+      }
+      if (active_counts) {  // 2 * kStepElems / 64 elements of this lane, all with owner set b
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g)
+          if (4 * g < n_workers) packed[g] += spread4(b >> (4 * g)) * (2 * kStepElems / 64);
+      }
+      continue;
+    }
 #pragma unroll 1
     for (int it = 0; it < kStepElems / 64; ++it) {
       const int64_t j = k * kStepElems + it * 64 + 2 * lane;
@@ -440,7 +477,7 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
       }
       if (active_counts) {
 #pragma unroll
-        for (int g = 0; g < 16; ++g)
+        for (int g = 0; g < kGroups; ++g)
           if (4 * g < n_workers) packed[g] += spread4(b0 >> (4 * g)) + spread4(b1 >> (4 * g));
       }
     }
@@ -448,7 +485,7 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
   if (active_counts) {
     // held-parameter count per worker: warp-shuffle reduce, one atomic per warp
 #pragma unroll
-    for (int g = 0; g < 16; ++g) {
+    for (int g = 0; g < kGroups; ++g) {
       if (4 * g >= n_workers) break;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -599,7 +636,8 @@ int sdp_build_masks(const sdp_param_desc* params, int n_params, const sdp_rule_d
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * std::max(1, per_sm)));
   auto ac = reinterpret_cast<unsigned long long*>(active_counts);
   cudaStream_t s = as_stream(stream);
-  const int mb = owner_mask ? mask_bytes : 1;
+  // the template width also bounds the per-worker counters: never below N
+  const int mb = owner_mask ? mask_bytes : (n_workers <= 8 ? 1 : n_workers <= 16 ? 2 : n_workers <= 32 ? 4 : 8);
 #define SDP_BUILD(MB)                                                                         \
   k_build_masks<MB><<<grid, kBuildThreads, 0, s>>>(params, n_params, rules, unit_bits,        \
                                                    n_workers, total,                          \
