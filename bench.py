@@ -344,6 +344,8 @@ def run_ours(args):
     cpu = None
     train = None
     builder = None
+    if world > 1 and not args.no_train and args.workload == "resnet18":
+        train = run_train_multi(args, dev, rank, world, red_dev)
     if rank == 0 and world == 1:
         e2e = run_e2e(args, a, dev, total_bytes)
         if not args.no_train and args.workload == "resnet18":
@@ -482,6 +484,72 @@ def run_train(args, dev):
                       "dp": "full-replica DP comparator (P=N)"}
     out["note"] = ("peak memory = one worker's compact fp32 master + grad + momentum + bf16 copy + "
                    "activations of its fwd/bwd, i.e. what a GPU holding that worker needs (N = G)")
+    return out
+
+
+def run_train_multi(args, dev, rank: int, world: int, red_dev):
+    """Train samples/s/GPU at G > 1 GPUs (BASELINE metric part 2 at 2/4/8 GPUs):
+    one process per GPU, the N = 8 workers placed contiguously (N/G per rank),
+    train.PeerTrainer (local fwd/bwd, peer-mapped owner sync, local fused
+    Nesterov + bf16 cast).  CUDA events over the timed steps, max over ranks;
+    peak memory = the largest local worker's step (train.worker_memory), max
+    over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_09029_b200 import masking, train
+
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def rmax(x: float) -> float:
+        t = torch.tensor([float(x)], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    batch, n = 64, args.n_logical
+    out = {"workload": f"ResNet-18 CIFAR-shape, N={n} workers on {world} GPUs ({n // world} per GPU), "
+                       f"batch {batch}/worker, bf16 autocast, peer-mapped owner sync + local fused Nesterov/bf16",
+           "data": "synthetic", "timing": "CUDA events per rank, max over ranks"}
+    for tag, p, strategy in (("subnet", args.p, "block"), ("widthwise", args.p, "neuron"), ("dp", n, "block")):
+        model = train.build_resnet18(dev)
+        a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
+        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.02)
+        gen = torch.Generator(device=dev)
+        batches = {}
+        for w in tr.local:
+            gen.manual_seed(w)
+            batches[w] = (torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
+                          torch.randint(0, 10, (batch,), generator=gen, device=dev))
+        out[f"{tag}_loss_first"] = rmax(tr.step(batches).item())
+        tr.step(batches)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.train_steps):
+            loss = tr.step(batches)
+        e.record()
+        torch.cuda.synchronize()
+        tr.group.check()
+        ms = rmax(s.elapsed_time(e) / args.train_steps)
+        dist.barrier()
+        out[f"{tag}_ms_per_step"] = ms
+        out[f"{tag}_samples_per_s_per_gpu"] = n * batch / (ms / 1e3) / world
+        out[f"{tag}_loss_last"] = rmax(loss.item())
+        mem = max(train.worker_memory(model, a, w if p < n else None, batch, dev)["peak_bytes"]
+                  for w in (tr.local if p < n else tr.local[:1]))
+        out[f"{tag}_peak_mem_per_worker_bytes"] = int(rmax(mem))
+        tr.close()
+        del tr, model, a
+        torch.cuda.empty_cache()
+        dist.barrier()
+    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
+    out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_worker_bytes"]
+                                            / out["dp_peak_mem_per_worker_bytes"])
+    out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
     return out
 
 

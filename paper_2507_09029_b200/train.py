@@ -407,6 +407,88 @@ class SubnetTrainer:
         return torch.stack(losses).mean()
 
 
+class PeerTrainer:
+    """One process per GPU (torchrun): this rank trains its local workers
+    (contiguous placement, comm.rank_layout) on their own parameter copies.
+    A step is: every local worker's forward/backward writes its fp32 gradient
+    into its peer-mapped replica; ONE owner-sync launch per rank (the leader
+    of each tile reads every owner's gradient -- local or over NVLink -- in
+    ascending worker order and writes the mean into every owner's replica);
+    then each local worker applies SGD-Nesterov to its copy with the bf16
+    cast fused (sdp_nesterov_update).  Remote traffic is 4 B per remote owner
+    per element; updating remote theta / velocity copies from the leader
+    instead would cost 10 B.  Every owner applies the same update to the same
+    mean, so the owners' copies of an owned parameter stay bit-identical to
+    the co-resident trainer's canonical theta (engine.py:222-223).
+
+    Width-wise (neuron) assignments keep replicas and parameter copies in the
+    window-class-major sync layout (layout.SyncLayout) and train compact
+    subnetworks through layout.WorkerTransfer, like SubnetTrainer."""
+
+    def __init__(self, model: GlobalModel, assignment, rank: int, world: int, device, all_gather,
+                 lr: float = 0.1, momentum: float = 0.9, autocast: bool = True, loss_fn=None,
+                 timeout_cycles: int = 20_000_000_000):
+        from . import comm
+        self.model, self.assignment = model, assignment
+        self.lr, self.momentum, self.autocast = lr, momentum, autocast
+        self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
+        self.device = torch.device(device)
+        self.compact = assignment.strategy == "neuron"
+        self.slayout = None
+        theta0 = model.theta.to(self.device)
+        if self.compact:
+            from .layout import SyncLayout, WorkerTransfer
+            from .models import SubnetLayout
+            self.slayout = SyncLayout(assignment)
+            theta0 = self.slayout.to_sync(theta0)
+        self.group = comm.PeerGroup(assignment, rank, world, self.device, all_gather, shadows=False,
+                                    timeout_cycles=timeout_cycles,
+                                    owner_mask=None if self.slayout is None else self.slayout.owner_mask)
+        self.local = self.group.layout.local_workers
+        self.views = {w: assignment.worker_view(w) for w in self.local}
+        if self.compact:
+            self.subs = {w: SubnetLayout(assignment, w) for w in self.local}
+            self.transfers = {w: WorkerTransfer(self.slayout, self.subs[w]) for w in self.local}
+        self.theta = {w: theta0.clone() for w in self.local}
+        self.velocity = {w: torch.zeros_like(theta0) for w in self.local}
+        self.theta_bf16 = {w: theta0.to(torch.bfloat16) for w in self.local}
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def step(self, batches: dict) -> torch.Tensor:
+        """batches: {local worker: (x, y)}; returns the local workers' mean loss."""
+        topo = self.model.topology
+        losses = []
+        for w in self.local:
+            x, y = batches[w]
+            if self.compact:
+                sub = self.subs[w]
+                leaf = self.transfers[w].to_compact(self.theta[w]).requires_grad_(True)
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                    loss = self.loss_fn(self.model.arch.forward_compact(sub.views(leaf), x, sub), y)
+                (g,) = torch.autograd.grad(loss, leaf)
+                self.transfers[w].from_compact(g, self.group.replicas[w])
+            else:
+                leaf = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach().requires_grad_(True)
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                    loss = self.loss_fn(self.model.arch.forward(param_views(topo, leaf), x, self.views[w]), y)
+                (g,) = torch.autograd.grad(loss, leaf)
+                self.group.replicas[w].copy_(g)
+            losses.append(loss.detach())
+        self.group.launch()  # peer-mapped owner sync: replicas[w] <- mean on w's elements
+        for w in self.local:
+            N.call("sdp_nesterov_update", N.DTYPE_F32, self.theta[w].numel(), ptr(self.theta[w]),
+                   ptr(self.velocity[w]), ptr(self.group.replicas[w]), float(self.lr), float(self.momentum),
+                   ptr(self.theta_bf16[w]), ptr(self.status), stream_ptr(self.device))
+        return torch.stack(losses).mean()
+
+    def theta_of(self, w: int) -> torch.Tensor:
+        """Worker w's parameter copy in the reference's flat layout."""
+        return self.slayout.from_sync(self.theta[w]) if self.slayout else self.theta[w]
+
+    def close(self) -> None:
+        self.group.close()
+
+
 def build_resnet18(dev, seed: int = 1) -> GlobalModel:
     arch = ResNet18Cifar()
     topo = arch.topology

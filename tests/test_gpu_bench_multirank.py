@@ -25,7 +25,7 @@ def test_torchrun_two_ranks_same_device(cuda):
     env = dict(os.environ, SDP_BENCH_SAME_DEVICE="1", SDP_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "5", "--warmup", "3"]
+           "--gpus", "2", "--steps", "5", "--warmup", "3", "--train-steps", "2"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -33,3 +33,6 @@ def test_torchrun_two_ranks_same_device(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["gpu_launches"] == 5 and d["value"] > 0
     assert "nvlink_frac" in d["roofline"]
+    t = d["train"]  # PeerTrainer at world 2: C2 / C3 / DP samples/s and memory
+    assert t["subnet_samples_per_s_per_gpu"] > 0 and t["widthwise_samples_per_s_per_gpu"] > 0
+    assert t["subnet_peak_mem_per_worker_bytes"] < t["dp_peak_mem_per_worker_bytes"]

@@ -105,3 +105,87 @@ def test_multi_process_ipc_owner_sync(cuda, tmp_path, strategy, layout, world):
             m = masks[w]
             assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32))
             assert np.array_equal(got[~m], host[w][~m])
+
+
+TRAIN_CHILD = textwrap.dedent(r"""
+    import os, sys, numpy as np, torch, torch.distributed as dist
+    sys.path.insert(0, os.environ["REPO"])
+    from paper_2507_09029_b200 import masking, train
+    torch.backends.cudnn.deterministic = True
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+    dev = torch.device("cuda", 0)
+    model = train.build_resnet18(dev, seed=5)
+    a = masking.build_assignment(model.topology, os.environ["STRATEGY"], 4, 2, seed=1)
+    tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=False,
+                           timeout_cycles=10_000_000_000)
+    for step in range(2):
+        batches = {}
+        for w in tr.local:
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(100 * step + w)
+            batches[w] = (torch.randn(4, 3, 32, 32, generator=gen, device=dev),
+                          torch.randint(0, 10, (4,), generator=gen, device=dev))
+        tr.step(batches)
+        torch.cuda.synchronize()
+        dist.barrier()
+    tr.group.check()
+    np.savez(os.path.join(os.environ["OUT"], f"rank{rank}.npz"),
+             **{f"w{w}": tr.theta_of(w).cpu().numpy() for w in tr.local})
+    tr.close()
+    dist.destroy_process_group()
+""")
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy):
+    """train.PeerTrainer over 2 processes (CUDA-IPC replicas, cross-rank sync,
+    local Nesterov) leaves every worker's copy of its parameters bit-identical
+    to the co-resident trainer's canonical theta (fp32, deterministic cuDNN)."""
+    import torch
+    from paper_2507_09029_b200 import masking, train
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy)
+        procs.append(subprocess.Popen([sys.executable, "-c", TRAIN_CHILD], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=300)[0])
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            pytest.fail("trainer ranks did not finish in 300 s")
+    assert all(p.returncode == 0 for p in procs), "\n".join(outs)
+    prev = torch.backends.cudnn.deterministic
+    torch.backends.cudnn.deterministic = True
+    try:
+        model = train.build_resnet18(cuda, seed=5)
+        a = masking.build_assignment(model.topology, strategy, 4, 2, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=0.05, autocast=False, sync_layout=strategy == "neuron")
+        for step in range(2):
+            batches = []
+            for w in range(4):
+                gen = torch.Generator(device=cuda)
+                gen.manual_seed(100 * step + w)
+                batches.append((torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
+                                torch.randint(0, 10, (4,), generator=gen, device=cuda)))
+            tr.step(batches)
+        canon = tr.theta().cpu().numpy()
+    finally:
+        torch.backends.cudnn.deterministic = prev
+    masks = a.param_masks.cpu().numpy()
+    for r in range(2):
+        z = np.load(tmp_path / f"rank{r}.npz")
+        for w in (0, 1) if r == 0 else (2, 3):
+            got = z[f"w{w}"]
+            assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
