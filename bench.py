@@ -550,6 +550,41 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
     out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_worker_bytes"]
                                             / out["dp_peak_mem_per_worker_bytes"])
     out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
+    # configs[3] C4 at G GPUs: GPT-2 small, seq 1024, micro-batch 8 per worker
+    g4 = {"workload": f"GPT-2 small 124M, seq 1024, N={n} workers on {world} GPUs x micro-batch 8, "
+                      "bf16 autocast, flash SDPA, fused LM-head cross-entropy", "data": "synthetic tokens"}
+    for tag, p in (("subnet", args.p), ("dp", n)):
+        model = train.build_gpt2(dev)
+        a = masking.build_assignment(model.topology, "block", n, p, seed=1)
+        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=1e-4, loss_fn=train.lm_loss)
+        gen = torch.Generator(device=dev)
+        batches = {}
+        for w in tr.local:
+            gen.manual_seed(w)
+            t = torch.randint(0, 50257, (8, 1024), generator=gen, device=dev)
+            batches[w] = (t, t)
+        tr.step(batches)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(2, args.train_steps // 2)
+        s.record()
+        for _ in range(steps):
+            loss = tr.step(batches)
+        e.record()
+        torch.cuda.synchronize()
+        tr.group.check()
+        ms = rmax(s.elapsed_time(e) / steps)
+        dist.barrier()
+        g4[f"{tag}_ms_per_step"] = ms
+        g4[f"{tag}_tokens_per_s_per_gpu"] = n * 8 * 1024 / (ms / 1e3) / world
+        g4[f"{tag}_loss_last"] = rmax(loss.item())
+        tr.close()
+        del tr, model, a
+        torch.cuda.empty_cache()
+        dist.barrier()
+    g4["speedup_vs_dp_per_step"] = g4["dp_ms_per_step"] / g4["subnet_ms_per_step"]
+    out["c4_gpt2"] = g4
     return out
 
 

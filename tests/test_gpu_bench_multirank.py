@@ -36,3 +36,4 @@ def test_torchrun_two_ranks_same_device(cuda):
     t = d["train"]  # PeerTrainer at world 2: C2 / C3 / DP samples/s and memory
     assert t["subnet_samples_per_s_per_gpu"] > 0 and t["widthwise_samples_per_s_per_gpu"] > 0
     assert t["subnet_peak_mem_per_worker_bytes"] < t["dp_peak_mem_per_worker_bytes"]
+    assert t["c4_gpt2"]["subnet_tokens_per_s_per_gpu"] > 0 and t["c4_gpt2"]["dp_tokens_per_s_per_gpu"] > 0
