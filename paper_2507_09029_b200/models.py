@@ -70,6 +70,16 @@ def active_group_norm(x, groups: int, gamma, beta, active: torch.Tensor, eps: fl
     return _group_norm_by_membership(x, member, gamma, beta, eps)
 
 
+def group_norm(x, groups: int, gamma, beta, eps: float = 1e-5):
+    """F.group_norm; under bf16 autocast bf16 activations stay bf16 in and out
+    (the kernel keeps fp32 statistics) instead of autocast's fp32 upcast --
+    half of what every GroupNorm saves for backward, and no cast kernels."""
+    if x.dtype == torch.bfloat16 and torch.is_autocast_enabled("cuda"):
+        with torch.autocast("cuda", enabled=False):
+            return F.group_norm(x, groups, gamma.to(x.dtype), beta.to(x.dtype), eps)
+    return F.group_norm(x, groups, gamma, beta, eps)
+
+
 def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: float = 1e-5,
                       counts: tuple[int, ...] | None = None):
     """Compact channels, each tagged with its original norm group (F4: ragged).
@@ -80,11 +90,11 @@ def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: 
     unequal ones are a few contiguous F.group_norm(., 1) calls."""
     if counts is not None:
         if len(set(counts)) == 1:
-            return F.group_norm(x, len(counts), gamma, beta, eps)
+            return group_norm(x, len(counts), gamma, beta, eps)
         outs, pos = [], 0
         for c in counts:
             if c:
-                outs.append(F.group_norm(x[:, pos:pos + c], 1, gamma[pos:pos + c], beta[pos:pos + c], eps))
+                outs.append(group_norm(x[:, pos:pos + c], 1, gamma[pos:pos + c], beta[pos:pos + c], eps))
             pos += c
         return torch.cat(outs, dim=1)
     member = F.one_hot(group_of.to(torch.long), groups)

@@ -25,6 +25,7 @@ import torch.nn.functional as F
 from . import _native as N
 from . import engine, masking, zoo
 from ._device import ptr, stream_ptr
+from .models import group_norm
 from .topology import GlobalModel
 
 
@@ -48,7 +49,7 @@ class ResNet18Cifar:
         (ops.py:140-204: dead channels output exact zeros)."""
         flags = None if worker is None else worker.channel_active.get(layer_id)
         if flags is None or bool(np.all(flags)):
-            return F.group_norm(x, self.norm_groups, gamma, beta)
+            return group_norm(x, self.norm_groups, gamma, beta)
         from .models import active_group_norm
         act = torch.as_tensor(np.array(flags, dtype=bool), device=x.device)
         return active_group_norm(x, self.norm_groups, gamma, beta, act)
@@ -56,7 +57,7 @@ class ResNet18Cifar:
     def forward(self, params, x, worker=None, block_mode: str = "skip"):
         g = self.norm_groups
         h = F.conv2d(x, params["conv1.w"], padding=1)
-        h = F.relu(F.group_norm(h, g, params["gn1.gamma"], params["gn1.beta"]))
+        h = F.relu(group_norm(h, g, params["gn1.gamma"], params["gn1.beta"]))
         for bi, (p, stride, down) in enumerate(self.block_plan):
             live = True if worker is None else bool(worker.block_active[bi])
             if not live and block_mode == "skip":
@@ -67,7 +68,7 @@ class ResNet18Cifar:
             o = self._gn(o, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"], worker, f"{p}.conv2")
             if down:
                 sc = downsample(h, params[f"{p}.down.w"], stride)
-                sc = F.group_norm(sc, g, params[f"{p}.down_gn.gamma"], params[f"{p}.down_gn.beta"])
+                sc = group_norm(sc, g, params[f"{p}.down_gn.gamma"], params[f"{p}.down_gn.beta"])
             else:
                 sc = h
             if not live:
@@ -83,7 +84,7 @@ class ResNet18Cifar:
         from .models import ragged_group_norm
         g = self.norm_groups
         h = F.conv2d(x, cp["conv1.w"], padding=1)
-        h = F.relu(F.group_norm(h, g, cp["gn1.gamma"], cp["gn1.beta"]))
+        h = F.relu(group_norm(h, g, cp["gn1.gamma"], cp["gn1.beta"]))
         for p, stride, down in self.block_plan:
             if not sub.present(f"{p}.conv1.w"):
                 continue
@@ -99,7 +100,7 @@ class ResNet18Cifar:
                                   counts=sub.group_counts(f"{p}.conv2", planes, g))
             if down:
                 sc = downsample(h, cp[f"{p}.down.w"], stride)
-                sc = F.group_norm(sc, g, cp[f"{p}.down_gn.gamma"], cp[f"{p}.down_gn.beta"])
+                sc = group_norm(sc, g, cp[f"{p}.down_gn.gamma"], cp[f"{p}.down_gn.beta"])
             else:
                 sc = h
             h = F.relu(sc.index_add(1, a2, o.to(sc.dtype)))
