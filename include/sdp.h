@@ -108,9 +108,8 @@ typedef struct {
  *   groups (device):   n_groups descriptors, drawn in order from ONE generator.
  *   unit_bits (device, out): uint64 owner mask per unit; units outside every
  *                      group get all N bits (they are never masked).
- *   scratch (device):  >= max group size int32 (used only when a group of
- *                      more than 12288 units does not fit in shared memory;
- *                      may be NULL otherwise).
+ *   scratch (device):  >= 8 x n_units + 1 int32 (the parallel shuffle's
+ *                      arrays: step targets, slots, buckets, chains).
  * Errors: SDP_ERR_CONFIG unless 1 <= P <= N <= 64 and groups are non-empty. */
 int sdp_assign_units(const uint32_t* seed_words, int n_seed_words,
                      const sdp_group_desc* groups, int n_groups, int max_group,

@@ -156,7 +156,7 @@ __device__ __forceinline__ uint64_t pcg_output(u128 state) {  // XSL-RR
   return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
-constexpr int kAssignThreads = 256;
+constexpr int kAssignThreads = 1024;
 constexpr int kAssignWords = 8192;               // 32-bit words per refill (4096 raw draws)
 constexpr int kRawPerThread = kAssignWords / 2 / kAssignThreads;
 
@@ -179,25 +179,84 @@ __device__ void refill_words(uint32_t* words, u128* state, u128 inc) {
   __syncthreads();
 }
 
-// One CTA.  The PCG64 stream is generated cooperatively, kAssignWords 32-bit
-// draws at a time, into shared memory (affine jump-ahead per thread); thread 0
-// then runs the inherently sequential Fisher-Yates of each group
-// (Generator.shuffle, one generator across groups, masking.py:107-116) on
-// plain shared-memory reads -- the 128-bit LCG chain is off its critical path
-// (~80 ns per unit on B200, shared-memory latency bound; splitting draws and
-// swaps into two concurrent warps measured no faster) -- and the whole CTA
-// writes the group's window masks.
+// Block-wide exclusive scan of cnt[0..n) into start[0..n] (start[n] = total).
+__device__ void block_exclusive_scan(const int32_t* cnt, int32_t* start, int n, int32_t* s_warp) {
+  const int per = (n + kAssignThreads - 1) / kAssignThreads;
+  const int b = threadIdx.x * per, e = min(n, b + per);
+  int local = 0;
+  for (int k = b; k < e; ++k) local += cnt[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kAssignThreads / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kAssignThreads / 32) s_warp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  int run = (warp > 0 ? s_warp[warp - 1] : 0) + incl - local;
+  for (int k = b; k < e; ++k) {
+    start[k] = run;
+    run += cnt[k];
+  }
+  if (threadIdx.x == kAssignThreads - 1) start[n] = s_warp[kAssignThreads / 32 - 1];
+  __syncthreads();
+}
+
+// One CTA.  numpy's Generator.shuffle of arange(n) per group (one generator
+// across groups, masking.py:107-116) in two parallel phases:
+//  (A) per group, in stream order: the masked rejection draws j_i for
+//      i = n-1..1 (numpy random_interval) depend on the 32-bit word stream
+//      and i only.  Warp 0 takes 32 words at a time: with a_k accepted draws
+//      before lane k (a_k <= k), lane k is surely accepted when v_k <= i - k,
+//      surely rejected when v_k > i, and only the first lane in between is
+//      resolved exactly (ballot + popc); a batch is cut where the mask (set by
+//      i's bit length) would change.  Every step records its target as a
+//      global unit position: js[first + i] = first + j_i.
+//  (B) once, over all groups: the swaps a[i] <-> a[j_i] are evaluated without
+//      running them.  The content of position x right before step i is set
+//      by the most recent earlier step (the smallest step index > i) that
+//      targeted x, so with the steps bucketed by target (counting sort) each
+//      final a[i] is a short chain walk:
+//        a[i] = g(nxt(i)) if a step s > i has j_s = j_i (nxt = the smallest),
+//               else j_i;   a[0] = g(npos(0)), else 0;
+//        g(y) = g(npos(y)) if a step s > y has j_s = y (npos = the smallest),
+//               else y.
+// The PCG64 stream is generated cooperatively into shared memory (affine
+// jump-ahead per thread).  scratch: 8 x n_units int32 (device).
 __global__ void __launch_bounds__(kAssignThreads)
 k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups, int n_units,
-         int n_workers, int replication, uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch,
-         int perm_cap) {
+         int n_workers, int replication, uint64_t* __restrict__ unit_bits, int32_t* __restrict__ scratch) {
   extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* words = s_dyn;
-  int32_t* s_perm = reinterpret_cast<int32_t*>(s_dyn + kAssignWords);
   __shared__ u128 s_state, s_inc;
   __shared__ int s_p, s_i;
+  __shared__ int32_t s_warp[kAssignThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nu = n_units;
+  int32_t* js = scratch;              // step target (global position); -1 group first, -2 no group
+  int32_t* slot_of = scratch + nu;    // window slot of each position
+  int32_t* cnt = scratch + 2 * nu;    // bucket sizes, then fill cursors, then results
+  int32_t* start = scratch + 3 * nu;  // [nu + 1]
+  int32_t* bucket = scratch + 4 * nu + 1;
+  int32_t* nxt = scratch + 5 * nu + 1;
+  int32_t* npos = scratch + 6 * nu + 1;
+  int32_t* res = cnt;
   const uint64_t full = n_workers == 64 ? ~0ull : ((1ull << n_workers) - 1);
-  for (int u = threadIdx.x; u < n_units; u += blockDim.x) unit_bits[u] = full;
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    unit_bits[u] = full;
+    js[u] = -2;
+  }
   if (threadIdx.x == 0) {
     Pcg64 g;
     seed_pcg(g, seed.w, seed.n);
@@ -208,27 +267,78 @@ k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups
   __syncthreads();
   const u128 inc = s_inc;
   refill_words(words, &s_state, inc);
-  uint64_t slot = 0;
+  // ---- (A) draws, group by group in stream order ---------------------------
+  // the first kGroupStage group descriptors are staged in shared memory with
+  // one parallel load (not a dependent global round trip per group)
+  constexpr int kGroupStage = 512;
+  __shared__ int2 s_groups[kGroupStage];
+  for (int g = threadIdx.x; g < min(n_groups, kGroupStage); g += blockDim.x)
+    s_groups[g] = make_int2(groups[g].first_unit, groups[g].size);
+  __syncthreads();
+  int slot = 0;
   for (int gi = 0; gi < n_groups; ++gi) {
-    const int first = groups[gi].first_unit, size = groups[gi].size;
-    int32_t* a = size <= perm_cap ? s_perm : scratch;
-    __syncthreads();  // previous group's readers are done with a[]
-    for (int k = threadIdx.x; k < size; k += blockDim.x) a[k] = k;
-    if (threadIdx.x == 0) s_i = size - 1;
+    const int2 gd = gi < kGroupStage ? s_groups[gi] : make_int2(groups[gi].first_unit, groups[gi].size);
+    const int first = gd.x, n = gd.y;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) slot_of[first + k] = slot + k;
+    if (threadIdx.x == 0) {
+      js[first] = -1;
+      s_i = n - 1;
+    }
+    slot += n;
     __syncthreads();
     while (true) {
-      if (threadIdx.x == 0) {  // Generator.shuffle (Fisher-Yates), masked rejection draws
+      if (warp == 0) {
         int i = s_i, p = s_p;
         while (i > 0 && p < kAssignWords) {
-          const uint32_t v = words[p++] & (0xffffffffu >> __clz(i));
-          if (v > static_cast<uint32_t>(i)) continue;
-          const int32_t t = a[i];
-          a[i] = a[v];
-          a[v] = t;
-          --i;
+          const uint32_t m = 0xffffffffu >> __clz(i);
+          const int lo = static_cast<int>((m >> 1) + 1);  // smallest i with this mask
+          const int B = min(min(32, kAssignWords - p), i - lo + 1);
+          uint32_t v = 0;
+          int t = -1;
+          if (lane < B) {
+            v = words[p + lane] & m;
+            t = i - static_cast<int>(v);
+          }
+          // classify every lane against the bounds on a_k (accepted draws
+          // before lane k), then resolve the undecided lanes one by one from
+          // the lowest, re-classifying the rest with the tightened bounds
+          const uint32_t live = B >= 32 ? 0xffffffffu : ((1u << B) - 1u);
+          uint32_t acc = __ballot_sync(0xffffffffu, lane < B && t >= lane);       // sure accepts
+          uint32_t dec = acc | (__ballot_sync(0xffffffffu, t < 0) & live);      // decided lanes
+          int u = -1;  // lanes <= u are resolved exactly
+          while (dec != live) {
+            const uint32_t und = live & ~dec;
+            const int k = __ffs(und) - 1;            // lowest undecided lane: its a_k is exact
+            const uint32_t below = (1u << k) - 1u;
+            const int tk = __shfl_sync(0xffffffffu, t, k);
+            if (__popc(acc & below) <= tk) acc |= 1u << k;
+            u = k;
+            dec |= (1u << k) | below;
+            // lanes above k: a in [A, A + (lane - k - 1)], A = accepted up to k
+            const int A = __popc(acc & (below | (1u << k)));
+            const bool hi = lane > k && ((und >> lane) & 1u);
+            const uint32_t sa = __ballot_sync(0xffffffffu, hi && A + (lane - k - 1) <= t);
+            const uint32_t sr = __ballot_sync(0xffffffffu, hi && A > t);
+            acc |= sa;
+            dec |= sa | sr;
+          }
+          (void)u;
+          int consumed = B;
+          if (__popc(acc) >= i) {  // the group's last draw: stop right after it
+            uint32_t a2 = acc;
+            for (int q = 1; q < i; ++q) a2 &= a2 - 1;  // the i-th accepted lane is now lowest
+            const int last = __ffs(a2) - 1;
+            acc &= last >= 31 ? 0xffffffffu : ((1u << (last + 1)) - 1u);
+            consumed = last + 1;
+          }
+          if ((acc >> lane) & 1u) js[first + i - __popc(acc & ((1u << lane) - 1u))] = first + static_cast<int32_t>(v);
+          i -= __popc(acc);
+          p += consumed;
         }
-        s_i = i;
-        s_p = p;
+        if (lane == 0) {
+          s_i = i;
+          s_p = p;
+        }
       }
       __syncthreads();
       if (s_i == 0) break;
@@ -236,10 +346,55 @@ k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups
       if (threadIdx.x == 0) s_p = 0;
       __syncthreads();
     }
-    for (int k = threadIdx.x; k < size; k += blockDim.x)
-      unit_bits[first + a[k]] = window_bits(slot + k, n_workers, replication);
-    slot += size;
   }
+  // ---- (B) final positions, all groups at once -----------------------------
+  for (int k = threadIdx.x; k < nu; k += blockDim.x) cnt[k] = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < nu; q += blockDim.x)
+    if (js[q] >= 0) atomicAdd(&cnt[js[q]], 1);
+  __syncthreads();
+  block_exclusive_scan(cnt, start, nu, s_warp);
+  for (int k = threadIdx.x; k < nu; k += blockDim.x) cnt[k] = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < nu; q += blockDim.x) {
+    const int x = js[q];
+    if (x >= 0) bucket[start[x] + atomicAdd(&cnt[x], 1)] = q;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nu; k += blockDim.x) {
+    // npos(k): smallest step > k targeting k;  nxt(k): smallest step > k targeting j_k
+    int bp = 0x7fffffff;
+    for (int q = start[k]; q < start[k + 1]; ++q) {
+      const int c = bucket[q];
+      if (c > k && c < bp) bp = c;
+    }
+    npos[k] = bp == 0x7fffffff ? -1 : bp;
+    int bn = 0x7fffffff;
+    const int x = js[k];
+    if (x >= 0)
+      for (int q = start[x]; q < start[x + 1]; ++q) {
+        const int c = bucket[q];
+        if (c > k && c < bn) bn = c;
+      }
+    nxt[k] = bn == 0x7fffffff ? -1 : bn;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nu; k += blockDim.x) {
+    const int x = js[k];
+    if (x == -2) continue;  // not in any group
+    int y = x == -1 ? npos[k] : nxt[k];
+    int r;
+    if (y < 0) {
+      r = x == -1 ? k : x;
+    } else {
+      while (npos[y] >= 0) y = npos[y];
+      r = y;
+    }
+    res[k] = r;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nu; k += blockDim.x)
+    if (js[k] != -2) unit_bits[res[k]] = window_bits(slot_of[k], n_workers, replication);
 }
 
 __global__ void k_permutation(SeedWords seed, const int32_t* skip_sizes_dev, int n_skip, int n,
@@ -588,16 +743,11 @@ int sdp_assign_units(const uint32_t* seed_words, int n_seed_words, const sdp_gro
   if (!seed_words || n_seed_words < 1 || n_seed_words > 8)
     return set_error(SDP_ERR_CONFIG, "seed must be given as 1..8 uint32 words");
   if (!unit_bits || !groups) return set_error(SDP_ERR_USAGE, "null device pointer");
-  const int smem_cap = 12288;  // units per group held in shared memory
-  const int smem_elems = max_group <= smem_cap ? max_group : 0;
-  if (max_group > smem_cap && !scratch)
-    return set_error(SDP_ERR_USAGE, "group of %d units needs a scratch buffer", max_group);
-  const size_t smem = (kAssignWords + static_cast<size_t>(smem_elems)) * sizeof(uint32_t);
-  SDP_CUDA_CHECK(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+  if (!scratch) return set_error(SDP_ERR_USAGE, "k_assign needs an 8 x n_units int32 scratch buffer");
+  const size_t smem = kAssignWords * sizeof(uint32_t);
   k_assign<<<1, kAssignThreads, smem, as_stream(stream)>>>(
       make_seed(seed_words, n_seed_words), groups, n_groups, n_units, n_workers, replication,
-      unit_bits, scratch, smem_elems);
+      unit_bits, scratch);
   SDP_LAUNCH_CHECK();
   return SDP_OK;
 }

@@ -93,7 +93,7 @@ def _device_assign(groups: list[tuple[int, int]], n_units: int, n_workers: int,
     g_dev = upload_struct(garr, dev)
     unit_bits = torch.empty(max(n_units, 1), dtype=torch.int64, device=dev)
     max_group = int(garr[:, 1].max())
-    scratch = torch.empty(max_group, dtype=torch.int32, device=dev) if max_group > 12288 else None
+    scratch = torch.empty(8 * max(n_units, 1) + 1, dtype=torch.int32, device=dev)
     words, nw = N.seed_words(seed)
     N.call("sdp_assign_units", words, nw, ptr(g_dev), len(groups), max_group, n_units,
            n_workers, replication, ptr(unit_bits), ptr(scratch), stream_ptr(dev))
