@@ -1,9 +1,9 @@
 // Block-assignment and mask builder (masking.py:56-359) on the device.
 //
 //   k_assign       one CTA: SeedSequence -> PCG64 stream generated in parallel
-//                  (affine jump-ahead) -> per-group Fisher-Yates on one thread
-//                  (sequential by definition) -> cyclic windows
-//                  (masking.py:56-117); bit-exact with numpy default_rng.
+//                  (affine jump-ahead) -> Fisher-Yates as warp-speculative
+//                  rejection draws + chain-walk final positions -> cyclic
+//                  windows (masking.py:56-117); bit-exact with numpy.
 //   k_build_masks  HBM-bound expansion: every element ANDs the owner sets of
 //                  the units that govern it (masking.py:131-149, 160-169) and
 //                  emits owner mask / [N,d] bool / coverage / divisor /
