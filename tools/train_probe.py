@@ -1,6 +1,6 @@
 """Where a co-resident training step's time goes (GPU kernel time vs wall).
 
-    python tools/train_probe.py
+    python tools/train_probe.py [--graphed] [subnet|widthwise|dp ...]
 """
 import sys
 import time
@@ -17,7 +17,10 @@ gen.manual_seed(0)
 n, batch = 8, 64
 batches = [(torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
             torch.randint(0, 10, (batch,), generator=gen, device=dev)) for _ in range(n)]
+which = [a for a in sys.argv[1:] if not a.startswith("--")] or ["subnet", "widthwise", "dp"]
 for tag, p, strategy in (("subnet", 4, "block"), ("widthwise", 4, "neuron"), ("dp", 8, "block")):
+    if tag not in which:
+        continue
     model = train.build_resnet18(dev)
     a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
     tr = train.SubnetTrainer(model, a, lr=0.02, sync_layout=(strategy == "neuron"),
@@ -38,7 +41,7 @@ for tag, p, strategy in (("subnet", 4, "block"), ("widthwise", 4, "neuron"), ("d
     kern = sum(e.device_time_total for e in ev) / 1e3
     print(f"{tag}: wall {wall * 1e3:.1f} ms/step, host enqueue {t_enq / 5 * 1e3:.1f} ms/step, "
           f"GPU kernel time {kern:.1f} ms/step, kernels {len(ev)}")
-    top = prof.key_averages().table(sort_by="cuda_time_total", row_limit=12)
-    print(top)
+    top = prof.key_averages().table(sort_by="cuda_time_total", row_limit=25)
+    print("\n".join(ln[:60] + ln[100:200] for ln in top.splitlines()))
     del tr, model
     torch.cuda.empty_cache()
