@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import sys
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -396,8 +397,13 @@ class _PinnedResults:
     def __init__(self, cap: int = 4):
         self.cap = cap
         self.bufs: dict = {}
+        self.lock = threading.Lock()
 
     def get(self, d: int, dt: torch.dtype) -> tuple[np.ndarray, torch.Tensor]:
+        with self.lock:  # concurrent callers never receive the same free buffer
+            return self._get(d, dt)
+
+    def _get(self, d: int, dt: torch.dtype) -> tuple[np.ndarray, torch.Tensor]:
         lst = self.bufs.setdefault((d, dt), [])
         if not lst:  # double-buffer from the start: `out = aggregate(...)` loops hold one
             t = torch.empty(d, dtype=dt, pin_memory=True)
