@@ -339,6 +339,9 @@ def run_ours(args):
         roofline["nvlink_peak_GBps"] = 770.0
         roofline["nvlink_frac"] = roofline["nvlink_achieved_GBps"] / 770.0
         roofline["nvlink_peak_source"] = "B200_PROFILING.md measured peer copy per direction (900 nominal)"
+        probe = meta.get("roofline", {}).get("p2p_copy_GBps_measured")
+        if probe:  # this run's own ring peer-copy probe (all ranks at once)
+            roofline["nvlink_frac_of_run_probe"] = roofline["nvlink_achieved_GBps"] / probe
 
     e2e = None
     cpu = None

@@ -363,6 +363,11 @@ int sdp_ipc_close(void* ptr);
 /* Enable direct peer access from the current device to `peer` (idempotent). */
 int sdp_enable_peer(int peer);
 
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream`: the peer
+ * copy probe bench.py runs at start-up for the measured NVLink peak (SURVEY
+ * §8d), with dst a peer-mapped (sdp_ipc_import) address. */
+int sdp_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,6 +126,7 @@ SIGNATURES = {
     "sdp_ipc_import": (C.c_int, [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_void_p)]),
     "sdp_ipc_close": (C.c_int, [VP]),
     "sdp_enable_peer": (C.c_int, [I32]),
+    "sdp_copy_async": (C.c_int, [VP, VP, C.c_size_t, VP]),
 }
 
 _lock = threading.Lock()

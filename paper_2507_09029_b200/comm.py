@@ -190,6 +190,7 @@ def bench_setup(assignment, rank: int, world: int, device):
                 N.call("sdp_enable_peer", peer)
             except Exception:
                 pass  # IPC mappings enable peer access lazily
+    p2p = p2p_copy_probe(rank, world, device, all_gather)
     g = PeerGroup(assignment, rank, world, device, all_gather)
     pm = assignment.param_masks
     gen = torch.Generator(device=device)
@@ -202,8 +203,41 @@ def bench_setup(assignment, rank: int, world: int, device):
     nvl = _nvlink_bytes(g.plan, g.layout)
     meta = {"tiles": g.plan.n_tiles, "grid": g.grid, "tiles_per_cta": g.plan.tiles_per_cta,
             "roofline": {"nvlink_bytes_per_launch": nvl,
-                         "nvlink_note": "bytes this rank moves over NVLink per launch (peer reads + peer writes)"}}
+                         "nvlink_note": "bytes this rank moves over NVLink per launch (peer reads + peer writes)",
+                         "p2p_copy_GBps_measured": p2p}}
     return g.launch, own * 4, own * 10, meta
+
+
+def p2p_copy_probe(rank: int, world: int, device, all_gather, mib: int = 512, reps: int = 5) -> float:
+    """Measured peer-copy bandwidth per direction: every rank
+    copies `mib` MiB into its ring neighbour's CUDA-IPC-mapped buffer at the
+    same time (copy engine, cudaMemcpyDefault); GB/s of this rank, CUDA events."""
+    import torch.distributed as dist
+    n = mib << 18  # float32 elements
+    dst = torch.empty(n, dtype=torch.float32, device=device)
+    src = torch.ones(n, dtype=torch.float32, device=device)
+    tables = exchange_handles({"probe": ipc_export(dst)}, all_gather)
+    peer = (rank + 1) % world
+    h, off = tables[peer]["probe"]
+    ptr_ = dst.data_ptr() if peer == rank else ipc_import(h, off)
+    s = torch.cuda.current_stream(device)
+    N.call("sdp_copy_async", C.c_void_p(ptr_), C.c_void_p(src.data_ptr()), C.c_size_t(n * 4),
+           C.c_void_p(s.cuda_stream))
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        N.call("sdp_copy_async", C.c_void_p(ptr_), C.c_void_p(src.data_ptr()), C.c_size_t(n * 4),
+               C.c_void_p(s.cuda_stream))
+    e1.record(s)
+    torch.cuda.synchronize(device)
+    gbps = n * 4 * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    dist.barrier()
+    if peer != rank:
+        N.call("sdp_ipc_close", C.c_void_p(ptr_))
+    del dst, src
+    return gbps
 
 
 def _nvlink_bytes(plan: SyncPlan, layout: RankLayout) -> int:

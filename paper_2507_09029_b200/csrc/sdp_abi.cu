@@ -118,6 +118,13 @@ int sdp_ipc_close(void* ptr) {
   return SDP_OK;
 }
 
+int sdp_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (!bytes) return SDP_OK;
+  if (!dst || !src) return sdp::set_error(SDP_ERR_USAGE, "null pointer");
+  SDP_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, sdp::as_stream(stream)));
+  return SDP_OK;
+}
+
 int sdp_enable_peer(int peer) {
   int dev = 0, count = 0;
   SDP_CUDA_CHECK(cudaGetDevice(&dev));

@@ -32,7 +32,7 @@ def test_torchrun_two_ranks_same_device(cuda):
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["gpu_launches"] == 5 and d["value"] > 0
-    assert "nvlink_frac" in d["roofline"]
+    assert "nvlink_frac" in d["roofline"] and d["roofline"]["p2p_copy_GBps_measured"] > 0
     t = d["train"]  # PeerTrainer at world 2: C2 / C3 / DP samples/s and memory
     assert t["subnet_samples_per_s_per_gpu"] > 0 and t["widthwise_samples_per_s_per_gpu"] > 0
     assert t["subnet_peak_mem_per_worker_bytes"] < t["dp_peak_mem_per_worker_bytes"]
