@@ -308,6 +308,26 @@ int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
                void* out, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Channels-last GroupNorm (+ReLU) over contiguous ragged channel groups      */
+/* (the active-channel GroupNorm of compact subnetworks, ops.py:140-204)      */
+/* ------------------------------------------------------------------------ */
+
+/* x, y: bf16 [batch, hw, channels] (channels_last); group g = channels
+ * [group_starts[g], group_starts[g+1]) (device int32 [groups + 1]); gamma,
+ * beta fp32 [channels]; mean / rstd fp32 [batch * groups] (out).
+ * y = relu?((x - mean) * rstd * gamma + beta), statistics in fp32. */
+int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, const int32_t* group_starts,
+                       int groups, int max_group_channels, const float* gamma, const float* beta, float eps,
+                       int relu, void* y_bf16, float* mean, float* rstd, void* stream);
+
+/* Backward of sdp_group_norm_fwd: dx (bf16, same layout); dgamma / dbeta fp32
+ * [channels] are ACCUMULATED (zero them first). */
+int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
+                       int channels, const int32_t* group_starts, int groups, int max_group_channels,
+                       const float* gamma, const float* mean, const float* rstd, int relu, void* dx_bf16,
+                       float* dgamma, float* dbeta, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Fused LM-head cross-entropy rows (C4 training step, train.lm_loss)        */
 /* ------------------------------------------------------------------------ */
 

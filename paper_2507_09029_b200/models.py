@@ -70,18 +70,80 @@ def active_group_norm(x, groups: int, gamma, beta, active: torch.Tensor, eps: fl
     return _group_norm_by_membership(x, member, gamma, beta, eps)
 
 
-def group_norm(x, groups: int, gamma, beta, eps: float = 1e-5):
-    """F.group_norm; under bf16 autocast bf16 activations stay bf16 in and out
-    (the kernel keeps fp32 statistics) instead of autocast's fp32 upcast --
-    half of what every GroupNorm saves for backward, and no cast kernels."""
+_STARTS: dict = {}
+
+
+def _group_starts(starts: tuple[int, ...], dev) -> torch.Tensor:
+    key = (starts, dev)
+    if key not in _STARTS:
+        _STARTS[key] = torch.tensor(starts, dtype=torch.int32, device=dev)
+    return _STARTS[key]
+
+
+class _GroupNormCL(torch.autograd.Function):
+    """libsdp k_gn_fwd / k_gn_bwd: GroupNorm (+ReLU) on channels-last bf16
+    activations over contiguous, possibly ragged channel groups; fp32
+    statistics and affine parameters, fp32 dgamma / dbeta."""
+
+    @staticmethod
+    def forward(ctx, x, gamma, beta, starts, eps, relu):
+        b, c, h, w = x.shape
+        x = x.contiguous(memory_format=torch.channels_last)
+        sd = _group_starts(starts, x.device)
+        groups = len(starts) - 1
+        max_cg = max(starts[k + 1] - starts[k] for k in range(groups))
+        g32, b32 = gamma.float().contiguous(), beta.float().contiguous()
+        y = torch.empty_like(x, memory_format=torch.channels_last)
+        mean = torch.empty(b * groups, dtype=torch.float32, device=x.device)
+        rstd = torch.empty_like(mean)
+        N.call("sdp_group_norm_fwd", ptr(x), b, h * w, c, ptr(sd), groups, max_cg, ptr(g32), ptr(b32),
+               C.c_float(eps), int(relu), ptr(y), ptr(mean), ptr(rstd), stream_ptr(x.device))
+        ctx.save_for_backward(x, y, g32, mean, rstd)
+        ctx.meta = (starts, relu, gamma.dtype, beta.dtype, max_cg)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, y, g32, mean, rstd = ctx.saved_tensors
+        starts, relu, gdt, bdt, max_cg = ctx.meta
+        b, c, h, w = x.shape
+        dy = dy.contiguous(memory_format=torch.channels_last)
+        dx = torch.empty_like(x, memory_format=torch.channels_last)
+        dg = torch.zeros(c, dtype=torch.float32, device=x.device)
+        db = torch.zeros_like(dg)
+        N.call("sdp_group_norm_bwd", ptr(x), ptr(y), ptr(dy), b, h * w, c, ptr(_group_starts(starts, x.device)),
+               len(starts) - 1, max_cg, ptr(g32), ptr(mean), ptr(rstd), int(relu), ptr(dx), ptr(dg), ptr(db),
+               stream_ptr(x.device))
+        return dx, dg.to(gdt), db.to(bdt), None, None, None
+
+
+def _channels_last_bf16(x) -> bool:
+    return (x.is_cuda and x.dtype == torch.bfloat16 and x.dim() == 4 and torch.is_autocast_enabled("cuda")
+            and x.is_contiguous(memory_format=torch.channels_last))
+
+
+def group_norm(x, groups: int, gamma, beta, eps: float = 1e-5, relu: bool = False,
+               starts: tuple[int, ...] | None = None):
+    """GroupNorm (+ReLU).  Channels-last bf16 activations under autocast (the
+    training path) run libsdp's kernels over contiguous channel groups
+    (`starts`: ragged group boundaries, default equal groups); otherwise
+    F.group_norm, where bf16 activations under autocast stay bf16 in and out
+    (fp32 statistics inside) instead of autocast's fp32 upcast."""
+    if _channels_last_bf16(x):
+        if starts is None:
+            c = x.shape[1]
+            starts = tuple(range(0, c + 1, c // groups))
+        return _GroupNormCL.apply(x, gamma, beta, starts, eps, relu)
     if x.dtype == torch.bfloat16 and torch.is_autocast_enabled("cuda"):
         with torch.autocast("cuda", enabled=False):
-            return F.group_norm(x, groups, gamma.to(x.dtype), beta.to(x.dtype), eps)
-    return F.group_norm(x, groups, gamma, beta, eps)
+            out = F.group_norm(x, groups, gamma.to(x.dtype), beta.to(x.dtype), eps)
+    else:
+        out = F.group_norm(x, groups, gamma, beta, eps)
+    return F.relu(out) if relu else out
 
 
 def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: float = 1e-5,
-                      counts: tuple[int, ...] | None = None):
+                      counts: tuple[int, ...] | None = None, relu: bool = False):
     """Compact channels, each tagged with its original norm group (F4: ragged).
 
     Compact channels keep ascending original order, so each group's live
@@ -89,16 +151,25 @@ def ragged_group_norm(x, group_of: torch.Tensor, groups: int, gamma, beta, eps: 
     (the grouped assignment's balanced case) are one fused F.group_norm and
     unequal ones are a few contiguous F.group_norm(., 1) calls."""
     if counts is not None:
-        if len(set(counts)) == 1:
-            return group_norm(x, len(counts), gamma, beta, eps)
-        outs, pos = [], 0
-        for c in counts:
-            if c:
-                outs.append(group_norm(x[:, pos:pos + c], 1, gamma[pos:pos + c], beta[pos:pos + c], eps))
-            pos += c
-        return torch.cat(outs, dim=1)
+        if _channels_last_bf16(x):  # one kernel over the ragged groups
+            starts = [0]
+            for c in counts:
+                if c:
+                    starts.append(starts[-1] + c)
+            return group_norm(x, len(starts) - 1, gamma, beta, eps, relu=relu, starts=tuple(starts))
+        elif len(set(counts)) == 1:
+            out = group_norm(x, len(counts), gamma, beta, eps)
+        else:
+            outs, pos = [], 0
+            for c in counts:
+                if c:
+                    outs.append(group_norm(x[:, pos:pos + c], 1, gamma[pos:pos + c], beta[pos:pos + c], eps))
+                pos += c
+            out = torch.cat(outs, dim=1)
+        return F.relu(out) if relu else out
     member = F.one_hot(group_of.to(torch.long), groups)
-    return _group_norm_by_membership(x, member, gamma, beta, eps)
+    out = _group_norm_by_membership(x, member, gamma, beta, eps)
+    return F.relu(out) if relu else out
 
 
 # ---------------------------------------------------------------------------

@@ -29,6 +29,32 @@ from .models import group_norm
 from .topology import GlobalModel
 
 
+class _ChannelScatterAdd(torch.autograd.Function):
+    """out = sc with o added into channels idx (the compact block output
+    written back into the residual stream), keeping channels-last layouts in
+    both directions (torch's index_add / index_select backward would hand
+    the next GroupNorm an NCHW gradient and force a transpose copy)."""
+
+    @staticmethod
+    def forward(ctx, sc, idx, o):
+        ctx.save_for_backward(idx)
+        fmt = torch.channels_last if sc.is_contiguous(memory_format=torch.channels_last) else torch.contiguous_format
+        ctx.fmt = fmt
+        return sc.clone(memory_format=fmt).index_add_(1, idx, o)
+
+    @staticmethod
+    def backward(ctx, g):
+        (idx,) = ctx.saved_tensors
+        b, _, h, w = g.shape
+        go = torch.empty((b, idx.numel(), h, w), dtype=g.dtype, device=g.device, memory_format=ctx.fmt)
+        torch.index_select(g, 1, idx, out=go)
+        return g, None, go
+
+
+def _channel_scatter_add(sc, idx, o):
+    return _ChannelScatterAdd.apply(sc, idx, o)
+
+
 class ResNet18Cifar:
     def __init__(self, classes: int = 10, norm_groups: int = 2):
         self.classes, self.norm_groups = classes, norm_groups
@@ -44,26 +70,33 @@ class ResNet18Cifar:
     def build_topology(self):
         return self.topology
 
-    def _gn(self, x, gamma, beta, worker, layer_id):
-        """GroupNorm; over the worker's live channels only when some are dead
-        (ops.py:140-204: dead channels output exact zeros)."""
+    def _gn(self, x, gamma, beta, worker, layer_id, relu=False):
+        """GroupNorm (+ReLU); over the worker's live channels only when some
+        are dead (ops.py:140-204: dead channels output exact zeros)."""
         flags = None if worker is None else worker.channel_active.get(layer_id)
         if flags is None or bool(np.all(flags)):
-            return group_norm(x, self.norm_groups, gamma, beta)
+            return group_norm(x, self.norm_groups, gamma, beta, relu=relu)
         from .models import active_group_norm
         act = torch.as_tensor(np.array(flags, dtype=bool), device=x.device)
-        return active_group_norm(x, self.norm_groups, gamma, beta, act)
+        out = active_group_norm(x, self.norm_groups, gamma, beta, act)
+        return F.relu(out) if relu else out
+
+    @staticmethod
+    def _layout(x):
+        """Training (bf16 autocast) keeps activations channels-last end to end:
+        cuDNN's NHWC kernels and libsdp's GroupNorm need no layout transposes."""
+        return x.contiguous(memory_format=torch.channels_last) if torch.is_autocast_enabled("cuda") else x
 
     def forward(self, params, x, worker=None, block_mode: str = "skip"):
         g = self.norm_groups
-        h = F.conv2d(x, params["conv1.w"], padding=1)
-        h = F.relu(group_norm(h, g, params["gn1.gamma"], params["gn1.beta"]))
+        h = F.conv2d(self._layout(x), params["conv1.w"], padding=1)
+        h = group_norm(h, g, params["gn1.gamma"], params["gn1.beta"], relu=True)
         for bi, (p, stride, down) in enumerate(self.block_plan):
             live = True if worker is None else bool(worker.block_active[bi])
             if not live and block_mode == "skip":
                 continue  # a dropped block is the identity and is never executed
             o = F.conv2d(h, params[f"{p}.conv1.w"], stride=stride, padding=1)
-            o = F.relu(self._gn(o, params[f"{p}.gn1.gamma"], params[f"{p}.gn1.beta"], worker, f"{p}.conv1"))
+            o = self._gn(o, params[f"{p}.gn1.gamma"], params[f"{p}.gn1.beta"], worker, f"{p}.conv1", relu=True)
             o = F.conv2d(o, params[f"{p}.conv2.w"], padding=1)
             o = self._gn(o, params[f"{p}.gn2.gamma"], params[f"{p}.gn2.beta"], worker, f"{p}.conv2")
             if down:
@@ -83,8 +116,8 @@ class ResNet18Cifar:
         block output is scattered back into the residual stream's channels."""
         from .models import ragged_group_norm
         g = self.norm_groups
-        h = F.conv2d(x, cp["conv1.w"], padding=1)
-        h = F.relu(group_norm(h, g, cp["gn1.gamma"], cp["gn1.beta"]))
+        h = F.conv2d(self._layout(x), cp["conv1.w"], padding=1)
+        h = group_norm(h, g, cp["gn1.gamma"], cp["gn1.beta"], relu=True)
         for p, stride, down in self.block_plan:
             if not sub.present(f"{p}.conv1.w"):
                 continue
@@ -93,8 +126,8 @@ class ResNet18Cifar:
             a1 = sub.channels(f"{p}.conv1", planes)
             a2 = sub.channels(f"{p}.conv2", planes)
             o = F.conv2d(h, cp[f"{p}.conv1.w"], stride=stride, padding=1)
-            o = F.relu(ragged_group_norm(o, a1 // gsize, g, cp[f"{p}.gn1.gamma"], cp[f"{p}.gn1.beta"],
-                                         counts=sub.group_counts(f"{p}.conv1", planes, g)))
+            o = ragged_group_norm(o, a1 // gsize, g, cp[f"{p}.gn1.gamma"], cp[f"{p}.gn1.beta"],
+                                  counts=sub.group_counts(f"{p}.conv1", planes, g), relu=True)
             o = F.conv2d(o, cp[f"{p}.conv2.w"], padding=1)
             o = ragged_group_norm(o, a2 // gsize, g, cp[f"{p}.gn2.gamma"], cp[f"{p}.gn2.beta"],
                                   counts=sub.group_counts(f"{p}.conv2", planes, g))
@@ -103,7 +136,7 @@ class ResNet18Cifar:
                 sc = group_norm(sc, g, cp[f"{p}.down_gn.gamma"], cp[f"{p}.down_gn.beta"])
             else:
                 sc = h
-            h = F.relu(sc.index_add(1, a2, o.to(sc.dtype)))
+            h = F.relu(_channel_scatter_add(sc, a2, o.to(sc.dtype)))
         return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 

@@ -212,3 +212,40 @@ def test_gather_scatter_all_paths_full_size(cuda, strategy, dtype):
         assert torch.equal(full, torch.where(mask, theta, torch.zeros((), dtype=dtype, device=cuda)))
         acc = sub.scatter(comp, base.clone(), accumulate=True)
         assert torch.equal(acc, torch.where(mask, base + theta, base))
+
+
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("counts", [(32, 32), (29, 35), (7, 1, 24)])
+def test_channels_last_group_norm_matches_torch(cuda, relu, counts):
+    """libsdp's channels-last GroupNorm (+ReLU) over ragged contiguous groups
+    == per-group F.group_norm in fp32 on the same bf16 input, forward and
+    backward, to bf16 rounding."""
+    import torch.nn.functional as F
+    from paper_2507_09029_b200 import models
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(sum(counts) + relu)
+    c = sum(counts)
+    x = (torch.randn(8, c, 12, 12, generator=gen, device=cuda) * 2 + 0.5).to(torch.bfloat16)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    gamma = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
+    beta = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
+    dy = torch.randn(8, c, 12, 12, generator=gen, device=cuda).to(torch.bfloat16)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        y = models.ragged_group_norm(x, None, len(counts), gamma, beta, counts=counts, relu=relu)
+    assert y.is_contiguous(memory_format=torch.channels_last)
+    gx, gg, gb = torch.autograd.grad(y, (x, gamma, beta), dy)
+    # reference: fp32 per-group F.group_norm on the same values
+    xr = x.detach().float().requires_grad_(True)
+    gr, br = gamma.detach().clone().requires_grad_(True), beta.detach().clone().requires_grad_(True)
+    outs, pos = [], 0
+    for k in counts:
+        outs.append(F.group_norm(xr[:, pos:pos + k], 1, gr[pos:pos + k], br[pos:pos + k]))
+        pos += k
+    yr = torch.cat(outs, dim=1)
+    if relu:
+        yr = F.relu(yr)
+    rx, rg, rb = torch.autograd.grad(yr, (xr, gr, br), dy.float())
+    assert torch.allclose(y.float(), yr, rtol=1e-2, atol=2e-2)
+    assert torch.allclose(gx.float(), rx, rtol=2e-2, atol=2e-2 * rx.abs().max().item())
+    assert torch.allclose(gg, rg, rtol=1e-2, atol=1e-2 * rg.abs().max().item())
+    assert torch.allclose(gb, rb, rtol=1e-2, atol=1e-2 * rb.abs().max().item())

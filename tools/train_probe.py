@@ -43,5 +43,9 @@ for tag, p, strategy in (("subnet", 4, "block"), ("widthwise", 4, "neuron"), ("d
           f"GPU kernel time {kern:.1f} ms/step, kernels {len(ev)}")
     top = prof.key_averages().table(sort_by="cuda_time_total", row_limit=25)
     print("\n".join(ln[:60] + ln[100:200] for ln in top.splitlines()))
+    if "--names" in sys.argv:
+        ka = sorted(prof.key_averages(), key=lambda k: -k.device_time_total)[:12]
+        for k in ka:
+            print(f"{k.device_time_total / 1e3:8.3f} ms {k.count:5d}  {k.key[:300]}")
     del tr, model
     torch.cuda.empty_cache()
