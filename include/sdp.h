@@ -312,10 +312,15 @@ int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
 /* (the active-channel GroupNorm of compact subnetworks, ops.py:140-204)      */
 /* ------------------------------------------------------------------------ */
 
+#define SDP_GN_RELU 0x1             /* y = relu(groupnorm(x)) */
+#define SDP_GN_GROUPS_ALIGNED8 0x2  /* every group start is a multiple of 8: 16-B vectors */
+
 /* x, y: bf16 [batch, hw, channels] (channels_last); group g = channels
  * [group_starts[g], group_starts[g+1]) (device int32 [groups + 1]); gamma,
  * beta fp32 [channels]; mean / rstd fp32 [batch * groups] (out).
- * y = relu?((x - mean) * rstd * gamma + beta), statistics in fp32. */
+ * y = relu?((x - mean) * rstd * gamma + beta), statistics in fp32.
+ * flags: SDP_GN_RELU | SDP_GN_GROUPS_ALIGNED8 (the caller's promise about
+ * group_starts; the library checks channels and pointer alignment). */
 int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, const int32_t* group_starts,
                        int groups, int max_group_channels, const float* gamma, const float* beta, float eps,
                        int relu, void* y_bf16, float* mean, float* rstd, void* stream);

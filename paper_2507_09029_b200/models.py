@@ -96,23 +96,24 @@ class _GroupNormCL(torch.autograd.Function):
         y = torch.empty_like(x, memory_format=torch.channels_last)
         mean = torch.empty(b * groups, dtype=torch.float32, device=x.device)
         rstd = torch.empty_like(mean)
+        flags = (1 if relu else 0) | (2 if all(v % 8 == 0 for v in starts) else 0)  # SDP_GN_*
         N.call("sdp_group_norm_fwd", ptr(x), b, h * w, c, ptr(sd), groups, max_cg, ptr(g32), ptr(b32),
-               C.c_float(eps), int(relu), ptr(y), ptr(mean), ptr(rstd), stream_ptr(x.device))
+               C.c_float(eps), flags, ptr(y), ptr(mean), ptr(rstd), stream_ptr(x.device))
         ctx.save_for_backward(x, y, g32, mean, rstd)
-        ctx.meta = (starts, relu, gamma.dtype, beta.dtype, max_cg)
+        ctx.meta = (starts, flags, gamma.dtype, beta.dtype, max_cg)
         return y
 
     @staticmethod
     def backward(ctx, dy):
         x, y, g32, mean, rstd = ctx.saved_tensors
-        starts, relu, gdt, bdt, max_cg = ctx.meta
+        starts, flags, gdt, bdt, max_cg = ctx.meta
         b, c, h, w = x.shape
         dy = dy.contiguous(memory_format=torch.channels_last)
         dx = torch.empty_like(x, memory_format=torch.channels_last)
         dg = torch.zeros(c, dtype=torch.float32, device=x.device)
         db = torch.zeros_like(dg)
         N.call("sdp_group_norm_bwd", ptr(x), ptr(y), ptr(dy), b, h * w, c, ptr(_group_starts(starts, x.device)),
-               len(starts) - 1, max_cg, ptr(g32), ptr(mean), ptr(rstd), int(relu), ptr(dx), ptr(dg), ptr(db),
+               len(starts) - 1, max_cg, ptr(g32), ptr(mean), ptr(rstd), flags, ptr(dx), ptr(dg), ptr(db),
                stream_ptr(x.device))
         return dx, dg.to(gdt), db.to(bdt), None, None, None
 
