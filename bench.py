@@ -62,6 +62,9 @@ def workload(name: str):
         return zoo.resnet18_cifar_topology(), "resnet18-cifar (configs[1], C2)"
     if name == "gpt2":
         return zoo.gpt2_small_topology(), "gpt2-small 124M (configs[3], C4)"
+    if name == "c1":  # the reference's own CPU-runnable case; use --n-logical 4 --p 2
+        return (zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32)),
+                "mini-ResNet 26ch x 8 blocks (configs[0], C1)")
     if name.startswith("sweep:"):
         mib = int(name.split(":")[1])
         return zoo.sweep_topology(mib * (1 << 20) // 4), f"sweep {mib} MiB fp32 (configs[4], C5)"
