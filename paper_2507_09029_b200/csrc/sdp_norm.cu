@@ -52,21 +52,52 @@ __device__ __forceinline__ void block_sum2(float& a, float& b) {
   __syncthreads();
 }
 
-// A cluster of kGnCluster CTAs per (sample, group), each over a contiguous
+// A cluster of up to kGnCluster CTAs per (sample, group), each over a contiguous
 // range of pixels of the group's slab; the group statistics are reduced
 // across the cluster through distributed shared memory.  Element e of a CTA's
 // range -> (pixel, channel): e = pixel * cg + k.
 constexpr int kGnCluster = 8;
 
-__device__ __forceinline__ float cluster_sum(cg::cluster_group& cl, float* s_part, float v) {
-  // v: this CTA's block-reduced partial (valid in every thread)
-  if (threadIdx.x == 0) *s_part = v;
+// CTAs per (sample, group): enough that each has >= 2048 elements of work,
+// a power of two <= kGnCluster (small late-layer slabs: fewer CTAs, fewer
+// cluster barriers)
+static int gn_parts(int hw, int max_cg) {
+  const int64_t slab = static_cast<int64_t>(hw) * max_cg;
+  int parts = 1;
+  while (parts < kGnCluster && slab / (2 * parts) >= 2048) parts *= 2;
+  return parts;
+}
+
+template <typename Kernel, typename... Args>
+static cudaError_t launch_clustered(Kernel k, unsigned grid, int parts, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGnThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = parts;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+__device__ __forceinline__ void cluster_sum2(cg::cluster_group& cl, float2* s_part, float& a, float& b) {
+  // a, b: this CTA's block-reduced partials (valid in every thread)
+  if (threadIdx.x == 0) *s_part = make_float2(a, b);
   cl.sync();
-  float t = 0.f;
-#pragma unroll
-  for (int r = 0; r < kGnCluster; ++r) t += *cl.map_shared_rank(s_part, r);
+  float ta = 0.f, tb = 0.f;
+  const int nb = static_cast<int>(cl.num_blocks());
+  for (int r = 0; r < nb; ++r) {
+    const float2 v = *cl.map_shared_rank(s_part, r);
+    ta += v.x;
+    tb += v.y;
+  }
   cl.sync();  // every CTA has read every partial before any is overwritten
-  return t;
+  a = ta;
+  b = tb;
 }
 
 // 8 channels per 16-B vector when the group's channel range and the row
@@ -103,13 +134,14 @@ struct GnSlab {
   int64_t base;  // element (p0, c0) of sample b
 };
 
-__device__ __forceinline__ GnSlab gn_slab(int bg, int part, int hw, int c, const int32_t* gs, int groups) {
+__device__ __forceinline__ GnSlab gn_slab(int bg, int part, int parts, int hw, int c, const int32_t* gs,
+                                          int groups) {
   GnSlab t;
   t.b = bg / groups;
   t.g = bg % groups;
   t.c0 = gs[t.g];
   t.cg = gs[t.g + 1] - t.c0;
-  const int per = (hw + kGnCluster - 1) / kGnCluster;
+  const int per = (hw + parts - 1) / parts;
   t.p0 = min(hw, part * per);
   t.p1 = min(hw, t.p0 + per);
   t.base = (static_cast<int64_t>(t.b) * hw + t.p0) * c + t.c0;
@@ -117,47 +149,44 @@ __device__ __forceinline__ GnSlab gn_slab(int bg, int part, int hw, int c, const
 }
 
 template <bool RELU, bool VEC>
-__global__ void __cluster_dims__(kGnCluster, 1, 1) __launch_bounds__(kGnThreads, 4)
+__global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __restrict__ gs, int groups,
          const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
          __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ float s_part;
-  const int bg = blockIdx.x / kGnCluster, part = static_cast<int>(cl.block_rank());
-  const GnSlab t = gn_slab(bg, part, hw, c, gs, groups);
+  __shared__ float2 s_part;
+  const int parts = static_cast<int>(cl.num_blocks());
+  const int bg = blockIdx.x / parts, part = static_cast<int>(cl.block_rank());
+  const GnSlab t = gn_slab(bg, part, parts, hw, c, gs, groups);
   const float n_all = static_cast<float>(hw) * t.cg;
   constexpr bool vec = VEC;  // host-checked: every group start, C and the pointers 8-aligned
   const int cv = vec ? t.cg / 8 : t.cg;                // vectors (or channels) per pixel
   const int nv = (t.p1 - t.p0) * cv;
-  // two passes (the second hits L1/L2): mean, then the centred sum of squares
-  float s0 = 0.f, unused = 0.f;
+  // one pass: sums of (x - K) and (x - K)^2 around the group's first element
+  // K (every CTA reads the same K), so the variance does not cancel
+  const float K = __bfloat162float(x[static_cast<int64_t>(t.b) * hw * c + t.c0]);
+  float s0 = 0.f, sq = 0.f;
   for (int q = threadIdx.x; q < nv; q += kGnThreads) {
     const int pix = q / cv, kv = q - pix * cv;
     if (vec) {
       const Bf8 r = ld8(x + t.base + static_cast<int64_t>(pix) * c + kv * 8);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s0 += r.v[k];
+      for (int k = 0; k < 8; ++k) {
+        const float d = r.v[k] - K;
+        s0 += d;
+        sq += d * d;
+      }
     } else {
-      s0 += __bfloat162float(x[t.base + static_cast<int64_t>(pix) * c + kv]);
-    }
-  }
-  block_sum2<kGnThreads>(s0, unused);
-  const float mean = cluster_sum(cl, &s_part, s0) / n_all;
-  float sq = 0.f;
-  unused = 0.f;
-  for (int q = threadIdx.x; q < nv; q += kGnThreads) {
-    const int pix = q / cv, kv = q - pix * cv;
-    if (vec) {
-      const Bf8 r = ld8(x + t.base + static_cast<int64_t>(pix) * c + kv * 8);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sq += (r.v[k] - mean) * (r.v[k] - mean);
-    } else {
-      const float d = __bfloat162float(x[t.base + static_cast<int64_t>(pix) * c + kv]) - mean;
+      const float d = __bfloat162float(x[t.base + static_cast<int64_t>(pix) * c + kv]) - K;
+      s0 += d;
       sq += d * d;
     }
   }
-  block_sum2<kGnThreads>(sq, unused);
-  const float rstd = rsqrtf(cluster_sum(cl, &s_part, sq) / n_all + eps);
+  block_sum2<kGnThreads>(s0, sq);
+  cluster_sum2(cl, &s_part, s0, sq);
+  const float md = s0 / n_all;
+  const float mean = K + md;
+  const float rstd = rsqrtf(fmaxf(sq / n_all - md * md, 0.f) + eps);
   if (part == 0 && threadIdx.x == 0) {
     mean_out[bg] = mean;
     rstd_out[bg] = rstd;
@@ -184,16 +213,17 @@ k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __re
 }
 
 template <bool RELU, bool VEC>
-__global__ void __cluster_dims__(kGnCluster, 1, 1) __launch_bounds__(kGnThreads, 4)
+__global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
          const __nv_bfloat16* __restrict__ dy, int hw, int c, const int32_t* __restrict__ gs, int groups,
          const float* __restrict__ gamma, const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
          __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ float s_dg[kGnMaxC], s_db[kGnMaxC];
-  __shared__ float s_part;
-  const int bg = blockIdx.x / kGnCluster, part = static_cast<int>(cl.block_rank());
-  const GnSlab t = gn_slab(bg, part, hw, c, gs, groups);
+  __shared__ float2 s_part;
+  const int parts = static_cast<int>(cl.num_blocks());
+  const int bg = blockIdx.x / parts, part = static_cast<int>(cl.block_rank());
+  const GnSlab t = gn_slab(bg, part, parts, hw, c, gs, groups);
   const float mean = mean_in[bg], rstd = rstd_in[bg];
   constexpr bool vec = VEC;  // host-checked: every group start, C and the pointers 8-aligned
   const int cv = vec ? t.cg / 8 : t.cg;
@@ -262,8 +292,9 @@ k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ 
   }
   block_sum2<kGnThreads>(s1, s2);
   const float inv_n = 1.f / (static_cast<float>(hw) * t.cg);
-  s1 = cluster_sum(cl, &s_part, s1) * inv_n;
-  s2 = cluster_sum(cl, &s_part, s2) * inv_n;
+  cluster_sum2(cl, &s_part, s1, s2);
+  s1 *= inv_n;
+  s2 *= inv_n;
   for (int q = threadIdx.x; q < nv; q += kGnThreads) {
     const int pix = q / cv, kv = q - pix * cv;
     const int64_t i = t.base + static_cast<int64_t>(pix) * c + (vec ? kv * 8 : kv);
@@ -311,14 +342,16 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
   if (max_group_channels > kGnMaxC) return set_error(SDP_ERR_USAGE, "a group of more than %d channels", kGnMaxC);
   if (batch == 0) return SDP_OK;
-  const unsigned grid = static_cast<unsigned>(batch) * groups * kGnCluster;
+  const int parts = gn_parts(hw, max_group_channels);
+  const unsigned grid = static_cast<unsigned>(batch) * groups * parts;
   cudaStream_t s = as_stream(stream);
   auto xb = static_cast<const __nv_bfloat16*>(x_bf16);
   auto yb = static_cast<__nv_bfloat16*>(y_bf16);
   const bool vec = (flags & SDP_GN_GROUPS_ALIGNED8) && (channels % 8) == 0 &&
                    ((reinterpret_cast<uintptr_t>(x_bf16) | reinterpret_cast<uintptr_t>(y_bf16)) & 15) == 0;
-#define SDP_GN_FWD(R, V) \
-  k_gn_fwd<R, V><<<grid, kGnThreads, 0, s>>>(xb, hw, channels, group_starts, groups, gamma, beta, eps, yb, mean, rstd)
+#define SDP_GN_FWD(R, V)                                                                                \
+  SDP_CUDA_CHECK(launch_clustered(k_gn_fwd<R, V>, grid, parts, s, xb, hw, channels, group_starts, groups, \
+                                  gamma, beta, eps, yb, mean, rstd))
   if (relu) {
     if (vec) SDP_GN_FWD(true, true); else SDP_GN_FWD(true, false);
   } else {
@@ -337,21 +370,22 @@ int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
   if (max_group_channels > kGnMaxC) return set_error(SDP_ERR_USAGE, "a group of more than %d channels", kGnMaxC);
   if (batch == 0) return SDP_OK;
-  const unsigned grid = static_cast<unsigned>(batch) * groups * kGnCluster;
+  const int parts = gn_parts(hw, max_group_channels);
+  const unsigned grid = static_cast<unsigned>(batch) * groups * parts;
   cudaStream_t s = as_stream(stream);
   auto xb = static_cast<const __nv_bfloat16*>(x_bf16);
   auto yb = static_cast<const __nv_bfloat16*>(y_bf16);
   auto db = static_cast<const __nv_bfloat16*>(dy_bf16);
   auto dxb = static_cast<__nv_bfloat16*>(dx_bf16);
-  // Measured on B200 (ResNet-18 step): the 16-B vector path speeds the
-  // forward up (3.1 -> 2.2 ms per DP step) but slows this kernel down (3.8 ->
-  // 4.5 ms: 8x fewer work items per CTA leave most threads idle on the small
-  // late-layer slabs), so the backward keeps one channel per element.
+  // Measured on B200 (ResNet-18 DP step): the 16-B vector path speeds the
+  // forward up but slows this kernel down (3.2 -> 3.9 ms per step: 8x fewer
+  // work items per CTA idle most threads on the late-layer slabs), so the
+  // backward keeps one channel per element.
   const bool vec = false;
   (void)flags;
-#define SDP_GN_BWD(R, V)                                                                                  \
-  k_gn_bwd<R, V><<<grid, kGnThreads, 0, s>>>(xb, yb, db, hw, channels, group_starts, groups, gamma, mean, rstd, \
-                                            dxb, dgamma, dbeta)
+#define SDP_GN_BWD(R, V)                                                                                 \
+  SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<R, V>, grid, parts, s, xb, yb, db, hw, channels, group_starts,  \
+                                  groups, gamma, mean, rstd, dxb, dgamma, dbeta))
   if (relu) {
     if (vec) SDP_GN_BWD(true, true); else SDP_GN_BWD(true, false);
   } else {
