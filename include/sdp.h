@@ -314,6 +314,7 @@ int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
 
 #define SDP_GN_RELU 0x1             /* y = relu(groupnorm(x)) */
 #define SDP_GN_GROUPS_ALIGNED8 0x2  /* every group start is a multiple of 8: 16-B vectors */
+#define SDP_GN_AFFINE_BF16 0x4      /* gamma / beta are bf16 (else fp32) */
 
 /* x, y: bf16 [batch, hw, channels] (channels_last); group g = channels
  * [group_starts[g], group_starts[g+1]) (device int32 [groups + 1]); gamma,
@@ -322,14 +323,14 @@ int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total,
  * flags: SDP_GN_RELU | SDP_GN_GROUPS_ALIGNED8 (the caller's promise about
  * group_starts; the library checks channels and pointer alignment). */
 int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, const int32_t* group_starts,
-                       int groups, int max_group_channels, const float* gamma, const float* beta, float eps,
-                       int relu, void* y_bf16, float* mean, float* rstd, void* stream);
+                       int groups, int max_group_channels, const void* gamma, const void* beta, float eps,
+                       int flags, void* y_bf16, float* mean, float* rstd, void* stream);
 
 /* Backward of sdp_group_norm_fwd: dx (bf16, same layout); dgamma / dbeta fp32
  * [channels] are ACCUMULATED (zero them first). */
 int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
                        int channels, const int32_t* group_starts, int groups, int max_group_channels,
-                       const float* gamma, const float* mean, const float* rstd, int relu, void* dx_bf16,
+                       const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
                        float* dgamma, float* dbeta, void* stream);
 
 /* ------------------------------------------------------------------------ */

@@ -129,6 +129,15 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float* v) {
   *reinterpret_cast<uint4*>(p) = u;
 }
 
+// gamma / beta in fp32 or bf16 (the parameter's own dtype: no cast kernels)
+struct Affine {
+  const void* p;
+  bool bf16;
+  __device__ __forceinline__ float operator[](int i) const {
+    return bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]) : static_cast<const float*>(p)[i];
+  }
+};
+
 struct GnSlab {
   int b, g, c0, cg, p0, p1;
   int64_t base;  // element (p0, c0) of sample b
@@ -151,7 +160,7 @@ __device__ __forceinline__ GnSlab gn_slab(int bg, int part, int parts, int hw, i
 template <bool RELU, bool VEC>
 __global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __restrict__ gs, int groups,
-         const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+         const Affine gamma, const Affine beta, float eps,
          __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ float2 s_part;
@@ -216,7 +225,7 @@ template <bool RELU, bool VEC>
 __global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
          const __nv_bfloat16* __restrict__ dy, int hw, int c, const int32_t* __restrict__ gs, int groups,
-         const float* __restrict__ gamma, const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+         const Affine gamma, const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
          __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ float s_dg[kGnMaxC], s_db[kGnMaxC];
@@ -336,9 +345,10 @@ using namespace sdp;
 extern "C" {
 
 int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, const int32_t* group_starts,
-                       int groups, int max_group_channels, const float* gamma, const float* beta, float eps,
+                       int groups, int max_group_channels, const void* gamma, const void* beta, float eps,
                        int flags, void* y_bf16, float* mean, float* rstd, void* stream) {
   const bool relu = flags & SDP_GN_RELU;
+  const Affine ga{gamma, (flags & SDP_GN_AFFINE_BF16) != 0}, be{beta, (flags & SDP_GN_AFFINE_BF16) != 0};
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
   if (max_group_channels > kGnMaxC) return set_error(SDP_ERR_USAGE, "a group of more than %d channels", kGnMaxC);
   if (batch == 0) return SDP_OK;
@@ -351,7 +361,7 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
                    ((reinterpret_cast<uintptr_t>(x_bf16) | reinterpret_cast<uintptr_t>(y_bf16)) & 15) == 0;
 #define SDP_GN_FWD(R, V)                                                                                \
   SDP_CUDA_CHECK(launch_clustered(k_gn_fwd<R, V>, grid, parts, s, xb, hw, channels, group_starts, groups, \
-                                  gamma, beta, eps, yb, mean, rstd))
+                                  ga, be, eps, yb, mean, rstd))
   if (relu) {
     if (vec) SDP_GN_FWD(true, true); else SDP_GN_FWD(true, false);
   } else {
@@ -364,9 +374,10 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
 
 int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
                        int channels, const int32_t* group_starts, int groups, int max_group_channels,
-                       const float* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
+                       const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
                        float* dgamma, float* dbeta, void* stream) {
   const bool relu = flags & SDP_GN_RELU;
+  const Affine ga{gamma, (flags & SDP_GN_AFFINE_BF16) != 0};
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
   if (max_group_channels > kGnMaxC) return set_error(SDP_ERR_USAGE, "a group of more than %d channels", kGnMaxC);
   if (batch == 0) return SDP_OK;
@@ -382,10 +393,9 @@ int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf
   // work items per CTA idle most threads on the late-layer slabs), so the
   // backward keeps one channel per element.
   const bool vec = false;
-  (void)flags;
 #define SDP_GN_BWD(R, V)                                                                                 \
   SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<R, V>, grid, parts, s, xb, yb, db, hw, channels, group_starts,  \
-                                  groups, gamma, mean, rstd, dxb, dgamma, dbeta))
+                                  groups, ga, mean, rstd, dxb, dgamma, dbeta))
   if (relu) {
     if (vec) SDP_GN_BWD(true, true); else SDP_GN_BWD(true, false);
   } else {

@@ -92,30 +92,38 @@ class _GroupNormCL(torch.autograd.Function):
         sd = _group_starts(starts, x.device)
         groups = len(starts) - 1
         max_cg = max(starts[k + 1] - starts[k] for k in range(groups))
-        g32, b32 = gamma.float().contiguous(), beta.float().contiguous()
+        if beta.dtype != gamma.dtype:
+            beta = beta.to(gamma.dtype)
+        gamma, beta = gamma.contiguous(), beta.contiguous()
+        # SDP_GN_RELU | SDP_GN_GROUPS_ALIGNED8 | SDP_GN_AFFINE_BF16
+        flags = ((1 if relu else 0) | (2 if all(v % 8 == 0 for v in starts) else 0)
+                 | (4 if gamma.dtype == torch.bfloat16 else 0))
+        if gamma.dtype not in (torch.float32, torch.bfloat16):
+            gamma, beta = gamma.float(), beta.float()
+            flags &= ~4
         y = torch.empty_like(x, memory_format=torch.channels_last)
         mean = torch.empty(b * groups, dtype=torch.float32, device=x.device)
         rstd = torch.empty_like(mean)
-        flags = (1 if relu else 0) | (2 if all(v % 8 == 0 for v in starts) else 0)  # SDP_GN_*
-        N.call("sdp_group_norm_fwd", ptr(x), b, h * w, c, ptr(sd), groups, max_cg, ptr(g32), ptr(b32),
+        N.call("sdp_group_norm_fwd", ptr(x), b, h * w, c, ptr(sd), groups, max_cg, ptr(gamma), ptr(beta),
                C.c_float(eps), flags, ptr(y), ptr(mean), ptr(rstd), stream_ptr(x.device))
-        ctx.save_for_backward(x, y, g32, mean, rstd)
-        ctx.meta = (starts, flags, gamma.dtype, beta.dtype, max_cg)
+        ctx.save_for_backward(x, y, gamma, mean, rstd)
+        ctx.meta = (starts, flags, max_cg)
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x, y, g32, mean, rstd = ctx.saved_tensors
-        starts, flags, gdt, bdt, max_cg = ctx.meta
+        x, y, gamma, mean, rstd = ctx.saved_tensors
+        starts, flags, max_cg = ctx.meta
         b, c, h, w = x.shape
         dy = dy.contiguous(memory_format=torch.channels_last)
         dx = torch.empty_like(x, memory_format=torch.channels_last)
-        dg = torch.zeros(c, dtype=torch.float32, device=x.device)
-        db = torch.zeros_like(dg)
+        dgb = torch.zeros(2 * c, dtype=torch.float32, device=x.device)  # dgamma | dbeta, one fill
         N.call("sdp_group_norm_bwd", ptr(x), ptr(y), ptr(dy), b, h * w, c, ptr(_group_starts(starts, x.device)),
-               len(starts) - 1, max_cg, ptr(g32), ptr(mean), ptr(rstd), flags, ptr(dx), ptr(dg), ptr(db),
-               stream_ptr(x.device))
-        return dx, dg.to(gdt), db.to(bdt), None, None, None
+               len(starts) - 1, max_cg, ptr(gamma), ptr(mean), ptr(rstd), flags, ptr(dx), ptr(dgb[:c]),
+               ptr(dgb[c:]), stream_ptr(x.device))
+        if gamma.dtype != torch.float32:
+            dgb = dgb.to(gamma.dtype)  # one cast for both
+        return dx, dgb[:c], dgb[c:], None, None, None
 
 
 def _channels_last_bf16(x) -> bool:

@@ -355,6 +355,28 @@ class SubnetTrainer:
         self.plan = self.slayout.plan() if self.slayout else assignment.sync_plan()
         self._prep = None
 
+    def _live_params(self, w: int) -> list:
+        """Parameters worker w's subnetwork uses (block strategy: not in a
+        dropped block; masking.py:160-169)."""
+        if not hasattr(self, "_live"):
+            self._live = {}
+        if w not in self._live:
+            topo = self.model.topology
+            dead = set()
+            view = self.views[w]
+            for b in topo.blocks:
+                if b.maskable and not bool(view.block_active[b.index]):
+                    dead.update(b.param_names)
+            self._live[w] = [p.name for p in topo.params if p.name not in dead]
+        return self._live[w]
+
+    def _grad_slots(self, w: int) -> dict:
+        if not hasattr(self, "_slots"):
+            self._slots = {}
+        if w not in self._slots:
+            self._slots[w] = param_views(self.model.topology, self.grads[w])
+        return self._slots[w]
+
     def theta(self) -> torch.Tensor:
         """theta in the reference's flat layout."""
         return self.slayout.from_sync(self.model.theta) if self.slayout else self.model.theta
@@ -427,15 +449,20 @@ class SubnetTrainer:
                     sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
                 losses.append(loss.detach())
                 continue
-            # the worker trains on the bf16 weights the previous sync wrote
-            leaf = (self.theta_bf16 if self.autocast else self.model.theta).detach().requires_grad_(True)
-            params = param_views(topo, leaf)
+            # the worker trains on the bf16 weights the previous sync wrote;
+            # every parameter is a leaf view and its gradient lands directly
+            # in its slot of the fp32 replica (one multi-tensor copy, no [d]
+            # concatenation); parameters of dropped blocks keep their zeros
+            src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
+            params = {k: v.requires_grad_(True) for k, v in param_views(topo, src).items()}
             with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                 logits = self.model.arch.forward(params, x, self.views[w])
                 loss = self.loss_fn(logits, y)
             del logits
-            (g,) = torch.autograd.grad(loss, leaf)
-            self.grads[w].copy_(g)  # fp32 gradient replica of worker w
+            names = self._live_params(w)
+            gs = torch.autograd.grad(loss, [params[k] for k in names])
+            slots = self._grad_slots(w)
+            torch._foreach_copy_([slots[k] for k in names], list(gs))
             losses.append(loss.detach())
         self._sync()
         return torch.stack(losses).mean()

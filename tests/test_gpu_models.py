@@ -214,9 +214,10 @@ def test_gather_scatter_all_paths_full_size(cuda, strategy, dtype):
         assert torch.equal(acc, torch.where(mask, base + theta, base))
 
 
+@pytest.mark.parametrize("affine", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("relu", [False, True])
 @pytest.mark.parametrize("counts", [(32, 32), (29, 35), (7, 1, 24)])
-def test_channels_last_group_norm_matches_torch(cuda, relu, counts):
+def test_channels_last_group_norm_matches_torch(cuda, relu, counts, affine):
     """libsdp's channels-last GroupNorm (+ReLU) over ragged contiguous groups
     == per-group F.group_norm in fp32 on the same bf16 input, forward and
     backward, to bf16 rounding."""
@@ -227,8 +228,8 @@ def test_channels_last_group_norm_matches_torch(cuda, relu, counts):
     c = sum(counts)
     x = (torch.randn(8, c, 12, 12, generator=gen, device=cuda) * 2 + 0.5).to(torch.bfloat16)
     x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
-    gamma = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
-    beta = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
+    gamma = torch.randn(c, generator=gen, device=cuda).to(affine).requires_grad_(True)
+    beta = torch.randn(c, generator=gen, device=cuda).to(affine).requires_grad_(True)
     dy = torch.randn(8, c, 12, 12, generator=gen, device=cuda).to(torch.bfloat16)
     with torch.autocast("cuda", dtype=torch.bfloat16):
         y = models.ragged_group_norm(x, None, len(counts), gamma, beta, counts=counts, relu=relu)
@@ -236,7 +237,7 @@ def test_channels_last_group_norm_matches_torch(cuda, relu, counts):
     gx, gg, gb = torch.autograd.grad(y, (x, gamma, beta), dy)
     # reference: fp32 per-group F.group_norm on the same values
     xr = x.detach().float().requires_grad_(True)
-    gr, br = gamma.detach().clone().requires_grad_(True), beta.detach().clone().requires_grad_(True)
+    gr, br = gamma.detach().float().requires_grad_(True), beta.detach().float().requires_grad_(True)
     outs, pos = [], 0
     for k in counts:
         outs.append(F.group_norm(xr[:, pos:pos + k], 1, gr[pos:pos + k], br[pos:pos + k]))
@@ -247,5 +248,6 @@ def test_channels_last_group_norm_matches_torch(cuda, relu, counts):
     rx, rg, rb = torch.autograd.grad(yr, (xr, gr, br), dy.float())
     assert torch.allclose(y.float(), yr, rtol=1e-2, atol=2e-2)
     assert torch.allclose(gx.float(), rx, rtol=2e-2, atol=2e-2 * rx.abs().max().item())
-    assert torch.allclose(gg, rg, rtol=1e-2, atol=1e-2 * rg.abs().max().item())
-    assert torch.allclose(gb, rb, rtol=1e-2, atol=1e-2 * rb.abs().max().item())
+    assert gg.dtype == affine and gb.dtype == affine
+    assert torch.allclose(gg.float(), rg, rtol=1e-2, atol=1e-2 * rg.abs().max().item())
+    assert torch.allclose(gb.float(), rb, rtol=1e-2, atol=1e-2 * rb.abs().max().item())
