@@ -337,17 +337,18 @@ int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf
 /* Fused LM-head cross-entropy rows (C4 training step, train.lm_loss)        */
 /* ------------------------------------------------------------------------ */
 
-/* For each row r of a contiguous bf16 [rows, vocab] logits chunk:
- *   lse[r] = log sum_j exp(logit[r, j]),  loss_rows[r] = lse[r] - logit[r, targets[r]]
+/* For each row r of a bf16 [rows, pitch] logits chunk (columns >= vocab are
+ * padding and ignored):
+ *   lse[r] = log sum_{j<vocab} exp(logit[r, j]),  loss_rows[r] = lse[r] - logit[r, targets[r]]
  * (fp32 accumulation, one pass). */
-int sdp_ce_rows_fwd(const void* logits_bf16, int64_t rows, int vocab, const int64_t* targets,
+int sdp_ce_rows_fwd(const void* logits_bf16, int64_t rows, int vocab, int64_t pitch, const int64_t* targets,
                     float* lse, float* loss_rows, void* stream);
 
-/* dlogits = bf16((exp(logit - lse[r]) - [j == targets[r]]) * grad_out[0] * inv_n):
- * the gradient of mean cross-entropy w.r.t. the chunk's logits; grad_out is a
- * device scalar (no host sync, CUDA-graph capturable).  16-B aligned buffers,
- * vocab >= 8. */
-int sdp_ce_rows_bwd(const void* logits_bf16, int64_t rows, int vocab, const int64_t* targets,
+/* dlogits = bf16((exp(logit - lse[r]) - [j == targets[r]]) * grad_out[0] * inv_n)
+ * for j < vocab and 0 in the padding columns: the gradient of mean
+ * cross-entropy w.r.t. the chunk's logits; grad_out is a device scalar (no
+ * host sync, CUDA-graph capturable).  16-B aligned buffers. */
+int sdp_ce_rows_bwd(const void* logits_bf16, int64_t rows, int vocab, int64_t pitch, const int64_t* targets,
                     const float* lse, const float* grad_out, float inv_n, void* dlogits_bf16,
                     void* stream);
 

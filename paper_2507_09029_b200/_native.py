@@ -108,10 +108,10 @@ SIGNATURES = {
     "sdp_last_error": (C.c_char_p, []),
     "sdp_device_sm_count": (C.c_int, [C.POINTER(C.c_int)]),
     "sdp_host_ptr_on_device": (C.c_int, [VP, C.POINTER(C.c_int)]),
-    "sdp_ce_rows_fwd": (C.c_int, [VP, I64, I32, VP, VP, VP, VP]),
+    "sdp_ce_rows_fwd": (C.c_int, [VP, I64, I32, I64, VP, VP, VP, VP]),
     "sdp_group_norm_fwd": (C.c_int, [VP, I32, I32, I32, VP, I32, I32, VP, VP, C.c_float, I32, VP, VP, VP, VP]),
     "sdp_group_norm_bwd": (C.c_int, [VP, VP, VP, I32, I32, I32, VP, I32, I32, VP, VP, VP, I32, VP, VP, VP, VP]),
-    "sdp_ce_rows_bwd": (C.c_int, [VP, I64, I32, VP, VP, VP, C.c_float, VP, VP]),
+    "sdp_ce_rows_bwd": (C.c_int, [VP, I64, I32, I64, VP, VP, VP, C.c_float, VP, VP]),
     "sdp_assign_units": (C.c_int, [C.POINTER(C.c_uint32), I32, VP, I32, I32, I32, I32, I32, VP, VP, VP]),
     "sdp_permutation": (C.c_int, [C.POINTER(C.c_uint32), I32, VP, I32, I32, VP, VP]),
     "sdp_build_masks": (C.c_int, [VP, I32, VP, I32, VP, I32, I64, VP, I32, VP, VP, VP, VP, VP, VP]),

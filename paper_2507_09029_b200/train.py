@@ -207,21 +207,40 @@ class _LinearCrossEntropy(torch.autograd.Function):
     def _cdt(h):
         return torch.get_autocast_dtype("cuda") if torch.is_autocast_enabled("cuda") else h.dtype
 
+    PAD = 64  # head GEMMs on a 64-aligned vocabulary (50257 -> 50304)
+
+    @staticmethod
+    def _padded(w, cdt):
+        """The tied head weight in the GEMM dtype with its rows padded to a
+        multiple of PAD (zero rows): an aligned leading dimension keeps cuBLAS
+        on its tensor-core kernels (odd 50257 fell back to align-1 mma.sync:
+        69% of the GPT-2 step)."""
+        v = w.shape[0]
+        vp = -(-v // _LinearCrossEntropy.PAD) * _LinearCrossEntropy.PAD
+        if vp == v:
+            return w.to(cdt)
+        wp = torch.empty((vp, w.shape[1]), dtype=cdt, device=w.device)
+        wp[:v].copy_(w)
+        wp[v:].zero_()
+        return wp
+
     @staticmethod
     def forward(ctx, h, w, t):
         cdt = _LinearCrossEntropy._cdt(h)
-        hc, wc = h.to(cdt), w.to(cdt)
         t = t.contiguous()
-        n = h.shape[0]
+        n, v = h.shape[0], w.shape[0]
         acc = torch.float64 if cdt == torch.float64 else torch.float32
         lse = torch.empty(n, dtype=acc, device=h.device)
         rows = torch.empty(n, dtype=acc, device=h.device)
+        hc = h.to(cdt)
+        fused = cdt == torch.bfloat16
+        wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
         with torch.autocast("cuda", enabled=False):
             for s in range(0, n, _LinearCrossEntropy.CHUNK):
                 e = min(n, s + _LinearCrossEntropy.CHUNK)
                 lg = hc[s:e] @ wc.t()
-                if cdt == torch.bfloat16:  # libsdp k_ce_fwd: one pass over the bf16 chunk
-                    N.call("sdp_ce_rows_fwd", ptr(lg), e - s, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
+                if fused:  # libsdp k_ce_fwd: one pass over the bf16 chunk (padding ignored)
+                    N.call("sdp_ce_rows_fwd", ptr(lg), e - s, v, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
                            ptr(rows[s:e]), stream_ptr(h.device))
                 else:
                     lg = lg.to(acc)
@@ -235,19 +254,21 @@ class _LinearCrossEntropy(torch.autograd.Function):
     def backward(ctx, g):
         h, w, t, lse = ctx.saved_tensors
         cdt = ctx.cdt
-        hc, wc = h.to(cdt), w.to(cdt)
-        n = h.shape[0]
+        n, v = h.shape[0], w.shape[0]
         acc = lse.dtype
+        fused = cdt == torch.bfloat16
+        hc = h.to(cdt)
+        wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
         gh = torch.empty(h.shape, dtype=cdt, device=h.device)
-        gw = torch.zeros(w.shape, dtype=acc, device=w.device)
+        gw = torch.zeros(wc.shape, dtype=acc, device=w.device)
         g32 = g.detach().to(torch.float32).reshape(1).contiguous()
         with torch.autocast("cuda", enabled=False):
             for s in range(0, n, _LinearCrossEntropy.CHUNK):
                 e = min(n, s + _LinearCrossEntropy.CHUNK)
                 lg = hc[s:e] @ wc.t()
-                if cdt == torch.bfloat16:  # libsdp k_ce_bwd: softmax - onehot, scaled, in one pass
+                if fused:  # libsdp k_ce_bwd: softmax - onehot, scaled; zero in the padding
                     dl = torch.empty_like(lg)
-                    N.call("sdp_ce_rows_bwd", ptr(lg), e - s, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
+                    N.call("sdp_ce_rows_bwd", ptr(lg), e - s, v, lg.shape[1], ptr(t[s:e]), ptr(lse[s:e]),
                            ptr(g32), C.c_float(1.0 / n), ptr(dl), stream_ptr(h.device))
                 else:
                     p = torch.exp(lg.to(acc) - lse[s:e, None])
@@ -256,7 +277,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                 del lg
                 gh[s:e] = dl @ wc
                 gw += (dl.t() @ hc[s:e]).to(acc)
-        return gh.to(h.dtype), gw.to(w.dtype), None
+        return gh.to(h.dtype), gw[:v].to(w.dtype), None
 
 
 def lm_loss(out, tokens):
