@@ -140,6 +140,15 @@ class ResNet18Cifar:
         return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 
+def _layer_norm(x, shape, w, b):
+    """F.layer_norm; under bf16 autocast bf16 activations stay bf16 in and out
+    (fp32 statistics inside the kernel) instead of autocast's fp32 upcast."""
+    if x.dtype == torch.bfloat16 and torch.is_autocast_enabled("cuda"):
+        with torch.autocast("cuda", enabled=False):
+            return F.layer_norm(x, shape, w.to(x.dtype), b.to(x.dtype))
+    return F.layer_norm(x, shape, w, b)
+
+
 class GPT2Small:
     """BASELINE configs[3] (C4): GPT-2 small over zoo.gpt2_small_topology's flat
     layout -- pre-LN blocks, HF Conv1D weights ([in, out]), causal flash SDPA,
@@ -162,13 +171,13 @@ class GPT2Small:
             if not live and block_mode == "skip":
                 continue
             p = f"h{i}"
-            a = F.layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
+            a = _layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
             qkv = torch.addmm(params[f"{p}.attn.c_attn.b"], a.reshape(b * t, e), params[f"{p}.attn.c_attn.w"])
             q, k, v = qkv.view(b, t, 3, nh, e // nh).permute(2, 0, 3, 1, 4)
             y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             y = y.transpose(1, 2).reshape(b * t, e)
             y = torch.addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
-            m = F.layer_norm(h + y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
+            m = _layer_norm(h + y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
             m = F.gelu(torch.addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
                        approximate="tanh")
             m = torch.addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
@@ -176,7 +185,7 @@ class GPT2Small:
             if not live:
                 o = o * 0.0
             h = h + o
-        h = F.layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
+        h = _layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
         return LMHead(h, params["wte"])  # tied head, logits h @ wte.T left to lm_loss
 
 
@@ -276,7 +285,10 @@ class _LinearCrossEntropy(torch.autograd.Function):
                     dl = (p * (g.to(acc) / n)).to(cdt)
                 del lg
                 gh[s:e] = dl @ wc
-                gw += (dl.t() @ hc[s:e]).to(acc)
+                if fused:  # bf16 x bf16 accumulated straight into the fp32 gradient (cuBLAS C = D)
+                    torch.addmm(gw, dl.t(), hc[s:e], out_dtype=torch.float32, out=gw)
+                else:
+                    gw += (dl.t() @ hc[s:e]).to(acc)
         return gh.to(h.dtype), gw[:v].to(w.dtype), None
 
 
