@@ -285,9 +285,11 @@ typedef struct {
  * flags & SDP_GATHER_REVERSE: full[...] = compact[...] through the same
  * forward maps (only mapped full elements are written) -- the inverse of a
  * gather whose descriptors tile the full tensor, e.g. leaving the
- * window-class-major sync layout.  dtype SDP_DTYPE_U8 moves owner masks. */
+ * window-class-major sync layout.  dtype SDP_DTYPE_U8 moves owner masks,
+ * SDP_DTYPE_U16 bf16 training copies (gathers are typeless copies). */
 #define SDP_GATHER_REVERSE 0x1
 #define SDP_DTYPE_U8 2
+#define SDP_DTYPE_U16 3  /* 2-byte elements moved as bits (bf16 training copies) */
 int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
                       int n_tasks, const int32_t* fwd_maps, const void* full,
                       void* compact, int flags, void* stream);

@@ -51,6 +51,15 @@ def mask_bytes_for(n_workers: int) -> int:
 MASK_TORCH_DTYPE = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
 
 
+def slice_dtype(t: torch.dtype) -> int:
+    """dtype code of the (typeless) gather kernels: 2-byte types move as bits."""
+    if t in (torch.bfloat16, torch.float16):
+        return N.DTYPE_U16
+    if t == torch.uint8:
+        return N.DTYPE_U8
+    return sdp_dtype(t)
+
+
 def sdp_dtype(t: torch.dtype) -> int:
     if t == torch.float32:
         return N.DTYPE_F32

@@ -36,6 +36,7 @@ SCATTER_ACCUMULATE = 0x2
 DTYPE_F32 = 0
 DTYPE_F64 = 1
 DTYPE_U8 = 2
+DTYPE_U16 = 3
 GATHER_REVERSE = 0x1
 
 TILE_UNIFORM = 0x80000000

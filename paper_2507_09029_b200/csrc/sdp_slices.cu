@@ -511,7 +511,8 @@ int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_ta
   if (dtype == SDP_DTYPE_F32) SDP_GATHER(float);
   else if (dtype == SDP_DTYPE_F64) SDP_GATHER(double);
   else if (dtype == SDP_DTYPE_U8) SDP_GATHER(uint8_t);
-  else return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32, SDP_DTYPE_F64 or SDP_DTYPE_U8");
+  else if (dtype == SDP_DTYPE_U16) SDP_GATHER(uint16_t);
+  else return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32, SDP_DTYPE_F64, SDP_DTYPE_U8 or SDP_DTYPE_U16");
 #undef SDP_GATHER
   SDP_LAUNCH_CHECK();
   return SDP_OK;

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._device import ptr, sdp_dtype, stream_ptr, upload_struct
+from ._device import ptr, slice_dtype, stream_ptr, upload_struct
 from .errors import ConfigError
 from .topology import fast_divisor
 
@@ -161,12 +161,12 @@ class SyncLayout:
 
     def to_sync(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         out = torch.empty_like(x) if out is None else out
-        _gather(sdp_dtype(x.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, x, out, False, x.device)
+        _gather(slice_dtype(x.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, x, out, False, x.device)
         return out
 
     def from_sync(self, s: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         out = torch.empty_like(s) if out is None else out
-        _gather(sdp_dtype(s.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, out, s, True, s.device)
+        _gather(slice_dtype(s.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, out, s, True, s.device)
         return out
 
 
@@ -205,12 +205,12 @@ class WorkerTransfer:
     def to_compact(self, theta_sync: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         out = torch.empty(max(1, self.compact_total), dtype=theta_sync.dtype, device=theta_sync.device) \
             if out is None else out
-        _gather(sdp_dtype(theta_sync.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, out,
+        _gather(slice_dtype(theta_sync.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, out,
                 theta_sync, True, theta_sync.device)
         return out
 
     def from_compact(self, g: torch.Tensor, grad_sync: torch.Tensor) -> torch.Tensor:
-        _gather(sdp_dtype(g.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, g, grad_sync, False,
+        _gather(slice_dtype(g.dtype), self.d_desc, self.d_tasks, self.n_tasks, self.maps, g, grad_sync, False,
                 g.device)
         return grad_sync
 

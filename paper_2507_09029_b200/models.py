@@ -31,7 +31,7 @@ import torch
 import torch.nn.functional as F
 
 from . import _native as N
-from ._device import device, ptr, sdp_dtype, stream_ptr
+from ._device import device, ptr, sdp_dtype, slice_dtype, stream_ptr
 from .errors import ConfigError, InputError
 from .topology import GlobalModel, fast_divisor
 from . import zoo
@@ -538,7 +538,7 @@ class SubnetLayout:
         """Full theta -> compact buffer (sdp_gather_slices)."""
         if out is None:
             out = torch.empty(max(1, self.compact_total), dtype=theta.dtype, device=theta.device)
-        N.call("sdp_gather_slices", sdp_dtype(theta.dtype), ptr(self.d_fwd), ptr(self.t_gather),
+        N.call("sdp_gather_slices", slice_dtype(theta.dtype), ptr(self.d_fwd), ptr(self.t_gather),
                self.n_gather, ptr(self.fwd_maps), ptr(theta), ptr(out), 0, stream_ptr(theta.device))
         return out
 

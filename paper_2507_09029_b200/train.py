@@ -467,15 +467,18 @@ class SubnetTrainer:
         for w, (x, y) in enumerate(batches):
             if self.compact:
                 sub = self.subs[w]
+                # the worker trains on the bf16 copy the previous sync wrote
+                src = self.theta_bf16 if self.autocast else self.model.theta
                 if self.slayout:  # the worker's blocks of the permuted theta
-                    leaf = self.transfers[w].to_compact(self.model.theta).requires_grad_(True)
+                    leaf = self.transfers[w].to_compact(src).requires_grad_(True)
                 else:
-                    leaf = sub.gather(self.model.theta).requires_grad_(True)  # sdp_gather_slices
+                    leaf = sub.gather(src).requires_grad_(True)  # sdp_gather_slices
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                     logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
                     loss = self.loss_fn(logits, y)
                 del logits
                 (g,) = torch.autograd.grad(loss, leaf)
+                g = g.float()  # fp32 gradient replica (the sync accumulates in fp32)
                 if self.slayout:
                     self.transfers[w].from_compact(g, self.grads[w])
                 else:
@@ -556,11 +559,12 @@ class PeerTrainer:
             x, y = batches[w]
             if self.compact:
                 sub = self.subs[w]
-                leaf = self.transfers[w].to_compact(self.theta[w]).requires_grad_(True)
+                src = self.theta_bf16[w] if self.autocast else self.theta[w]
+                leaf = self.transfers[w].to_compact(src).requires_grad_(True)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
                     loss = self.loss_fn(self.model.arch.forward_compact(sub.views(leaf), x, sub), y)
                 (g,) = torch.autograd.grad(loss, leaf)
-                self.transfers[w].from_compact(g, self.group.replicas[w])
+                self.transfers[w].from_compact(g.float(), self.group.replicas[w])
             else:
                 leaf = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach().requires_grad_(True)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
@@ -621,9 +625,9 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
     base = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
     # compact fp32 master + fp32 gradient (what the sync reads) + momentum + bf16
-    # training copy.  The step mirrors SubnetTrainer's: block workers run on
-    # the bf16 copy, width-wise workers on the fp32 compact master under
-    # autocast (no weight-cast cache, as in the graphed step).  Every
+    # training copy.  The step mirrors SubnetTrainer's: every worker runs on
+    # the bf16 copy under autocast (no weight-cast cache, as in the graphed
+    # step).  Every
     # parameter is a leaf view whose gradient is written into its slot of the
     # fp32 flat gradient the moment autograd finishes it and then freed
     # (post-accumulate hook): no second gradient-sized buffer and no
@@ -633,7 +637,7 @@ def worker_memory(model: GlobalModel, assignment, worker: int | None, batch: int
     momentum = torch.zeros_like(master)
     shadow = master.to(torch.bfloat16)
     gviews = sub.views(grad)
-    weights = sub.views(master if assignment.strategy == "neuron" else shadow)
+    weights = sub.views(shadow)
     leaves = {}
     for name, v in weights.items():
         if v.numel() == 0:

@@ -123,9 +123,7 @@ def test_memory_step_gradient_is_the_worker_gradient(cuda, strategy):
     y = torch.randint(0, 10, (8,), generator=gen, device=cuda)
     got = train.worker_memory(model, a, 3, 8, cuda, make_batch=lambda: (x, y), return_grad=True)["grad"]
     sub = models.SubnetLayout(a, 3)
-    leaf = sub.gather(model.theta)
-    if strategy == "block":  # block workers train on the bf16 copy
-        leaf = leaf.to(torch.bfloat16)
+    leaf = sub.gather(model.theta).to(torch.bfloat16)  # workers train on the bf16 copy
     leaf.requires_grad_(True)
     with torch.autocast("cuda", dtype=torch.bfloat16):
         if strategy == "neuron":
