@@ -524,12 +524,13 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
 
     batch, n = 64, args.n_logical
     out = {"workload": f"ResNet-18 CIFAR-shape, N={n} workers on {world} GPUs ({n // world} per GPU), "
-                       f"batch {batch}/worker, bf16 autocast, peer-mapped owner sync + local fused Nesterov/bf16",
+                       f"batch {batch}/worker, bf16 autocast, peer-mapped owner sync + local fused Nesterov/bf16, "
+                       "each rank's step replayed from a CUDA graph",
            "data": "synthetic", "timing": "CUDA events per rank, max over ranks"}
     for tag, p, strategy in (("subnet", args.p, "block"), ("widthwise", args.p, "neuron"), ("dp", n, "block")):
         model = train.build_resnet18(dev)
         a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
-        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.02)
+        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.02, graphed=True)
         gen = torch.Generator(device=dev)
         batches = {}
         for w in tr.local:
@@ -569,7 +570,8 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
     for tag, p in (("subnet", args.p), ("dp", n)):
         model = train.build_gpt2(dev)
         a = masking.build_assignment(model.topology, "block", n, p, seed=1)
-        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=1e-4, loss_fn=train.lm_loss)
+        tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=1e-4, loss_fn=train.lm_loss,
+                               graphed=True)
         gen = torch.Generator(device=dev)
         batches = {}
         for w in tr.local:

@@ -216,6 +216,11 @@ typedef struct {
    * the bias corrections bias1 = 1 - beta1^t, bias2 = 1 - beta2^t. */
   void* second_moment;
   double beta1, beta2, one_minus_beta1, one_minus_beta2, bias1, bias2, eps;
+  /* multi-GPU, optional: device-resident barrier epochs, one uint32 per CTA
+   * (zeroed once).  When set, each CTA takes epoch = counter + 1 and stores
+   * it back after its exit barrier, so the launch can be replayed from a
+   * CUDA graph; `epoch` above is then ignored. */
+  uint32_t* epoch_counters;
 } sdp_sync_args;
 
 /* Launch the owner-subset sync.  For every element j with owner set O_j:

@@ -98,6 +98,7 @@ class SyncArgs(C.Structure):
         ("beta1", C.c_double), ("beta2", C.c_double), ("one_minus_beta1", C.c_double),
         ("one_minus_beta2", C.c_double), ("bias1", C.c_double), ("bias2", C.c_double),
         ("eps", C.c_double),
+        ("epoch_counters", C.c_void_p),
     ]
 
 

@@ -153,10 +153,15 @@ class PeerGroup:
         self.args = bind_rank_args(self.plan, N.DTYPE_F32 if dtype == torch.float32 else N.DTYPE_F64,
                                    self.rep_ptr, self.sh_ptr, self.pad_ptr, self.status.data_ptr(),
                                    timeout_cycles)
+        # barrier epochs live on the device (one per CTA), so a launch recorded
+        # in a CUDA graph replays with fresh flag values every time
+        self.epochs = torch.zeros(self.grid, dtype=torch.int32, device=self.device)
+        self.args.epoch_counters = self.epochs.data_ptr()
         self._fn = N.lib().sdp_owner_sync
 
     def launch(self, stream=None) -> None:
-        """One synchronised owner-subset sync step (asynchronous on the stream)."""
+        """One synchronised owner-subset sync step (asynchronous on the stream;
+        capturable in a CUDA graph — every rank must replay its graph in step)."""
         self.epoch += 1
         self.args.epoch = self.epoch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)

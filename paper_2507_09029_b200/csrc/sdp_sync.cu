@@ -102,6 +102,7 @@ struct SyncParams {
   int32_t n_workers, tile, n_tiles, tiles_per_cta, flags, rank, world;
   uint32_t epoch;
   bool has_shadow;
+  uint32_t* epoch_ctr;  // device-resident barrier epochs (graph replay), or null
 };
 
 // Pairwise per-CTA barrier: CTA b of every rank meets CTA b of every other rank.
@@ -400,7 +401,8 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
   __shared__ alignas(16) sdp_tile_desc s_desc[kStage];
   __shared__ alignas(8) uint64_t s_bar;
   uint32_t st = 0;
-  if (p.world > 1 && !cross_rank_barrier(p, 2u * p.epoch + 1u)) return;
+  const uint32_t ep = p.epoch_ctr ? __ldcg(p.epoch_ctr + blockIdx.x) + 1u : p.epoch;
+  if (p.world > 1 && !cross_rank_barrier(p, 2u * ep + 1u)) return;
 
   const int first = blockIdx.x * p.tiles_per_cta;
   const int count = min(p.tiles_per_cta, p.n_tiles - first);
@@ -416,7 +418,8 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
       run_tile<T, MB, R>(p, d, st);
     }
     if (st && p.status) atomicOr(p.status, st);
-    if (p.world > 1) cross_rank_barrier(p, 2u * p.epoch + 2u);
+    if (p.world > 1) cross_rank_barrier(p, 2u * ep + 2u);
+    if (p.epoch_ctr && threadIdx.x == 0) p.epoch_ctr[blockIdx.x] = ep;
     return;
   }
   if (threadIdx.x == 0) {
@@ -438,7 +441,8 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
     __syncthreads();  // s_desc is overwritten by the next stage
   }
   if (st && p.status) atomicOr(p.status, st);
-  if (p.world > 1) cross_rank_barrier(p, 2u * p.epoch + 2u);
+  if (p.world > 1) cross_rank_barrier(p, 2u * ep + 2u);
+  if (p.epoch_ctr && threadIdx.x == 0) p.epoch_ctr[blockIdx.x] = ep;
 }
 
 template <typename T>
@@ -545,6 +549,7 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   p.rank = a->rank;
   p.world = a->world;
   p.epoch = a->epoch;
+  p.epoch_ctr = a->world > 1 ? a->epoch_counters : nullptr;
 
   const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
   cudaStream_t s = as_stream(stream);

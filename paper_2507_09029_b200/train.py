@@ -339,6 +339,16 @@ def downsample(h: torch.Tensor, w: torch.Tensor, stride: int) -> torch.Tensor:
     return F.conv2d(h[:, :, ::stride, ::stride], w)
 
 
+def live_params(topology, view) -> list:
+    """Parameters a worker's subnetwork uses (block strategy: not in a dropped
+    block; masking.py:160-169)."""
+    dead = set()
+    for b in topology.blocks:
+        if b.maskable and not bool(view.block_active[b.index]):
+            dead.update(b.param_names)
+    return [p.name for p in topology.params if p.name not in dead]
+
+
 @dataclass
 class StepStats:
     loss_mean: float
@@ -389,18 +399,10 @@ class SubnetTrainer:
         self._prep = None
 
     def _live_params(self, w: int) -> list:
-        """Parameters worker w's subnetwork uses (block strategy: not in a
-        dropped block; masking.py:160-169)."""
         if not hasattr(self, "_live"):
             self._live = {}
         if w not in self._live:
-            topo = self.model.topology
-            dead = set()
-            view = self.views[w]
-            for b in topo.blocks:
-                if b.maskable and not bool(view.block_active[b.index]):
-                    dead.update(b.param_names)
-            self._live[w] = [p.name for p in topo.params if p.name not in dead]
+            self._live[w] = live_params(self.model.topology, self.views[w])
         return self._live[w]
 
     def _grad_slots(self, w: int) -> dict:
@@ -524,10 +526,17 @@ class PeerTrainer:
 
     def __init__(self, model: GlobalModel, assignment, rank: int, world: int, device, all_gather,
                  lr: float = 0.1, momentum: float = 0.9, autocast: bool = True, loss_fn=None,
-                 timeout_cycles: int = 20_000_000_000):
+                 timeout_cycles: int = 20_000_000_000, graphed: bool = False):
+        """graphed: capture the rank's whole step (local workers' fwd/bwd, the
+        peer-mapped sync, the Nesterov updates) in one CUDA graph, as
+        SubnetTrainer does.  The sync kernel keeps its cross-rank barrier
+        epochs on the device (comm.PeerGroup.epochs), so replays stay in step
+        as long as every rank calls step() the same number of times."""
         from . import comm
         self.model, self.assignment = model, assignment
         self.lr, self.momentum, self.autocast = lr, momentum, autocast
+        self.graphed = graphed
+        self._graph = None
         self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
         self.device = torch.device(device)
         self.compact = assignment.strategy == "neuron"
@@ -550,9 +559,49 @@ class PeerTrainer:
         self.velocity = {w: torch.zeros_like(theta0) for w in self.local}
         self.theta_bf16 = {w: theta0.to(torch.bfloat16) for w in self.local}
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if not self.compact:
+            # per-parameter gradient slots of each replica; parameters of a
+            # worker's dropped blocks are never written (the replica keeps
+            # zeros there: the sync only writes owned elements)
+            self._slots = {w: param_views(model.topology, self.group.replicas[w]) for w in self.local}
+            self._live = {w: live_params(model.topology, self.views[w]) for w in self.local}
 
     def step(self, batches: dict) -> torch.Tensor:
         """batches: {local worker: (x, y)}; returns the local workers' mean loss."""
+        if not self.graphed:
+            return self._step_eager(batches)
+        if self._graph is None or self._graph_lr != self.lr:
+            self._capture(batches)
+        for w, (x, y) in batches.items():
+            sx, sy = self._static[w]
+            if sx.data_ptr() != x.data_ptr():
+                sx.copy_(x)
+            if sy.data_ptr() != y.data_ptr():
+                sy.copy_(y)
+        self._graph.replay()
+        return self._static_loss
+
+    def _capture(self, batches, warmup: int = 2) -> None:
+        """Warm-up steps on a side stream (they run the collective sync, so
+        every rank does the same number), rolled back, then one captured step."""
+        self._static = {w: (x.clone(), y.clone()) for w, (x, y) in batches.items()}
+        state = [t for w in self.local for t in (self.theta[w], self.velocity[w], self.theta_bf16[w])]
+        saved = [t.clone() for t in state]
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._step_eager(self._static, cache=False)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        for t, v in zip(state, saved):
+            t.copy_(v)
+        del saved
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self._static_loss = self._step_eager(self._static, cache=False)
+        self._graph_lr = self.lr
+
+    def _step_eager(self, batches: dict, cache: bool = True) -> torch.Tensor:
         topo = self.model.topology
         losses = []
         for w in self.local:
@@ -561,16 +610,19 @@ class PeerTrainer:
                 sub = self.subs[w]
                 src = self.theta_bf16[w] if self.autocast else self.theta[w]
                 leaf = self.transfers[w].to_compact(src).requires_grad_(True)
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                     loss = self.loss_fn(self.model.arch.forward_compact(sub.views(leaf), x, sub), y)
                 (g,) = torch.autograd.grad(loss, leaf)
                 self.transfers[w].from_compact(g.float(), self.group.replicas[w])
             else:
-                leaf = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach().requires_grad_(True)
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast):
-                    loss = self.loss_fn(self.model.arch.forward(param_views(topo, leaf), x, self.views[w]), y)
-                (g,) = torch.autograd.grad(loss, leaf)
-                self.group.replicas[w].copy_(g)
+                src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
+                params = {k: v.requires_grad_(True) for k, v in param_views(topo, src).items()}
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
+                    loss = self.loss_fn(self.model.arch.forward(params, x, self.views[w]), y)
+                names = self._live[w]
+                gs = torch.autograd.grad(loss, [params[k] for k in names])
+                slots = self._slots[w]
+                torch._foreach_copy_([slots[k] for k in names], list(gs))
             losses.append(loss.detach())
         self.group.launch()  # peer-mapped owner sync: replicas[w] <- mean on w's elements
         for w in self.local:

@@ -123,7 +123,7 @@ TRAIN_CHILD = textwrap.dedent(r"""
     model = train.build_resnet18(dev, seed=5)
     a = masking.build_assignment(model.topology, os.environ["STRATEGY"], 4, 2, seed=1)
     tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=False,
-                           timeout_cycles=10_000_000_000)
+                           timeout_cycles=10_000_000_000, graphed=os.environ["GRAPHED"] == "1")
     for step in range(2):
         batches = {}
         for w in tr.local:
@@ -142,11 +142,14 @@ TRAIN_CHILD = textwrap.dedent(r"""
 """)
 
 
+@pytest.mark.parametrize("graphed", [False, True])
 @pytest.mark.parametrize("strategy", ["block", "neuron"])
-def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy):
+def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
     """train.PeerTrainer over 2 processes (CUDA-IPC replicas, cross-rank sync,
     local Nesterov) leaves every worker's copy of its parameters bit-identical
-    to the co-resident trainer's canonical theta (fp32, deterministic cuDNN)."""
+    to the co-resident trainer's canonical theta (fp32, deterministic cuDNN) --
+    also when each rank replays its step from a CUDA graph (device-resident
+    barrier epochs)."""
     import torch
     from paper_2507_09029_b200 import masking, train
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -154,7 +157,8 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy):
     procs = []
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy)
+                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy,
+                   GRAPHED=str(int(graphed)))
         procs.append(subprocess.Popen([sys.executable, "-c", TRAIN_CHILD], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
