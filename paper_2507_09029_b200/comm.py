@@ -17,7 +17,7 @@ Per-CTA release/acquire flag barriers on the signal pads bracket the launch
 replicas have landed), with a spin timeout that reports instead of hanging.
 
 The exchange logic (`exchange_handles`, `rank_layout`) is CUDA-free so the
-N > 1 host path is tested with gloo on CPU (tests/test_multirank_gloo.py).
+N > 1 host path is tested with gloo on CPU (tests/test_multirank.py).
 """
 
 from __future__ import annotations
@@ -178,6 +178,75 @@ class PeerGroup:
         for p in self._imported:
             N.call("sdp_ipc_close", C.c_void_p(p))
         self._imported.clear()
+
+
+_GROUPS: dict = {}
+
+
+def _dist_all_gather(obj) -> list:
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def aggregate_local(grads, assignment, rank: int | None = None, world: int | None = None,
+                    device=None, all_gather=None, fresh: bool = True, check: bool = False) -> dict:
+    """Per-rank form of engine.aggregate (engine.py:60-79) for torchrun jobs
+    (SURVEY.md §8b): every rank passes the gradients of ITS local workers
+    (contiguous placement, rank_layout) and receives, for each of them, the
+    owner-subset mean on that worker's owned elements.
+
+    grads: {worker: fp32 [d] tensor on this rank's GPU} (a bare tensor when
+    the rank holds one worker); gradients must be zero off the worker's mask,
+    as the reference's masked backward leaves them (models.py:369-382).
+    Returns {worker: [d] fp32}: gbar on the worker's owned elements, 0
+    elsewhere -- exactly `aggregate(...).gbar * param_masks[w]`, bit for bit
+    with the co-resident kernel.  All ranks must call it together (it is a
+    collective over the peer-mapped replicas; the first call per assignment
+    exchanges CUDA-IPC handles through torch.distributed).  fresh=False
+    returns the peer group's replicas themselves (overwritten by the next
+    call) instead of copies.  check=True waits for the kernel and raises on a
+    cross-rank barrier timeout."""
+    import torch.distributed as dist
+    if rank is None or world is None:
+        if not dist.is_initialized():
+            raise ProtocolError("aggregate_local needs rank/world or an initialised torch.distributed")
+        rank = dist.get_rank() if rank is None else rank
+        world = dist.get_world_size() if world is None else world
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (id(assignment), rank, world, dev)
+    g = _GROUPS.get(key)
+    if g is None or g.assignment is not assignment:
+        g = PeerGroup(assignment, rank, world, dev, all_gather or _dist_all_gather, shadows=False)
+        _GROUPS[key] = g
+    local = g.layout.local_workers
+    if torch.is_tensor(grads):
+        if len(local) != 1:
+            raise ProtocolError(f"rank {rank} holds workers {local}: pass a {{worker: gradient}} dict")
+        grads = {local[0]: grads}
+    if sorted(grads) != local:
+        raise ProtocolError(f"aggregate_local on rank {rank} received gradients for workers "
+                            f"{sorted(grads)}, expected its local workers {local}")
+    d = assignment.topology.total
+    for w, t in grads.items():
+        if not torch.is_tensor(t) or t.shape != (d,) or t.dtype != torch.float32 or t.device != dev:
+            raise ProtocolError(f"worker {w}: expected a float32 [{d}] tensor on {dev}")
+        if t.data_ptr() != g.replicas[w].data_ptr():
+            g.replicas[w].copy_(t)
+    g.launch()
+    if check:
+        torch.cuda.current_stream(dev).synchronize()
+        g.check()
+    return {w: g.replicas[w].clone() if fresh else g.replicas[w] for w in local}
+
+
+def close_local_groups() -> None:
+    """Unmap every peer group aggregate_local opened (call before
+    destroy_process_group)."""
+    for g in _GROUPS.values():
+        g.close()
+    _GROUPS.clear()
 
 
 def bench_setup(assignment, rank: int, world: int, device):

@@ -193,3 +193,71 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
         for w in (0, 1) if r == 0 else (2, 3):
             got = z[f"w{w}"]
             assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
+
+
+LOCAL_CHILD = textwrap.dedent(r"""
+    import os, sys, numpy as np, torch, torch.distributed as dist
+    sys.path.insert(0, os.environ["REPO"])
+    from paper_2507_09029_b200 import comm, masking, zoo
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32))
+    a = masking.build_assignment(topo, os.environ["STRATEGY"], 4, 2, seed=1)
+    local = comm.rank_layout(4, world, rank).local_workers
+    res = {}
+    for step in range(2):  # the second call reuses the cached peer group
+        grads = {}
+        gen = torch.Generator(device="cuda")
+        for w in local:
+            gen.manual_seed(50 + 10 * step + w)
+            grads[w] = torch.randn(topo.total, generator=gen, device="cuda") * a.param_masks[w]
+        out = comm.aggregate_local(grads if len(local) > 1 else grads[local[0]], a, check=True)
+        res.update({f"s{step}w{w}": t.cpu().numpy() for w, t in out.items()})
+    np.savez(os.path.join(os.environ["OUT"], f"rank{rank}.npz"), **res)
+    comm.close_local_groups()
+    dist.destroy_process_group()
+""")
+
+
+@pytest.mark.parametrize("strategy,world", [("block", 2), ("neuron", 2), ("block", 4)])
+def test_aggregate_local_matches_aggregate(cuda, tmp_path, strategy, world):
+    """comm.aggregate_local (the per-rank form of engine.aggregate)
+    over real processes: every rank gets gbar * mask_w for its local workers,
+    bit-identical to the oracle's ordered fp32 mean; 0 off the mask."""
+    import torch
+    from oracle import oracle as O
+    from paper_2507_09029_b200 import masking, zoo
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy)
+        procs.append(subprocess.Popen([sys.executable, "-c", LOCAL_CHILD], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=180)[0])
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            pytest.fail("aggregate_local ranks did not finish in 180 s")
+    assert all(p.returncode == 0 for p in procs), "\n".join(outs)
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32))
+    a = masking.build_assignment(topo, strategy, 4, 2, seed=1)
+    masks = a.param_masks.cpu().numpy()
+    for step in range(2):
+        gen = torch.Generator(device="cuda")
+        host = []
+        for w in range(4):
+            gen.manual_seed(50 + 10 * step + w)
+            host.append((torch.randn(topo.total, generator=gen, device="cuda") * a.param_masks[w]).cpu().numpy())
+        want = O.aggregate_f32_ordered(host, masks)
+        for r in range(world):
+            z = np.load(tmp_path / f"rank{r}.npz")
+            for w in [w for w in range(4) if w * world // 4 == r]:
+                got, m = z[f"s{step}w{w}"], masks[w]
+                assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (step, r, w)
+                assert not got[~m].any()

@@ -128,3 +128,15 @@ def test_gloo_world2_handle_exchange_and_partition():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_aggregate_local_requires_rank_or_process_group():
+    """comm.aggregate_local raises the reference's ProtocolError (not a CUDA
+    error) when it cannot tell which rank it runs on."""
+    import torch.distributed as dist
+    from paper_2507_09029_b200 import comm
+    from paper_2507_09029_b200.errors import ProtocolError
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised in this process")
+    with pytest.raises(ProtocolError):
+        comm.aggregate_local({0: None}, object())

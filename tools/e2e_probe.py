@@ -139,3 +139,53 @@ for k in (4, 8, 16, 32):
     ok = np.array_equal(out_h.numpy().view(np.uint32), ref.view(np.uint32))
     print(f'hybrid copy-engine H2D + zero-copy output, {k} chunks: {ms:.3f} ms  e2e {plan.owned_elems * 4 / ms / 1e6:.1f} GB/s',
           'bit-exact' if ok else 'MISMATCH')
+
+# where does the hybrid lose time?  (a) the same pipeline writing the mean to a
+# DEVICE buffer (no PCIe writes), (b) pinned output; host issue time per call
+out_d = torch.empty(d, device=dev)
+plans = {}
+
+
+def hybrid2(k, out):
+    bounds = [n_tiles * c // k for c in range(k + 1)]
+    cur = torch.cuda.current_stream()
+    s_in.wait_stream(cur)
+    for c in range(k):
+        lo_e, hi_e = bounds[c] * tile, min(d, bounds[c + 1] * tile)
+        with torch.cuda.stream(s_in):
+            for w in range(8):
+                for st, ln in full.worker_ranges(w):
+                    x0, x1 = max(st, lo_e), min(st + ln, hi_e)
+                    if x0 < x1:
+                        reps_d[w][x0:x1].copy_(hp[w][x0:x1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s_in)
+        cur.wait_event(ev)
+        plan = a.sync_plan(tile=tile, tile_lo=bounds[c], tile_hi=bounds[c + 1])
+        engine.owner_sync(reps_d, a, out=out, writeback=False, plan=plan, zero_copy=True)
+
+
+for k in (4, 8):
+    for name, o in (("device out", out_d), ("pinned out", out_h)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hybrid2(k, o)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ms = tm(lambda: hybrid2(k, o))
+        print(f'hybrid2 {k} chunks, {name}: {ms:.3f} ms (host issue {1e3 * (t1 - t0):.3f} ms of {1e3 * (t2 - t0):.3f})')
+# copies only (same chunking), no kernels
+for k in (1, 4, 8):
+    def copies_only():
+        bounds = [n_tiles * c // k for c in range(k + 1)]
+        with torch.cuda.stream(s_in):
+            for c in range(k):
+                lo_e, hi_e = bounds[c] * tile, min(d, bounds[c + 1] * tile)
+                for w in range(8):
+                    for st, ln in full.worker_ranges(w):
+                        x0, x1 = max(st, lo_e), min(st + ln, hi_e)
+                        if x0 < x1:
+                            reps_d[w][x0:x1].copy_(hp[w][x0:x1], non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s_in)
+    print(f'owned-range H2D in {k} chunks: {tm(copies_only):.3f} ms')

@@ -115,6 +115,30 @@ int main() {
       if (rep) report(name, ms);
     }
   }
+  // (d) concurrent: SM 16-B loads over the first f of the buffer while the copy
+  //     engine moves the rest (a hybrid zero-copy + staged sync would do this)
+  cudaStream_t s1, s2;
+  cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  cudaEvent_t j;
+  cudaEventCreate(&j);
+  for (int rep = 0; rep < 2; ++rep) {
+    for (double f : {0.3, 0.4, 0.5, 0.6, 0.7}) {
+      const size_t a = ((size_t)(bytes * f) / 4096) * 4096;
+      cudaEventRecord(e0, s1);
+      cudaStreamWaitEvent(s2, e0, 0);
+      k_vec<<<sms * 8, 256, 0, s1>>>(reinterpret_cast<const float4*>(h), a / 16, out);
+      cudaMemcpyAsync(d + a, h + a, bytes - a, cudaMemcpyHostToDevice, s2);
+      cudaEventRecord(j, s2);
+      cudaStreamWaitEvent(s1, j, 0);
+      cudaEventRecord(e1, s1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      char name[64];
+      snprintf(name, sizeof name, "SM loads %.0f%% || copy engine %.0f%%", 100 * f, 100 * (1 - f));
+      if (rep) report(name, ms);
+    }
+  }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
