@@ -128,7 +128,8 @@ class SyncPlan:
     def __init__(self, assignment, world: int = 1, rank: int = 0, tile: int | None = None,
                  resident: bool = False, max_grid: int | None = None,
                  force_grid: int | None = None, tile_lo: int | None = None,
-                 tile_hi: int | None = None, owner_mask: torch.Tensor | None = None):
+                 tile_hi: int | None = None, owner_mask: torch.Tensor | None = None,
+                 order: str = "mixed_first"):
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
@@ -155,6 +156,20 @@ class SyncPlan:
         if tile_lo is not None or tile_hi is not None:  # a chunk of the vector (pipelined host path)
             lo, hi = tile_lo or 0, n_tiles if tile_hi is None else tile_hi
             mine = mine[(mine["tile_index"] >= lo) & (mine["tile_index"] < hi)]
+        # dispatch order of the tiles (CTA b takes b, b + grid, ...): the
+        # lane-per-element mixed tiles are the slow ones, so they go out in the
+        # first wave instead of forming the tail (same-box A/B, tools/c3_ab.py:
+        # C3 sync layout 63.6 -> 60.1 us, C2 unchanged)
+        if order != "index":
+            uni = (mine["len_flags"] & N.TILE_UNIFORM) != 0
+            if order == "mixed_first":
+                key = uni.astype(np.int64)
+            elif order == "cost":  # heaviest first: owners read, x5 for lane-per-element tiles
+                pc = np.bitwise_count(mine["owner_bits"]).astype(np.int64)
+                key = -(pc * np.where(uni, 1, 5))
+            else:
+                raise ValueError(f"unknown tile order {order!r}")
+            mine = mine[np.argsort(key, kind="stable")]
         self.n_tiles = len(mine)
         # every CTA must be co-resident for the cross-rank flag barrier
         self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1,

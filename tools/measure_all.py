@@ -61,7 +61,7 @@ def emit(kernel, config, us, us_min, nbytes, **extra):
 
 
 def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None, reps=20,
-              sync_layout=False):
+              sync_layout=False, **plan_kw):
     a = masking.build_assignment(topo, strategy, n, p, seed=1)
     d = topo.total
     pm = a.param_masks
@@ -77,9 +77,9 @@ def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None
         from paper_2507_09029_b200.layout import SyncLayout
         lay = SyncLayout(a)
         reps_t = [lay.to_sync(r) for r in reps_t]
-        plan = lay.plan(tile=tile)
+        plan = lay.plan(tile=tile, **plan_kw)
     else:
-        plan = a.sync_plan(tile=tile)
+        plan = a.sync_plan(tile=tile, **plan_kw)
     prep = engine.PreparedSync(reps_t, a, writeback=writeback, shadows_bf16=sh, out=out, plan=plan)
     us, us_min = timed(prep.launch, reps=reps)
     own = plan.owned_elems
@@ -87,7 +87,7 @@ def sync_case(topo, tag, strategy, n, p, writeback=True, shadows=True, tile=None
     nbytes = own * 4 + (own * (4 + (2 if shadows else 0)) if writeback else d * 4) + mixed * plan.tile
     emit("k_owner_sync", tag, us, us_min, nbytes, strategy=strategy, n=n, p=p, d=d,
          mode="replica writeback" + (" + bf16" if shadows else "") if writeback else "aggregate (out)",
-         tile=plan.tile, tiles=plan.n_tiles, mixed_tiles=mixed,
+         tile=plan.tile, tiles=plan.n_tiles, mixed_tiles=mixed, grid=plan.grid,
          sync_GBps=round(own * 4 / us / 1e3, 1))
     return a, reps_t
 
