@@ -340,6 +340,28 @@ int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf
                        const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
                        float* dgamma, float* dbeta, void* stream);
 
+/* Row LayerNorm on bf16 [rows, cols] activations, cols a multiple of 256 (up
+ * to 2048 forward, 1024 backward): the GPT-2 blocks of the C4 training step
+ * (train._layer_norm).  Forward saves fp32 mean / rstd per row.  Backward
+ * writes dx and the bf16 dgamma / dbeta; `scratch` holds 2 x cols x parts
+ * floats, parts = sdp_layer_norm_bwd_parts(rows, cols) (per-CTA partial sums folded
+ * in CTA order: deterministic). */
+int sdp_layer_norm_fwd(const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                       const void* beta_bf16, float eps, void* y_bf16, float* mean, float* rstd, void* stream);
+int sdp_layer_norm_bwd_parts(int64_t rows, int cols);
+int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                       const float* mean, const float* rstd, void* dx_bf16, void* dgamma_bf16, void* dbeta_bf16,
+                       float* scratch, int parts, void* stream);
+
+/* Attention-head gradient merge (train._SplitHeads backward): dq, dk, dv
+ * [batch, heads, seq, head_dim] with element strides (stride_batch,
+ * stride_head, stride_seq) shared by the three and contiguous head rows ->
+ * out [batch, seq, 3, heads, head_dim], the fused qkv projection's gradient.
+ * elem_bytes 2 or 4. */
+int sdp_merge_heads(const void* dq, const void* dk, const void* dv, int64_t batch, int64_t seq, int heads,
+                    int head_dim, int elem_bytes, int64_t stride_batch, int64_t stride_head, int64_t stride_seq,
+                    void* out, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Fused LM-head cross-entropy rows (C4 training step, train.lm_loss)        */
 /* ------------------------------------------------------------------------ */

@@ -140,13 +140,132 @@ class ResNet18Cifar:
         return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 
-def _layer_norm(x, shape, w, b):
-    """F.layer_norm; under bf16 autocast bf16 activations stay bf16 in and out
-    (fp32 statistics inside the kernel) instead of autocast's fp32 upcast."""
+class _LayerNormBF16(torch.autograd.Function):
+    """Row LayerNorm of bf16 activations on libsdp's k_ln_fwd / k_ln_bwd (one
+    warp per row, fp32 statistics; the weight / bias gradients reduced per CTA
+    and folded in CTA order).  torch's bf16 layer_norm backward spent 74 us of
+    a [8192, 768] call in its gamma/beta kernel: ~1 ms of a GPT-2 worker step."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, eps):
+        cols = x.shape[-1]
+        rows = x.numel() // cols
+        x2 = x.contiguous()
+        y = torch.empty_like(x2)
+        mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        N.call("sdp_layer_norm_fwd", ptr(x2), rows, cols, ptr(w), ptr(b), C.c_float(eps), ptr(y), ptr(mean),
+               ptr(rstd), stream_ptr(x.device))
+        ctx.save_for_backward(x2, w, mean, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w, mean, rstd = ctx.saved_tensors
+        cols = x.shape[-1]
+        rows = x.numel() // cols
+        dy = dy.contiguous()
+        if dy.data_ptr() % 16:
+            dy = dy.clone()
+        parts = N.lib().sdp_layer_norm_bwd_parts(rows, cols)
+        scratch = torch.empty(2 * cols * parts, dtype=torch.float32, device=x.device)
+        dx = torch.empty_like(x)
+        dw = torch.empty(cols, dtype=torch.bfloat16, device=x.device)
+        db = torch.empty(cols, dtype=torch.bfloat16, device=x.device)
+        N.call("sdp_layer_norm_bwd", ptr(dy), ptr(x), rows, cols, ptr(w), ptr(mean), ptr(rstd), ptr(dx), ptr(dw),
+               ptr(db), ptr(scratch), parts, stream_ptr(x.device))
+        return dx, dw, db, None
+
+
+def _ln_native(x, w, b) -> bool:
+    cols = x.shape[-1]
+    return (x.is_cuda and x.dtype == torch.bfloat16 and cols % 256 == 0 and cols <= 1024
+            and w.dtype == torch.bfloat16 and b.dtype == torch.bfloat16)
+
+
+def _aligned16(t: torch.Tensor) -> torch.Tensor:
+    return t if t.is_contiguous() and t.data_ptr() % 16 == 0 else t.contiguous().clone()
+
+
+def _layer_norm(x, shape, w, b, eps: float = 1e-5):
+    """LayerNorm over the last dim; under bf16 autocast bf16 activations stay
+    bf16 in and out (fp32 statistics inside the kernel) instead of autocast's
+    fp32 upcast, on libsdp's row kernels (_LayerNormBF16)."""
     if x.dtype == torch.bfloat16 and torch.is_autocast_enabled("cuda"):
         with torch.autocast("cuda", enabled=False):
-            return F.layer_norm(x, shape, w.to(x.dtype), b.to(x.dtype))
-    return F.layer_norm(x, shape, w, b)
+            wb, bb = w.to(x.dtype), b.to(x.dtype)
+            if _ln_native(x, wb, bb) and len(shape) == 1:
+                x2 = x if x.data_ptr() % 16 == 0 else x.clone()
+                return _LayerNormBF16.apply(x2, _aligned16(wb), _aligned16(bb), eps)
+            return F.layer_norm(x, shape, wb, bb, eps)
+    return F.layer_norm(x, shape, w, b, eps)
+
+
+class _SplitHeads(torch.autograd.Function):
+    """qkv [b*t, 3e] -> q, k, v [b, nh, t, hd] (strided views, as
+    `view(b, t, 3, nh, hd).permute(2, 0, 3, 1, 4)`).  The backward writes the
+    three head gradients straight into one [b, t, 3, nh, hd] buffer, which IS
+    the [b*t, 3e] gradient of qkv; autograd's unbind/permute/view backward
+    stacked them ([3, b, nh, t, hd]) and then copied that into the qkv
+    layout: a 97 us cat + a copy per block on a GPT-2 worker step.  libsdp
+    k_merge_heads interleaves the three in one pass whatever their (batch,
+    head, seq) strides (strided torch copies otherwise)."""
+
+    @staticmethod
+    def forward(ctx, qkv, b, t, nh, hd):
+        ctx.shape = (b, t, nh, hd)
+        q, k, v = qkv.view(b, t, 3, nh, hd).permute(2, 0, 3, 1, 4)
+        return q, k, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        b, t, nh, hd = ctx.shape
+        ref = next(x for x in (dq, dk, dv) if x is not None)
+        g = torch.empty((b, t, 3, nh, hd), dtype=ref.dtype, device=ref.device)
+        es = ref.element_size()
+        st = ref.stride()
+        if (all(x is not None and x.stride() == st and x.dtype == ref.dtype and x.data_ptr() % 16 == 0
+                for x in (dq, dk, dv))
+                and ref.is_cuda and st[3] == 1 and es in (2, 4) and hd * es % 16 == 0
+                and all(s_ * es % 16 == 0 for s_ in st[:3])):  # libsdp k_merge_heads
+            N.call("sdp_merge_heads", ptr(dq), ptr(dk), ptr(dv), b, t, nh, hd, es, st[0], st[1], st[2], ptr(g),
+                   stream_ptr(ref.device))
+            return g.view(b * t, 3 * nh * hd), None, None, None, None
+        for i, x in enumerate((dq, dk, dv)):
+            dst = g[:, :, i].transpose(1, 2)  # [b, nh, t, hd] view
+            if x is None:
+                dst.zero_()
+            else:
+                dst.copy_(x)
+        return g.view(b * t, 3 * nh * hd), None, None, None, None
+
+
+class _Linear(torch.autograd.Function):
+    """addmm(bias, x, w) (HF Conv1D: w is [in, out]) whose backward takes the
+    bias gradient as ones @ dy on cuBLAS instead of dy.sum(0): torch's
+    reduce kernel ran 19 us per [8192, <=3072] bf16 gradient, 4 per block."""
+
+    @staticmethod
+    def forward(ctx, bias, x, w):
+        ctx.save_for_backward(x, w)
+        return torch.addmm(bias, x, w)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w = ctx.saved_tensors
+        dx = dy @ w.t() if ctx.needs_input_grad[1] else None
+        dw = x.t() @ dy if ctx.needs_input_grad[2] else None
+        db = None
+        if ctx.needs_input_grad[0]:
+            ones = torch.ones((1, dy.shape[0]), dtype=dy.dtype, device=dy.device)
+            db = (ones @ dy).view(-1)
+        return db, dx, dw
+
+
+def _addmm(bias, x, w):
+    if x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and bias.dtype == torch.bfloat16:
+        return _Linear.apply(bias, x, w)
+    return torch.addmm(bias, x, w)
 
 
 class GPT2Small:
@@ -172,15 +291,15 @@ class GPT2Small:
                 continue
             p = f"h{i}"
             a = _layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
-            qkv = torch.addmm(params[f"{p}.attn.c_attn.b"], a.reshape(b * t, e), params[f"{p}.attn.c_attn.w"])
-            q, k, v = qkv.view(b, t, 3, nh, e // nh).permute(2, 0, 3, 1, 4)
+            qkv = _addmm(params[f"{p}.attn.c_attn.b"], a.reshape(b * t, e), params[f"{p}.attn.c_attn.w"])
+            q, k, v = _SplitHeads.apply(qkv, b, t, nh, e // nh)
             y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             y = y.transpose(1, 2).reshape(b * t, e)
-            y = torch.addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
+            y = _addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
             m = _layer_norm(h + y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
-            m = F.gelu(torch.addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
+            m = F.gelu(_addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
                        approximate="tanh")
-            m = torch.addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
+            m = _addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
             o = y + m
             if not live:
                 o = o * 0.0

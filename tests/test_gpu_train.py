@@ -182,3 +182,59 @@ def test_fused_lm_head_cross_entropy_matches_unfused(cuda):
         assert abs(fused.item() - plain.item()) <= tol * abs(plain.item())
         for a, b in zip(gf, gp):
             assert torch.allclose(a.double(), b.double(), rtol=tol, atol=tol * b.abs().max().item())
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 768), (5, 768), (300, 256), (1000, 512), (77, 1024)])
+def test_layer_norm_bf16_matches_fp32_reference(cuda, rows, cols):
+    """libsdp k_ln_fwd / k_ln_bwd (train._LayerNormBF16) against torch fp32
+    layer_norm of the same bf16 inputs: y and dx within bf16 rounding of the
+    fp32 result, dgamma / dbeta (sums over the rows) to 1e-2 relative; the
+    backward is deterministic (same bits on a second call)."""
+    import torch.nn.functional as F
+    from paper_2507_09029_b200 import train
+    g = torch.Generator(device=cuda)
+    g.manual_seed(rows + cols)
+    x = (torch.randn(rows, cols, generator=g, device=cuda) * 2 + 0.5).bfloat16()
+    w = (1 + 0.1 * torch.randn(cols, generator=g, device=cuda)).bfloat16()
+    b = (0.1 * torch.randn(cols, generator=g, device=cuda)).bfloat16()
+    dy = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    xs, ws, bs = (t.clone().requires_grad_(True) for t in (x, w, b))
+    y = train._LayerNormBF16.apply(xs, ws, bs, 1e-5)
+    y.backward(dy)
+    xr, wr, br = (t.float().requires_grad_(True) for t in (x, w, b))
+    yr = F.layer_norm(xr, (cols,), wr, br, 1e-5)
+    yr.backward(dy.float())
+    assert y.dtype == torch.bfloat16 and xs.grad.dtype == torch.bfloat16
+    tol = lambda r: 2 ** -7 * r.abs() + 1e-3  # noqa: E731  (one bf16 ulp of the fp32 value + slack)
+    assert (y.float() - yr).abs().le(tol(yr)).all()
+    assert (xs.grad.float() - xr.grad).abs().le(tol(xr.grad) + 1e-2 * xr.grad.abs().max()).all()
+    for got, ref in ((ws.grad, wr.grad), (bs.grad, br.grad)):
+        assert (got.float() - ref).abs().max() <= 1e-2 * ref.abs().max() + 1e-3
+    xs2, ws2, bs2 = (t.clone().requires_grad_(True) for t in (x, w, b))
+    train._LayerNormBF16.apply(xs2, ws2, bs2, 1e-5).backward(dy)
+    assert torch.equal(xs2.grad, xs.grad) and torch.equal(ws2.grad, ws.grad) and torch.equal(bs2.grad, bs.grad)
+
+
+@pytest.mark.parametrize("layout", ["bhtd", "bthd"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_split_heads_backward_merges_bit_exact(cuda, dtype, layout):
+    """train._SplitHeads: forward views equal the permute of qkv; backward
+    (libsdp k_merge_heads) equals autograd's gradient of the plain
+    view/permute bit for bit (a pure data movement)."""
+    from paper_2507_09029_b200 import train
+    b, t, nh, hd = 2, 37, 3, 64
+    g = torch.Generator(device=cuda)
+    g.manual_seed(3)
+    qkv = torch.randn(b * t, 3 * nh * hd, generator=g, device=cuda).to(dtype)
+    grads = [torch.randn(b, nh, t, hd, generator=g, device=cuda).to(dtype) for _ in range(3)]
+    if layout == "bthd":  # the SDPA backward's [b, t, nh, hd]-major gradients
+        grads = [x.transpose(1, 2).contiguous().transpose(1, 2) for x in grads]
+    a = qkv.clone().requires_grad_(True)
+    outs = train._SplitHeads.apply(a, b, t, nh, hd)
+    r = qkv.clone().requires_grad_(True)
+    refs = r.view(b, t, 3, nh, hd).permute(2, 0, 3, 1, 4)
+    for o, ref in zip(outs, refs):
+        assert torch.equal(o, ref)
+    torch.autograd.backward(outs, grads)
+    torch.autograd.backward(list(refs), grads)
+    assert torch.equal(a.grad, r.grad)
