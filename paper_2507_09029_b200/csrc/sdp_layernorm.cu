@@ -10,7 +10,8 @@
 //                  dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat));
 //                  every lane keeps its columns' dgamma / dbeta partial sums
 //                  in registers over the rows its warp visits, the CTA folds
-//                  its warps in shared memory and writes one partial row.
+//                  its warps (a fixed tree through shared memory) and writes
+//                  one partial row.
 //   k_ln_bwd_fold  sums the per-CTA partial rows in a fixed order
 //                  (deterministic, no atomics) and writes bf16 dgamma / dbeta.
 // HBM bytes per element: fwd 2 read + 2 write; bwd 4 read (x, dy) + 2 write.
@@ -107,8 +108,8 @@ __global__ void __launch_bounds__(kLnThreads, (V <= 3 ? 2 : 1)) k_ln_bwd(const _
                                                         const float* __restrict__ rstd,
                                                         __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
   constexpr int cols = 256 * V;
-  __shared__ float s_dg[cols];
-  __shared__ float s_db[cols];
+  __shared__ float s_dg[kLnWarps / 2][cols];
+  __shared__ float s_db[kLnWarps / 2][cols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // dgamma / dbeta partials in registers; gamma re-read per row (L1 hits) so
   // that two CTAs fit per SM (128 registers)
@@ -155,38 +156,59 @@ __global__ void __launch_bounds__(kLnThreads, (V <= 3 ? 2 : 1)) k_ln_bwd(const _
       dxr[32 * k + lane] = pack8(o);
     }
   }
-  // fold the warps' partials in warp order (deterministic), then one row out
-  for (int w = 0; w < kLnWarps; ++w) {
-    if (warp == w) {
+  // fold the 8 warps' partials as a fixed tree (4+4, 2+2, 1+1: deterministic,
+  // three barriers), then warp 0 writes the CTA's partial row
+#pragma unroll
+  for (int half = kLnWarps / 2; half >= 1; half >>= 1) {
+    if (warp >= half && warp < 2 * half) {
 #pragma unroll
       for (int k = 0; k < V; ++k)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int c = 256 * k + 8 * lane + i;
-          s_dg[c] = w ? s_dg[c] + dg[k][i] : dg[k][i];
-          s_db[c] = w ? s_db[c] + db[k][i] : db[k][i];
+          s_dg[warp - half][256 * k + 8 * lane + i] = dg[k][i];
+          s_db[warp - half][256 * k + 8 * lane + i] = db[k][i];
+        }
+    }
+    __syncthreads();
+    if (warp < half) {
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          dg[k][i] += s_dg[warp][256 * k + 8 * lane + i];
+          db[k][i] += s_db[warp][256 * k + 8 * lane + i];
         }
     }
     __syncthreads();
   }
-  float* out = part + static_cast<int64_t>(blockIdx.x) * 2 * cols;
-  for (int c = threadIdx.x; c < cols; c += kLnThreads) {
-    out[c] = s_dg[c];
-    out[cols + c] = s_db[c];
+  if (warp == 0) {
+    float4* out = reinterpret_cast<float4*>(part + static_cast<int64_t>(blockIdx.x) * 2 * cols);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int c4 = (256 * k + 8 * lane) / 4;
+      out[c4] = make_float4(dg[k][0], dg[k][1], dg[k][2], dg[k][3]);
+      out[c4 + 1] = make_float4(dg[k][4], dg[k][5], dg[k][6], dg[k][7]);
+      out[cols / 4 + c4] = make_float4(db[k][0], db[k][1], db[k][2], db[k][3]);
+      out[cols / 4 + c4 + 1] = make_float4(db[k][4], db[k][5], db[k][6], db[k][7]);
+    }
   }
 }
 
-// 32 columns per CTA; each of the 8 warps sums every 8th partial row (in
-// order), then the 8 slices are folded in warp order: deterministic
-__global__ void __launch_bounds__(256) k_ln_bwd_fold(const float* __restrict__ part, int parts, int cols,
-                                                     __nv_bfloat16* __restrict__ dgamma,
-                                                     __nv_bfloat16* __restrict__ dbeta) {
-  __shared__ float sa[8][32], sb[8][32];
+// 32 columns per CTA; each of the 32 warps sums every 32nd partial row (in
+// order, loads batched), then the 32 slices are folded in warp order:
+// deterministic
+constexpr int kFoldWarps = 32;
+
+__global__ void __launch_bounds__(32 * kFoldWarps) k_ln_bwd_fold(const float* __restrict__ part, int parts, int cols,
+                                                                 __nv_bfloat16* __restrict__ dgamma,
+                                                                 __nv_bfloat16* __restrict__ dbeta) {
+  __shared__ float sa[kFoldWarps][33], sb[kFoldWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
   if (c < cols) {
-    for (int p = warp; p < parts; p += 8) {
+#pragma unroll 4
+    for (int p = warp; p < parts; p += kFoldWarps) {
       a += part[static_cast<int64_t>(p) * 2 * cols + c];
       b += part[static_cast<int64_t>(p) * 2 * cols + cols + c];
     }
@@ -195,8 +217,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd_fold(const float* __restrict__ p
   sb[warp][lane] = b;
   __syncthreads();
   if (warp == 0 && c < cols) {
-#pragma unroll
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < kFoldWarps; ++w) {
       a += sa[w][lane];
       b += sb[w][lane];
     }
@@ -281,7 +302,7 @@ int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, in
   } else {
     SDP_CUDA_CHECK(cudaMemsetAsync(scratch, 0, sizeof(float) * 2 * cols * parts, s));
   }
-  k_ln_bwd_fold<<<(cols + 31) / 32, 256, 0, s>>>(scratch, parts, cols, static_cast<__nv_bfloat16*>(dgamma_bf16),
+  k_ln_bwd_fold<<<(cols + 31) / 32, 32 * kFoldWarps, 0, s>>>(scratch, parts, cols, static_cast<__nv_bfloat16*>(dgamma_bf16),
                                                    static_cast<__nv_bfloat16*>(dbeta_bf16));
   SDP_LAUNCH_CHECK();
   return SDP_OK;

@@ -140,6 +140,9 @@ class ResNet18Cifar:
         return F.linear(h.mean(dim=(2, 3)), cp["fc.w"], cp["fc.b"])
 
 
+_LN_PARTS: dict = {}
+
+
 class _LayerNormBF16(torch.autograd.Function):
     """Row LayerNorm of bf16 activations on libsdp's k_ln_fwd / k_ln_bwd (one
     warp per row, fp32 statistics; the weight / bias gradients reduced per CTA
@@ -167,7 +170,10 @@ class _LayerNormBF16(torch.autograd.Function):
         dy = dy.contiguous()
         if dy.data_ptr() % 16:
             dy = dy.clone()
-        parts = N.lib().sdp_layer_norm_bwd_parts(rows, cols)
+        key = (rows, cols, x.device)
+        parts = _LN_PARTS.get(key)
+        if parts is None:
+            parts = _LN_PARTS[key] = N.lib().sdp_layer_norm_bwd_parts(rows, cols)
         scratch = torch.empty(2 * cols * parts, dtype=torch.float32, device=x.device)
         dx = torch.empty_like(x)
         dw = torch.empty(cols, dtype=torch.bfloat16, device=x.device)
