@@ -588,8 +588,24 @@ class SubnetTrainer:
             self._static_loss = self._step_eager(self._static, cache=False)
         self._graph_lr = self.lr
 
+    def _step_params(self) -> dict:
+        """Leaf parameters of one step's block-strategy workers: views of the
+        bf16 copy, with the 4-D convolution weights made channels-last ONCE
+        per step (cuDNN's NHWC kernels would otherwise convert every weight
+        for every worker).  The leaves are shared by the N workers;
+        torch.autograd.grad returns each worker's gradients separately."""
+        topo = self.model.topology
+        src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
+        out = {}
+        for k, v in param_views(topo, src).items():
+            if self.autocast and v.dim() == 4 and v.is_cuda:
+                v = v.contiguous(memory_format=torch.channels_last)
+            out[k] = v.requires_grad_(True)
+        return out
+
     def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
         topo = self.model.topology
+        step_params = None
         losses = []
         for w, (x, y) in enumerate(batches):
             if self.compact:
@@ -616,8 +632,9 @@ class SubnetTrainer:
             # every parameter is a leaf view and its gradient lands directly
             # in its slot of the fp32 replica (one multi-tensor copy, no [d]
             # concatenation); parameters of dropped blocks keep their zeros
-            src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
-            params = {k: v.requires_grad_(True) for k, v in param_views(topo, src).items()}
+            if step_params is None:  # once per step: every worker reads the same bf16 copy
+                step_params = self._step_params()
+            params = step_params
             with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                 logits = self.model.arch.forward(params, x, self.views[w])
                 loss = self.loss_fn(logits, y)
