@@ -27,6 +27,7 @@ namespace sdp {
 
 constexpr int kGnThreads = 256;
 constexpr int kGnMaxC = 1024;  // channels per group handled by the shared partials
+constexpr int kGnU = 8;        // pixels per thread per round in the backward (loads in flight)
 
 template <int NT>
 __device__ __forceinline__ void block_sum2(float& a, float& b) {
@@ -245,6 +246,71 @@ k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ 
   // the thread's channel (vector) is fixed when the vectors per pixel divide
   // the CTA width: per-channel partials stay in registers
   const bool fixed = (kGnThreads % cv) == 0;
+  if (!vec && fixed) {
+    // one channel per thread, kGnU pixels per round with all their loads in
+    // flight (the element-at-a-time loop kept ~6 KB per SM in flight: latency
+    // bound), gamma read once
+    const int kv = threadIdx.x % cv, pstep = kGnThreads / cv, npix = t.p1 - t.p0;
+    const float gch = gamma[t.c0 + kv];
+    const __nv_bfloat16* xb = x + t.base + kv;
+    const __nv_bfloat16* yb = y + t.base + kv;
+    const __nv_bfloat16* db = dy + t.base + kv;
+    float s1 = 0.f, s2 = 0.f, pgs = 0.f, pbs = 0.f;
+    for (int p0 = threadIdx.x / cv; p0 < npix; p0 += kGnU * pstep) {
+      float vx[kGnU], vd[kGnU], vy[kGnU];
+#pragma unroll
+      for (int u = 0; u < kGnU; ++u) {
+        const int pix = p0 + u * pstep;
+        const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
+        vx[u] = __bfloat162float(xb[o]);
+        vd[u] = pix < npix ? __bfloat162float(db[o]) : 0.f;
+        vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kGnU; ++u) {
+        const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
+        const float xh = (vx[u] - mean) * rstd;
+        s1 += dz * gch;
+        s2 += dz * gch * xh;
+        pgs += dz * xh;
+        pbs += dz;
+      }
+    }
+    if (threadIdx.x < npix * cv) {
+      atomicAdd(&s_dg[kv], pgs);
+      atomicAdd(&s_db[kv], pbs);
+    }
+    block_sum2<kGnThreads>(s1, s2);
+    const float inv_n = 1.f / (static_cast<float>(hw) * t.cg);
+    cluster_sum2(cl, &s_part, s1, s2);
+    s1 *= inv_n;
+    s2 *= inv_n;
+    __nv_bfloat16* dxb = dx + t.base + kv;
+    for (int p0 = threadIdx.x / cv; p0 < npix; p0 += kGnU * pstep) {
+      float vx[kGnU], vd[kGnU], vy[kGnU];
+#pragma unroll
+      for (int u = 0; u < kGnU; ++u) {
+        const int pix = p0 + u * pstep;
+        const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
+        vx[u] = __bfloat162float(xb[o]);
+        vd[u] = __bfloat162float(db[o]);
+        vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kGnU; ++u) {
+        const int pix = p0 + u * pstep;
+        const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
+        const float xh = (vx[u] - mean) * rstd;
+        if (pix < npix) dxb[static_cast<int64_t>(pix) * c] = __float2bfloat16_rn(rstd * (dz * gch - s1 - xh * s2));
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < t.cg; k += kGnThreads) {
+      atomicAdd(&dgamma[t.c0 + k], s_dg[k]);
+      atomicAdd(&dbeta[t.c0 + k], s_db[k]);
+    }
+    return;
+  }
   float s1 = 0.f, s2 = 0.f, pg[8], pb[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) pg[k] = pb[k] = 0.f;
