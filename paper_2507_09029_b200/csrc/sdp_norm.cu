@@ -60,12 +60,17 @@ __device__ __forceinline__ void block_sum2(float& a, float& b) {
 constexpr int kGnCluster = 8;
 
 // CTAs per (sample, group): enough that each has >= 2048 elements of work,
-// a power of two <= kGnCluster (small late-layer slabs: fewer CTAs, fewer
-// cluster barriers)
+// a power of two <= kGnPartsCap (small late-layer slabs: fewer CTAs, fewer
+// cluster barriers).  Same-box A/B of graphed ResNet-18 steps (batch 64, 2
+// groups): cap 8 / 4 / 2 / 1 -> C2 9.5 / 9.1 / 9.3 / 10.1 ms, DP 12.6 / 12.0
+// / 12.2 / 13.5 ms GPU time; 8-CTA clusters of the 32x32 layers ran in two
+// waves of co-scheduled clusters.
+constexpr int kGnPartsCap = 4;
+
 static int gn_parts(int hw, int max_cg) {
   const int64_t slab = static_cast<int64_t>(hw) * max_cg;
   int parts = 1;
-  while (parts < kGnCluster && slab / (2 * parts) >= 2048) parts *= 2;
+  while (parts < kGnPartsCap && slab / (2 * parts) >= 2048) parts *= 2;
   return parts;
 }
 
