@@ -362,6 +362,23 @@ int sdp_merge_heads(const void* dq, const void* dk, const void* dv, int64_t batc
                     int head_dim, int elem_bytes, int64_t stride_batch, int64_t stride_head, int64_t stride_seq,
                     void* out, void* stream);
 
+/* Convolution-weight gradients, channels-last bf16 -> reference-layout fp32
+ * (train.SubnetTrainer._store_grads): for each descriptor, the weight at
+ * element `offset` of both buffers is [out, kernel_elems, in] (OHWI) in
+ * `src_bf16` and is written [out, in, kernel_elems] (OIHW) into `dst`.
+ * in_channels * kernel_elems <= sdp_conv_grad_max_block(). */
+typedef struct {
+  int64_t offset;
+  int32_t out_channels;
+  int32_t in_channels;
+  int32_t kernel_elems;
+  int32_t pad_;
+} sdp_conv_grad_desc;
+
+int sdp_conv_grads_to_oihw(const sdp_conv_grad_desc* descs, int n_desc, int max_out_channels, const void* src_bf16,
+                           float* dst, void* stream);
+int sdp_conv_grad_max_block(void);
+
 /* ------------------------------------------------------------------------ */
 /* Fused LM-head cross-entropy rows (C4 training step, train.lm_loss)        */
 /* ------------------------------------------------------------------------ */

@@ -238,3 +238,33 @@ def test_split_heads_backward_merges_bit_exact(cuda, dtype, layout):
     torch.autograd.backward(outs, grads)
     torch.autograd.backward(list(refs), grads)
     assert torch.equal(a.grad, r.grad)
+
+
+def test_store_grads_bf16_channels_last_matches_slot_copy(cuda):
+    """SubnetTrainer._store_grads: bf16 gradients (conv weights channels-last,
+    as cuDNN's NHWC kernels return them) land in the fp32 replica exactly as
+    a per-parameter g.float() copy into the reference-layout slots would put
+    them (libsdp k_conv_grad_oihw + per-run casts); dropped parameters keep
+    their zeros."""
+    from paper_2507_09029_b200 import masking, train
+    model = train.build_resnet18(cuda)
+    a = masking.build_assignment(model.topology, "block", 8, 4, seed=1)
+    tr = train.SubnetTrainer(model, a, lr=0.02)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    for w in (0, 5):
+        names = tr._live_params(w)
+        spec = {p.name: p for p in model.topology.params}
+        gs = []
+        for k in names:
+            t = torch.randn(spec[k].shape, generator=g, device=cuda).bfloat16()
+            if t.dim() == 4:
+                t = t.contiguous(memory_format=torch.channels_last)
+            gs.append(t)
+        tr.grads[w].zero_()
+        tr._store_grads(w, names, gs)
+        want = torch.zeros_like(tr.grads[w])
+        slots = train.param_views(model.topology, want)
+        for k, t in zip(names, gs):
+            slots[k].copy_(t.float())
+        assert torch.equal(tr.grads[w], want), w
