@@ -227,12 +227,48 @@ k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __re
   }
 }
 
+// Optional fused epilogue of the backward: dgamma / dbeta accumulate in a
+// persistent fp32 scratch (zero between calls) and the LAST CTA to finish
+// (a global counter) writes them in the parameter's dtype, re-zeroes the
+// scratch and resets the counter -- no fill and no cast kernel per call.
+struct GnOut {
+  void* g;                 // dgamma output (bf16 or fp32), or null: plain fp32 accumulation
+  void* b;                 // dbeta output
+  bool bf16;
+  unsigned int* counter;   // CTAs finished (zero between calls)
+  int channels;
+};
+
+__device__ __forceinline__ void gn_finish(const GnOut& out, float* acc_g, float* acc_b) {
+  if (!out.g) return;
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(out.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = threadIdx.x; k < out.channels; k += kGnThreads) {
+    const float a = __ldcg(acc_g + k), b = __ldcg(acc_b + k);
+    if (out.bf16) {
+      static_cast<__nv_bfloat16*>(out.g)[k] = __float2bfloat16_rn(a);
+      static_cast<__nv_bfloat16*>(out.b)[k] = __float2bfloat16_rn(b);
+    } else {
+      static_cast<float*>(out.g)[k] = a;
+      static_cast<float*>(out.b)[k] = b;
+    }
+    acc_g[k] = 0.f;
+    acc_b[k] = 0.f;
+  }
+  if (threadIdx.x == 0) *out.counter = 0u;
+}
+
 template <bool RELU, bool VEC>
 __global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
          const __nv_bfloat16* __restrict__ dy, int hw, int c, const int32_t* __restrict__ gs, int groups,
          const Affine gamma, const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-         __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta) {
+         __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, const GnOut out) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ float s_dg[kGnMaxC], s_db[kGnMaxC];
   __shared__ float2 s_part;
@@ -314,6 +350,7 @@ k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ 
       atomicAdd(&dgamma[t.c0 + k], s_dg[k]);
       atomicAdd(&dbeta[t.c0 + k], s_db[k]);
     }
+    gn_finish(out, dgamma, dbeta);
     return;
   }
   float s1 = 0.f, s2 = 0.f, pg[8], pb[8];
@@ -402,6 +439,7 @@ k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ 
     atomicAdd(&dgamma[t.c0 + k], s_dg[k]);
     atomicAdd(&dbeta[t.c0 + k], s_db[k]);
   }
+  gn_finish(out, dgamma, dbeta);
 }
 
 static int check_groups(int b, int hw, int c, int groups) {
@@ -443,10 +481,35 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
   return SDP_OK;
 }
 
+static int gn_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw, int channels,
+                  const int32_t* group_starts, int groups, int max_group_channels, const void* gamma,
+                  const float* mean, const float* rstd, int flags, void* dx_bf16, float* dgamma, float* dbeta,
+                  const GnOut out, void* stream);
+
 int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
                        int channels, const int32_t* group_starts, int groups, int max_group_channels,
                        const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
                        float* dgamma, float* dbeta, void* stream) {
+  return gn_bwd(x_bf16, y_bf16, dy_bf16, batch, hw, channels, group_starts, groups, max_group_channels, gamma, mean,
+                rstd, flags, dx_bf16, dgamma, dbeta, GnOut{nullptr, nullptr, false, nullptr, 0}, stream);
+}
+
+int sdp_group_norm_bwd_fused(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
+                             int channels, const int32_t* group_starts, int groups, int max_group_channels,
+                             const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
+                             void* dgamma_out, void* dbeta_out, float* scratch, unsigned int* counter,
+                             void* stream) {
+  if (!dgamma_out || !dbeta_out || !scratch || !counter) return set_error(SDP_ERR_USAGE, "null device pointer");
+  if (batch == 0) return set_error(SDP_ERR_USAGE, "fused group-norm backward needs batch > 0");
+  const GnOut out{dgamma_out, dbeta_out, (flags & SDP_GN_AFFINE_BF16) != 0, counter, channels};
+  return gn_bwd(x_bf16, y_bf16, dy_bf16, batch, hw, channels, group_starts, groups, max_group_channels, gamma, mean,
+                rstd, flags, dx_bf16, scratch, scratch + channels, out, stream);
+}
+
+static int gn_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw, int channels,
+                  const int32_t* group_starts, int groups, int max_group_channels, const void* gamma,
+                  const float* mean, const float* rstd, int flags, void* dx_bf16, float* dgamma, float* dbeta,
+                  const GnOut out, void* stream) {
   const bool relu = flags & SDP_GN_RELU;
   const Affine ga{gamma, (flags & SDP_GN_AFFINE_BF16) != 0};
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
@@ -466,7 +529,7 @@ int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf
   const bool vec = false;
 #define SDP_GN_BWD(R, V)                                                                                 \
   SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<R, V>, grid, parts, s, xb, yb, db, hw, channels, group_starts,  \
-                                  groups, ga, mean, rstd, dxb, dgamma, dbeta))
+                                  groups, ga, mean, rstd, dxb, dgamma, dbeta, out))
   if (relu) {
     if (vec) SDP_GN_BWD(true, true); else SDP_GN_BWD(true, false);
   } else {
