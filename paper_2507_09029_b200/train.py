@@ -25,7 +25,7 @@ import torch.nn.functional as F
 from . import _native as N
 from . import engine, masking, zoo
 from ._device import ptr, stream_ptr
-from .models import group_norm
+from .models import _channels_last_bf16, group_norm
 from .topology import GlobalModel
 
 
@@ -126,10 +126,13 @@ class ResNet18Cifar:
             a1 = sub.channels(f"{p}.conv1", planes)
             a2 = sub.channels(f"{p}.conv2", planes)
             o = F.conv2d(h, cp[f"{p}.conv1.w"], stride=stride, padding=1)
-            o = ragged_group_norm(o, a1 // gsize, g, cp[f"{p}.gn1.gamma"], cp[f"{p}.gn1.beta"],
+            # the channels-last kernel needs only the per-group counts (the
+            # channel -> group map would be two index divisions per block)
+            fast = _channels_last_bf16(o)
+            o = ragged_group_norm(o, None if fast else a1 // gsize, g, cp[f"{p}.gn1.gamma"], cp[f"{p}.gn1.beta"],
                                   counts=sub.group_counts(f"{p}.conv1", planes, g), relu=True)
             o = F.conv2d(o, cp[f"{p}.conv2.w"], padding=1)
-            o = ragged_group_norm(o, a2 // gsize, g, cp[f"{p}.gn2.gamma"], cp[f"{p}.gn2.beta"],
+            o = ragged_group_norm(o, None if fast else a2 // gsize, g, cp[f"{p}.gn2.gamma"], cp[f"{p}.gn2.beta"],
                                   counts=sub.group_counts(f"{p}.conv2", planes, g))
             if down:
                 sc = downsample(h, cp[f"{p}.down.w"], stride)
@@ -608,6 +611,9 @@ class SubnetTrainer:
         step_params = None
         losses = []
         for w, (x, y) in enumerate(batches):
+            if self.compact and self.autocast:
+                losses.append(self._compact_step_bf16(w, x, y, cache))
+                continue
             if self.compact:
                 sub = self.subs[w]
                 # the worker trains on the bf16 copy the previous sync wrote
@@ -645,6 +651,72 @@ class SubnetTrainer:
             losses.append(loss.detach())
         self._sync()
         return torch.stack(losses).mean()
+
+    def _compact_step_bf16(self, w: int, x, y, cache: bool) -> torch.Tensor:
+        """Width-wise worker step under bf16 autocast: the compact parameters
+        are per-parameter leaves (conv weights made channels-last once, as
+        cuDNN's NHWC kernels want them), so the backward returns per-parameter
+        gradients instead of one concatenation; they reach the fp32 replica
+        through a bf16 compact scratch (one fused copy), one bf16 -> fp32 cast
+        of the whole compact vector, one libsdp launch that puts the conv
+        weights back in OIHW order, and the sync-space transfer."""
+        sub = self.subs[w]
+        cvec = self.transfers[w].to_compact(self.theta_bf16) if self.slayout else sub.gather(self.theta_bf16)
+        views = sub.views(cvec)
+        params = {}
+        for k, v in views.items():
+            if v.dim() == 4 and v.numel() > 0:
+                v = v.contiguous(memory_format=torch.channels_last)
+            params[k] = v.requires_grad_(True)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=True, cache_enabled=cache):
+            logits = self.model.arch.forward_compact(params, x, sub)
+            loss = self.loss_fn(logits, y)
+        del logits
+        names = [k for k, v in views.items() if v.numel() > 0]
+        gs = torch.autograd.grad(loss, [params[k] for k in names], allow_unused=True)
+        n = sub.compact_total
+        if getattr(self, "_cbuf", None) is None:
+            m = max(max(1, s_.compact_total) for s_ in self.subs)
+            self._cbuf = torch.empty(m, dtype=torch.bfloat16, device=cvec.device)
+            self._cbuf32 = torch.empty(m, dtype=torch.float32, device=cvec.device)
+            self._cg_max = N.lib().sdp_conv_grad_max_block()
+        slots = sub.views(self._cbuf)
+        dst, src, conv = [], [], []
+        for k, g in zip(names, gs):
+            slot = slots[k]
+            if g is None:
+                slot.zero_()
+                continue
+            if g.dim() == 4 and not g.is_contiguous() and g.is_contiguous(memory_format=torch.channels_last) \
+                    and g.shape[1] * g.shape[2] * g.shape[3] <= self._cg_max:
+                o, i, kh, kw = g.shape
+                slot = self._cbuf.as_strided((o, i, kh, kw), (i * kh * kw, 1, kw * i, i), slot.storage_offset())
+                conv.append(k)
+            dst.append(slot)
+            src.append(g)
+        torch._foreach_copy_(dst, src)
+        g32 = self._cbuf32[:max(1, n)]
+        g32.copy_(self._cbuf[:max(1, n)])  # conv slots are OHWI here; rewritten below
+        if conv:
+            key = (w, tuple(conv))
+            if not hasattr(self, "_ccdescs"):
+                self._ccdescs = {}
+            if key not in self._ccdescs:
+                dt = np.dtype([("offset", "<i8"), ("out", "<i4"), ("inp", "<i4"), ("k", "<i4"), ("pad", "<i4")])
+                arr = np.zeros(len(conv), dtype=dt)
+                for j, k in enumerate(conv):
+                    sh = slots[k].shape
+                    arr[j] = (slots[k].storage_offset(), sh[0], sh[1], sh[2] * sh[3], 0)
+                self._ccdescs[key] = (torch.from_numpy(arr.view(np.uint8).copy()).to(cvec.device),
+                                      int(arr["out"].max()))
+            descs, max_o = self._ccdescs[key]
+            N.call("sdp_conv_grads_to_oihw", ptr(descs), len(conv), max_o, ptr(self._cbuf), ptr(g32),
+                   stream_ptr(cvec.device))
+        if self.slayout:
+            self.transfers[w].from_compact(g32, self.grads[w])
+        else:
+            sub.scatter(g32, self.grads[w])
+        return loss.detach()
 
     def _store_grads(self, w: int, names: list, gs) -> None:
         """Parameter gradients -> worker w's fp32 replica.  bf16 gradients go

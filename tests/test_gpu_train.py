@@ -268,3 +268,35 @@ def test_store_grads_bf16_channels_last_matches_slot_copy(cuda):
         for k, t in zip(names, gs):
             slots[k].copy_(t.float())
         assert torch.equal(tr.grads[w], want), w
+
+
+def test_widthwise_bf16_per_parameter_leaves_match_single_leaf(cuda):
+    """The width-wise bf16 step's per-parameter compact leaves (channels-last
+    conv weights, fused gradient store + k_conv_grad_oihw) give the worker's
+    fp32 sync-space gradient bit for bit as the single compact leaf whose
+    gradient is one concatenation (deterministic cuDNN)."""
+    from paper_2507_09029_b200 import masking, train
+    prev = torch.backends.cudnn.deterministic
+    torch.backends.cudnn.deterministic = True
+    try:
+        model = train.build_resnet18(cuda, seed=3)
+        a = masking.build_assignment(model.topology, "neuron", 8, 4, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=0.02, sync_layout=True)
+        g = torch.Generator(device=cuda)
+        g.manual_seed(5)
+        x = torch.randn(16, 3, 32, 32, generator=g, device=cuda)
+        y = torch.randint(0, 10, (16,), generator=g, device=cuda)
+        for w in (0, 3):
+            tr.grads[w].zero_()
+            tr._compact_step_bf16(w, x, y, cache=True)
+            got = tr.grads[w].clone()
+            sub = tr.subs[w]
+            leaf = tr.transfers[w].to_compact(tr.theta_bf16).requires_grad_(True)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = tr.loss_fn(model.arch.forward_compact(sub.views(leaf), x, sub), y)
+            (gl,) = torch.autograd.grad(loss, leaf)
+            want = torch.zeros_like(tr.grads[w])
+            tr.transfers[w].from_compact(gl.float(), want)
+            assert torch.equal(got, want), (w, (got - want).abs().max().item())
+    finally:
+        torch.backends.cudnn.deterministic = prev
