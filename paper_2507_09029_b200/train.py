@@ -482,56 +482,10 @@ class StepStats:
     loss_mean: float
 
 
-class SubnetTrainer:
-    """N logical workers co-resident on one GPU (the reference's in-process
-    structure, engine.py:180-245) with the owner-subset sync fused into the
-    optimizer step.
-
-    theta / velocity: canonical fp32 master state (engine.py:223 updates one
-    shared theta); theta_bf16: the training copy every worker's forward reads,
-    written by the sync kernel's epilogue."""
-
-    def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
-                 autocast: bool = True, compact: bool | None = None, loss_fn=None,
-                 sync_layout: bool = False, graphed: bool = False):
-        """graphed: capture the whole protocol step (N worker fwd/bwd, gather /
-        scatter, the fused sync) in one CUDA graph and replay it -- the eager
-        step is host-bound (thousands of small launches), see step()."""
-        self.model = model
-        self.graphed = graphed
-        self._graph = None
-        self.assignment = assignment
-        self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
-        self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
-        # width-wise (neuron) workers run their compact subnetwork: gather ->
-        # dense compact fwd/bwd -> scatter into the worker's flat gradient
-        self.compact = assignment.strategy == "neuron" if compact is None else compact
-        if self.compact:
-            from .models import SubnetLayout
-            self.subs = [SubnetLayout(assignment, w) for w in range(assignment.n_workers)]
-        d = model.topology.total
-        dev = model.theta.device
-        # sync_layout: keep theta / velocity / gradient replicas permuted into the
-        # window-class-major layout (layout.py) so the sync sees uniform tiles
-        self.slayout = None
-        if sync_layout and self.compact:
-            from .layout import SyncLayout, WorkerTransfer
-            self.slayout = SyncLayout(assignment)
-            self.transfers = [WorkerTransfer(self.slayout, s) for s in self.subs]
-            model.theta = self.slayout.to_sync(model.theta)
-        self.velocity = torch.zeros(d, device=dev)
-        self.theta_bf16 = model.theta.to(torch.bfloat16)
-        self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
-        self.lr, self.momentum, self.autocast = lr, momentum, autocast
-        self.plan = self.slayout.plan() if self.slayout else assignment.sync_plan()
-        self._prep = None
-
-    def _live_params(self, w: int) -> list:
-        if not hasattr(self, "_live"):
-            self._live = {}
-        if w not in self._live:
-            self._live[w] = live_params(self.model.topology, self.views[w])
-        return self._live[w]
+class _GradStore:
+    """bf16 training-step plumbing shared by SubnetTrainer and PeerTrainer:
+    gradients into the fp32 replicas (`self.grads[w]`) with fused copies and
+    libsdp's conv-weight OIHW cast, and the width-wise compact step."""
 
     def _grad_slots(self, w: int) -> dict:
         if not hasattr(self, "_slots"):
@@ -540,119 +494,7 @@ class SubnetTrainer:
             self._slots[w] = param_views(self.model.topology, self.grads[w])
         return self._slots[w]
 
-    def theta(self) -> torch.Tensor:
-        """theta in the reference's flat layout."""
-        return self.slayout.from_sync(self.model.theta) if self.slayout else self.model.theta
-
-    def _sync(self):
-        if self._prep is None:
-            self._prep = engine.PreparedSync(
-                self.grads, self.assignment, writeback=False, plan=self.plan,
-                nesterov={"theta": self.model.theta, "velocity": self.velocity, "lr": self.lr,
-                          "momentum": self.momentum, "theta_bf16": self.theta_bf16})
-        self._prep.args.lr = float(self.lr)
-        self._prep.launch()
-
-    def step(self, batches) -> torch.Tensor:
-        """batches: list of N (x, y) device tensors; returns the mean loss (device).
-
-        graphed: the first call (and any call after `lr` changed) captures the
-        step into a CUDA graph -- after warm-up steps on a side stream whose
-        effect on theta / velocity is rolled back -- and every call copies the
-        batches into the graph's static inputs and replays it.  Same math, same
-        kernels, same order as the eager step."""
-        if not self.graphed:
-            return self._step_eager(batches)
-        if self._graph is None or self._graph_lr != self.lr:
-            self._capture(batches)
-        for (sx, sy), (x, y) in zip(self._static, batches):
-            if sx.data_ptr() != x.data_ptr():
-                sx.copy_(x)
-            if sy.data_ptr() != y.data_ptr():
-                sy.copy_(y)
-        self._graph.replay()
-        return self._static_loss
-
-    def _capture(self, batches, warmup: int = 2) -> None:
-        self._static = [(x.clone(), y.clone()) for x, y in batches]
-        state = [self.model.theta, self.velocity, self.theta_bf16]
-        saved = [t.clone() for t in state]
-        side = torch.cuda.Stream(self.model.theta.device)
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):  # autograd / cuDNN warm-up outside the capture
-            for _ in range(warmup):
-                self._step_eager(self._static, cache=False)
-        torch.cuda.current_stream().wait_stream(side)
-        for t, v in zip(state, saved):  # the warm-up steps never happened
-            t.copy_(v)
-        del saved
-        self._graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self._graph):
-            self._static_loss = self._step_eager(self._static, cache=False)
-        self._graph_lr = self.lr
-
-    def _step_params(self) -> dict:
-        """Leaf parameters of one step's block-strategy workers: views of the
-        bf16 copy, with the 4-D convolution weights made channels-last ONCE
-        per step (cuDNN's NHWC kernels would otherwise convert every weight
-        for every worker).  The leaves are shared by the N workers;
-        torch.autograd.grad returns each worker's gradients separately."""
-        topo = self.model.topology
-        src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
-        out = {}
-        for k, v in param_views(topo, src).items():
-            if self.autocast and v.dim() == 4 and v.is_cuda:
-                v = v.contiguous(memory_format=torch.channels_last)
-            out[k] = v.requires_grad_(True)
-        return out
-
-    def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
-        topo = self.model.topology
-        step_params = None
-        losses = []
-        for w, (x, y) in enumerate(batches):
-            if self.compact and self.autocast:
-                losses.append(self._compact_step_bf16(w, x, y, cache))
-                continue
-            if self.compact:
-                sub = self.subs[w]
-                # the worker trains on the bf16 copy the previous sync wrote
-                src = self.theta_bf16 if self.autocast else self.model.theta
-                if self.slayout:  # the worker's blocks of the permuted theta
-                    leaf = self.transfers[w].to_compact(src).requires_grad_(True)
-                else:
-                    leaf = sub.gather(src).requires_grad_(True)  # sdp_gather_slices
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
-                    logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
-                    loss = self.loss_fn(logits, y)
-                del logits
-                (g,) = torch.autograd.grad(loss, leaf)
-                g = g.float()  # fp32 gradient replica (the sync accumulates in fp32)
-                if self.slayout:
-                    self.transfers[w].from_compact(g, self.grads[w])
-                else:
-                    sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
-                losses.append(loss.detach())
-                continue
-            # the worker trains on the bf16 weights the previous sync wrote;
-            # every parameter is a leaf view and its gradient lands directly
-            # in its slot of the fp32 replica (one multi-tensor copy, no [d]
-            # concatenation); parameters of dropped blocks keep their zeros
-            if step_params is None:  # once per step: every worker reads the same bf16 copy
-                step_params = self._step_params()
-            params = step_params
-            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
-                logits = self.model.arch.forward(params, x, self.views[w])
-                loss = self.loss_fn(logits, y)
-            del logits
-            names = self._live_params(w)
-            gs = torch.autograd.grad(loss, [params[k] for k in names])
-            self._store_grads(w, names, gs)
-            losses.append(loss.detach())
-        self._sync()
-        return torch.stack(losses).mean()
-
-    def _compact_step_bf16(self, w: int, x, y, cache: bool) -> torch.Tensor:
+    def _compact_step_bf16(self, w: int, x, y, cache: bool, src: torch.Tensor | None = None) -> torch.Tensor:
         """Width-wise worker step under bf16 autocast: the compact parameters
         are per-parameter leaves (conv weights made channels-last once, as
         cuDNN's NHWC kernels want them), so the backward returns per-parameter
@@ -661,7 +503,8 @@ class SubnetTrainer:
         of the whole compact vector, one libsdp launch that puts the conv
         weights back in OIHW order, and the sync-space transfer."""
         sub = self.subs[w]
-        cvec = self.transfers[w].to_compact(self.theta_bf16) if self.slayout else sub.gather(self.theta_bf16)
+        src = self.theta_bf16 if src is None else src
+        cvec = self.transfers[w].to_compact(src) if self.slayout else sub.gather(src)
         views = sub.views(cvec)
         params = {}
         for k, v in views.items():
@@ -676,7 +519,8 @@ class SubnetTrainer:
         gs = torch.autograd.grad(loss, [params[k] for k in names], allow_unused=True)
         n = sub.compact_total
         if getattr(self, "_cbuf", None) is None:
-            m = max(max(1, s_.compact_total) for s_ in self.subs)
+            subs = self.subs.values() if isinstance(self.subs, dict) else self.subs
+            m = max(max(1, s_.compact_total) for s_ in subs)
             self._cbuf = torch.empty(m, dtype=torch.bfloat16, device=cvec.device)
             self._cbuf32 = torch.empty(m, dtype=torch.float32, device=cvec.device)
             self._cg_max = N.lib().sdp_conv_grad_max_block()
@@ -790,7 +634,170 @@ class SubnetTrainer:
         return self._runs[w]
 
 
-class PeerTrainer:
+class SubnetTrainer(_GradStore):
+    """N logical workers co-resident on one GPU (the reference's in-process
+    structure, engine.py:180-245) with the owner-subset sync fused into the
+    optimizer step.
+
+    theta / velocity: canonical fp32 master state (engine.py:223 updates one
+    shared theta); theta_bf16: the training copy every worker's forward reads,
+    written by the sync kernel's epilogue."""
+
+    def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
+                 autocast: bool = True, compact: bool | None = None, loss_fn=None,
+                 sync_layout: bool = False, graphed: bool = False):
+        """graphed: capture the whole protocol step (N worker fwd/bwd, gather /
+        scatter, the fused sync) in one CUDA graph and replay it -- the eager
+        step is host-bound (thousands of small launches), see step()."""
+        self.model = model
+        self.graphed = graphed
+        self._graph = None
+        self.assignment = assignment
+        self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
+        self.views = [assignment.worker_view(w) for w in range(assignment.n_workers)]
+        # width-wise (neuron) workers run their compact subnetwork: gather ->
+        # dense compact fwd/bwd -> scatter into the worker's flat gradient
+        self.compact = assignment.strategy == "neuron" if compact is None else compact
+        if self.compact:
+            from .models import SubnetLayout
+            self.subs = [SubnetLayout(assignment, w) for w in range(assignment.n_workers)]
+        d = model.topology.total
+        dev = model.theta.device
+        # sync_layout: keep theta / velocity / gradient replicas permuted into the
+        # window-class-major layout (layout.py) so the sync sees uniform tiles
+        self.slayout = None
+        if sync_layout and self.compact:
+            from .layout import SyncLayout, WorkerTransfer
+            self.slayout = SyncLayout(assignment)
+            self.transfers = [WorkerTransfer(self.slayout, s) for s in self.subs]
+            model.theta = self.slayout.to_sync(model.theta)
+        self.velocity = torch.zeros(d, device=dev)
+        self.theta_bf16 = model.theta.to(torch.bfloat16)
+        self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
+        self.lr, self.momentum, self.autocast = lr, momentum, autocast
+        self.plan = self.slayout.plan() if self.slayout else assignment.sync_plan()
+        self._prep = None
+
+    def _live_params(self, w: int) -> list:
+        if not hasattr(self, "_live"):
+            self._live = {}
+        if w not in self._live:
+            self._live[w] = live_params(self.model.topology, self.views[w])
+        return self._live[w]
+
+    def theta(self) -> torch.Tensor:
+        """theta in the reference's flat layout."""
+        return self.slayout.from_sync(self.model.theta) if self.slayout else self.model.theta
+
+    def _sync(self):
+        if self._prep is None:
+            self._prep = engine.PreparedSync(
+                self.grads, self.assignment, writeback=False, plan=self.plan,
+                nesterov={"theta": self.model.theta, "velocity": self.velocity, "lr": self.lr,
+                          "momentum": self.momentum, "theta_bf16": self.theta_bf16})
+        self._prep.args.lr = float(self.lr)
+        self._prep.launch()
+
+    def step(self, batches) -> torch.Tensor:
+        """batches: list of N (x, y) device tensors; returns the mean loss (device).
+
+        graphed: the first call (and any call after `lr` changed) captures the
+        step into a CUDA graph -- after warm-up steps on a side stream whose
+        effect on theta / velocity is rolled back -- and every call copies the
+        batches into the graph's static inputs and replays it.  Same math, same
+        kernels, same order as the eager step."""
+        if not self.graphed:
+            return self._step_eager(batches)
+        if self._graph is None or self._graph_lr != self.lr:
+            self._capture(batches)
+        for (sx, sy), (x, y) in zip(self._static, batches):
+            if sx.data_ptr() != x.data_ptr():
+                sx.copy_(x)
+            if sy.data_ptr() != y.data_ptr():
+                sy.copy_(y)
+        self._graph.replay()
+        return self._static_loss
+
+    def _capture(self, batches, warmup: int = 2) -> None:
+        self._static = [(x.clone(), y.clone()) for x, y in batches]
+        state = [self.model.theta, self.velocity, self.theta_bf16]
+        saved = [t.clone() for t in state]
+        side = torch.cuda.Stream(self.model.theta.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # autograd / cuDNN warm-up outside the capture
+            for _ in range(warmup):
+                self._step_eager(self._static, cache=False)
+        torch.cuda.current_stream().wait_stream(side)
+        for t, v in zip(state, saved):  # the warm-up steps never happened
+            t.copy_(v)
+        del saved
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self._static_loss = self._step_eager(self._static, cache=False)
+        self._graph_lr = self.lr
+
+    def _step_params(self) -> dict:
+        """Leaf parameters of one step's block-strategy workers: views of the
+        bf16 copy, with the 4-D convolution weights made channels-last ONCE
+        per step (cuDNN's NHWC kernels would otherwise convert every weight
+        for every worker).  The leaves are shared by the N workers;
+        torch.autograd.grad returns each worker's gradients separately."""
+        topo = self.model.topology
+        src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
+        out = {}
+        for k, v in param_views(topo, src).items():
+            if self.autocast and v.dim() == 4 and v.is_cuda:
+                v = v.contiguous(memory_format=torch.channels_last)
+            out[k] = v.requires_grad_(True)
+        return out
+
+    def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
+        topo = self.model.topology
+        step_params = None
+        losses = []
+        for w, (x, y) in enumerate(batches):
+            if self.compact and self.autocast:
+                losses.append(self._compact_step_bf16(w, x, y, cache))
+                continue
+            if self.compact:
+                sub = self.subs[w]
+                # the worker trains on the bf16 copy the previous sync wrote
+                src = self.theta_bf16 if self.autocast else self.model.theta
+                if self.slayout:  # the worker's blocks of the permuted theta
+                    leaf = self.transfers[w].to_compact(src).requires_grad_(True)
+                else:
+                    leaf = sub.gather(src).requires_grad_(True)  # sdp_gather_slices
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
+                    logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
+                    loss = self.loss_fn(logits, y)
+                del logits
+                (g,) = torch.autograd.grad(loss, leaf)
+                g = g.float()  # fp32 gradient replica (the sync accumulates in fp32)
+                if self.slayout:
+                    self.transfers[w].from_compact(g, self.grads[w])
+                else:
+                    sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
+                losses.append(loss.detach())
+                continue
+            # the worker trains on the bf16 weights the previous sync wrote;
+            # every parameter is a leaf view and its gradient lands directly
+            # in its slot of the fp32 replica (one multi-tensor copy, no [d]
+            # concatenation); parameters of dropped blocks keep their zeros
+            if step_params is None:  # once per step: every worker reads the same bf16 copy
+                step_params = self._step_params()
+            params = step_params
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
+                logits = self.model.arch.forward(params, x, self.views[w])
+                loss = self.loss_fn(logits, y)
+            del logits
+            names = self._live_params(w)
+            gs = torch.autograd.grad(loss, [params[k] for k in names])
+            self._store_grads(w, names, gs)
+            losses.append(loss.detach())
+        self._sync()
+        return torch.stack(losses).mean()
+
+class PeerTrainer(_GradStore):
     """One process per GPU (torchrun): this rank trains its local workers
     (contiguous placement, comm.rank_layout) on their own parameter copies.
     A step is: every local worker's forward/backward writes its fp32 gradient
@@ -843,11 +850,11 @@ class PeerTrainer:
         self.velocity = {w: torch.zeros_like(theta0) for w in self.local}
         self.theta_bf16 = {w: theta0.to(torch.bfloat16) for w in self.local}
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # the gradient replicas are the peer-mapped ones; parameters of a
+        # worker's dropped blocks are never written (the replica keeps zeros
+        # there: the sync only writes owned elements)
+        self.grads = self.group.replicas
         if not self.compact:
-            # per-parameter gradient slots of each replica; parameters of a
-            # worker's dropped blocks are never written (the replica keeps
-            # zeros there: the sync only writes owned elements)
-            self._slots = {w: param_views(model.topology, self.group.replicas[w]) for w in self.local}
             self._live = {w: live_params(model.topology, self.views[w]) for w in self.local}
 
     def step(self, batches: dict) -> torch.Tensor:
@@ -890,6 +897,9 @@ class PeerTrainer:
         losses = []
         for w in self.local:
             x, y = batches[w]
+            if self.compact and self.autocast:
+                losses.append(self._compact_step_bf16(w, x, y, cache, src=self.theta_bf16[w]))
+                continue
             if self.compact:
                 sub = self.subs[w]
                 src = self.theta_bf16[w] if self.autocast else self.theta[w]
@@ -900,13 +910,16 @@ class PeerTrainer:
                 self.transfers[w].from_compact(g.float(), self.group.replicas[w])
             else:
                 src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
-                params = {k: v.requires_grad_(True) for k, v in param_views(topo, src).items()}
+                params = {}
+                for k, v in param_views(topo, src).items():
+                    if self.autocast and v.dim() == 4:  # channels-last conv weights (cuDNN NHWC)
+                        v = v.contiguous(memory_format=torch.channels_last)
+                    params[k] = v.requires_grad_(True)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                     loss = self.loss_fn(self.model.arch.forward(params, x, self.views[w]), y)
                 names = self._live[w]
                 gs = torch.autograd.grad(loss, [params[k] for k in names])
-                slots = self._slots[w]
-                torch._foreach_copy_([slots[k] for k in names], list(gs))
+                self._store_grads(w, names, gs)
             losses.append(loss.detach())
         self.group.launch()  # peer-mapped owner sync: replicas[w] <- mean on w's elements
         for w in self.local:

@@ -122,7 +122,7 @@ TRAIN_CHILD = textwrap.dedent(r"""
     dev = torch.device("cuda", 0)
     model = train.build_resnet18(dev, seed=5)
     a = masking.build_assignment(model.topology, os.environ["STRATEGY"], 4, 2, seed=1)
-    tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=False,
+    tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=os.environ["AUTOCAST"] == "1",
                            timeout_cycles=10_000_000_000, graphed=os.environ["GRAPHED"] == "1")
     for step in range(2):
         batches = {}
@@ -142,14 +142,15 @@ TRAIN_CHILD = textwrap.dedent(r"""
 """)
 
 
-@pytest.mark.parametrize("graphed", [False, True])
+@pytest.mark.parametrize("graphed,autocast", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("strategy", ["block", "neuron"])
-def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
+def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, autocast):
     """train.PeerTrainer over 2 processes (CUDA-IPC replicas, cross-rank sync,
     local Nesterov) leaves every worker's copy of its parameters bit-identical
-    to the co-resident trainer's canonical theta (fp32, deterministic cuDNN) --
-    also when each rank replays its step from a CUDA graph (device-resident
-    barrier epochs)."""
+    to the co-resident trainer's canonical theta (deterministic cuDNN; fp32,
+    and the bf16 autocast step with its fused gradient stores) -- also when
+    each rank replays its step from a CUDA graph (device-resident barrier
+    epochs)."""
     import torch
     from paper_2507_09029_b200 import masking, train
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -158,7 +159,7 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy,
-                   GRAPHED=str(int(graphed)))
+                   GRAPHED=str(int(graphed)), AUTOCAST=str(int(autocast)))
         procs.append(subprocess.Popen([sys.executable, "-c", TRAIN_CHILD], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
@@ -174,8 +175,9 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
     torch.backends.cudnn.deterministic = True
     try:
         model = train.build_resnet18(cuda, seed=5)
+        theta0 = model.theta.cpu().numpy()
         a = masking.build_assignment(model.topology, strategy, 4, 2, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=0.05, autocast=False, sync_layout=strategy == "neuron")
+        tr = train.SubnetTrainer(model, a, lr=0.05, autocast=autocast, sync_layout=strategy == "neuron")
         for step in range(2):
             batches = []
             for w in range(4):
@@ -192,7 +194,16 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed):
         z = np.load(tmp_path / f"rank{r}.npz")
         for w in (0, 1) if r == 0 else (2, 3):
             got = z[f"w{w}"]
-            assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
+            if not autocast:
+                assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
+            else:
+                # libsdp's GroupNorm backward sums dgamma / dbeta with fp32
+                # atomics (order varies run to run): same plumbing, not the
+                # same bits -- the copies agree to a small fraction of the
+                # two steps' update (a wrong slot or layout would be O(1))
+                upd = np.abs(canon - theta0)[masks[w]].max()
+                err = np.abs(got - canon)[masks[w]].max()
+                assert err <= 0.05 * upd, (r, w, err, upd)
 
 
 LOCAL_CHILD = textwrap.dedent(r"""
