@@ -180,21 +180,41 @@ k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __re
   // one pass: sums of (x - K) and (x - K)^2 around the group's first element
   // K (every CTA reads the same K), so the variance does not cancel
   const float K = __bfloat162float(x[static_cast<int64_t>(t.b) * hw * c + t.c0]);
+  // UF items per thread per round, all loads issued before the arithmetic
+  constexpr int UF = vec ? 4 : 8;
   float s0 = 0.f, sq = 0.f;
-  for (int q = threadIdx.x; q < nv; q += kGnThreads) {
-    const int pix = q / cv, kv = q - pix * cv;
+  for (int q0 = threadIdx.x; q0 < nv; q0 += UF * kGnThreads) {
     if (vec) {
-      const Bf8 r = ld8(x + t.base + static_cast<int64_t>(pix) * c + kv * 8);
+      Bf8 r[UF];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float d = r.v[k] - K;
-        s0 += d;
-        sq += d * d;
+      for (int u = 0; u < UF; ++u) {
+        const int q = q0 + u * kGnThreads;
+        const int pix = q / cv, kv = q - pix * cv;
+        if (q < nv) r[u] = ld8(x + t.base + static_cast<int64_t>(pix) * c + kv * 8);
       }
+#pragma unroll
+      for (int u = 0; u < UF; ++u)
+        if (q0 + u * kGnThreads < nv) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float d = r[u].v[k] - K;
+            s0 += d;
+            sq += d * d;
+          }
+        }
     } else {
-      const float d = __bfloat162float(x[t.base + static_cast<int64_t>(pix) * c + kv]) - K;
-      s0 += d;
-      sq += d * d;
+      float v[UF];
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        const int q = q0 + u * kGnThreads;
+        const int pix = q / cv, kv = q - pix * cv;
+        v[u] = q < nv ? __bfloat162float(x[t.base + static_cast<int64_t>(pix) * c + kv]) - K : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        s0 += v[u];
+        sq += v[u] * v[u];
+      }
     }
   }
   block_sum2<kGnThreads>(s0, sq);
