@@ -357,6 +357,8 @@ def run_ours(args):
         if not args.no_train and args.workload == "resnet18":
             train = run_train(args, dev)
             train["c4_gpt2"] = run_train_gpt2(args, dev)
+        if not args.no_train and args.workload == "c1":
+            train = run_train_c1(args, dev)
         if not args.no_cpu_baseline:
             cpu = run_cpu_baseline(args, topo)
             builder = run_mask_builder(args, topo, dev)
@@ -497,6 +499,47 @@ def run_train(args, dev):
                    "*_peak_mem_per_worker_bytes / mem_reduction_vs_dp: the largest worker (block "
                    "sizes are unequal: the window holding layer4.1 keeps most parameters); "
                    "*_mean: averaged over the N workers, as PAPER.md reports per-worker savings")
+    return out
+
+
+def run_train_c1(args, dev, batch: int = 8):
+    """configs[0] C1, the reference's own CPU-runnable case: mini-ResNet 26 ch
+    x 8 blocks at 32x32, N=4 co-resident workers, P=2, batch 8/worker, block
+    dropping; DP comparator at P=N.  Graphed steps; the config is tiny
+    (launch-bound), not a kernel number."""
+    import torch
+
+    from paper_2507_09029_b200 import masking, models, train
+    n, p = args.n_logical, args.p
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    batches = [(torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
+                torch.randint(0, 10, (batch,), generator=gen, device=dev)) for _ in range(n)]
+    out = {"workload": f"mini-ResNet 26ch x 8 blocks 32x32, N={n} co-resident workers, P={p}, batch {batch}/worker, "
+                       "bf16 autocast, fused sync+Nesterov+bf16 cast, whole step in one CUDA graph",
+           "data": "synthetic (the reference uses its blobs dataset)"}
+    for tag, pp in (("subnet", p), ("dp", n)):
+        model = models.build_mini_resnet(26, 8, 10, 2, 3, (32, 32), seed=1, device_=dev)
+        a = masking.build_assignment(model.topology, "block", n, pp, seed=1)
+        tr = train.SubnetTrainer(model, a, lr=0.002, graphed=True)
+        for _ in range(3):
+            tr.step(batches)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.train_steps):
+            loss = tr.step(batches)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / args.train_steps
+        out[f"{tag}_ms_per_step"] = ms
+        out[f"{tag}_samples_per_s_per_gpu"] = n * batch / (ms / 1e3)
+        out[f"{tag}_loss_last"] = float(loss.item())
+        del tr, model, a
+        torch.cuda.empty_cache()
+    out["reference_cpu_samples_per_s"] = 69.8
+    out["reference_cpu_note"] = ("SURVEY.md §8(d)/F9: the reference's engine at C1 on N CPU threads in the survey "
+                                 "container (the reference is not installed on the GPU box, so not re-timed here)")
     return out
 
 

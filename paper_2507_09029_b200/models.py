@@ -221,8 +221,21 @@ class MiniResNet:
     def forward(self, params, x, worker=None, block_mode="skip"):
         g = self.norm_groups
         ones = torch.ones(self.channels, dtype=torch.bool, device=x.device)
+        # bf16 autocast training: channels-last activations and libsdp's
+        # GroupNorm wherever every channel is live (block dropping); the
+        # membership formulation otherwise (the f64 parity path)
+        fast = x.is_cuda and torch.is_autocast_enabled("cuda")
+        if fast:
+            x = x.contiguous(memory_format=torch.channels_last)
+
+        def gn(h, gamma, beta, active, relu):
+            if fast and active is ones:
+                return group_norm(h, g, gamma, beta, relu=relu)
+            out = active_group_norm(h, g, gamma, beta, active)
+            return F.relu(out) if relu else out
+
         h = F.conv2d(x, params["stem.w"], params["stem.b"], padding=1)
-        h = F.relu(active_group_norm(h, g, params["stem_gn.gamma"], params["stem_gn.beta"], ones))
+        h = gn(h, params["stem_gn.gamma"], params["stem_gn.beta"], ones, True)
         for i in range(self.blocks):
             live = True if worker is None else bool(worker.block_active[i])
             if not live and block_mode == "skip":
@@ -230,9 +243,9 @@ class MiniResNet:
             a1 = _flags(worker, f"block{i}.conv1", ones)
             a2 = _flags(worker, f"block{i}.conv2", ones)
             hb = F.conv2d(h, params[f"block{i}.conv1.w"], params[f"block{i}.conv1.b"], padding=1)
-            hb = F.relu(active_group_norm(hb, g, params[f"block{i}.gn1.gamma"], params[f"block{i}.gn1.beta"], a1))
+            hb = gn(hb, params[f"block{i}.gn1.gamma"], params[f"block{i}.gn1.beta"], a1, True)
             hb = F.conv2d(hb, params[f"block{i}.conv2.w"], params[f"block{i}.conv2.b"], padding=1)
-            hb = active_group_norm(hb, g, params[f"block{i}.gn2.gamma"], params[f"block{i}.gn2.beta"], a2)
+            hb = gn(hb, params[f"block{i}.gn2.gamma"], params[f"block{i}.gn2.beta"], a2, False)
             if not live:
                 hb = hb * 0.0
             h = h + hb
@@ -293,7 +306,10 @@ class ResidualMLP:
 def _flags(worker, layer_id, ones):
     if worker is None or layer_id not in worker.channel_active:
         return ones
-    return torch.as_tensor(np.array(worker.channel_active[layer_id], dtype=bool), device=ones.device)
+    flags = np.array(worker.channel_active[layer_id], dtype=bool)
+    if flags.all():  # every channel live (block strategy): the shared all-ones mask
+        return ones
+    return torch.as_tensor(flags, device=ones.device)
 
 
 def _make_global(arch, theta: torch.Tensor | None, dtype, dev) -> GlobalModel:
