@@ -305,14 +305,15 @@ class GPT2Small:
             y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             y = y.transpose(1, 2).reshape(b * t, e)
             y = _addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
-            m = _layer_norm(h + y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
+            r = h + y
+            m = _layer_norm(r, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
             m = F.gelu(_addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
                        approximate="tanh")
             m = _addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
-            o = y + m
-            if not live:
-                o = o * 0.0
-            h = h + o
+            if live:
+                h = r + m  # (h + attn) + mlp, as GPT-2 adds its two residual branches
+            else:  # block_mode "multiply": the dropped block's output scaled by 0
+                h = h + (y + m) * 0.0
         h = _layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
         return LMHead(h, params["wte"])  # tied head, logits h @ wte.T left to lm_loss
 
