@@ -391,6 +391,13 @@ int sdp_conv_grads_to_oihw(const sdp_conv_grad_desc* descs, int n_desc, int max_
                            float* dst, void* stream);
 int sdp_conv_grad_max_block(void);
 
+/* Column sums of a bf16 [rows, cols] matrix into bf16 [cols] with fp32
+ * accumulation (GPT-2 projection bias gradients, train._Linear); cols a
+ * multiple of 8, x 16-B aligned; `scratch` holds cols x sdp_col_sum_parts()
+ * floats; deterministic (parts folded in order). */
+int sdp_col_sum_parts(void);
+int sdp_col_sum_bf16(const void* x_bf16, int64_t rows, int cols, void* out_bf16, float* scratch, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Fused LM-head cross-entropy rows (C4 training step, train.lm_loss)        */
 /* ------------------------------------------------------------------------ */

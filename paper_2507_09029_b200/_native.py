@@ -121,6 +121,8 @@ SIGNATURES = {
     "sdp_merge_heads": (C.c_int, [VP, VP, VP, I64, I64, I32, I32, I32, I64, I64, I64, VP, VP]),
     "sdp_conv_grads_to_oihw": (C.c_int, [VP, I32, I32, VP, VP, VP]),
     "sdp_conv_grad_max_block": (C.c_int, []),
+    "sdp_col_sum_parts": (C.c_int, []),
+    "sdp_col_sum_bf16": (C.c_int, [VP, I64, I32, VP, VP, VP]),
     "sdp_ce_rows_bwd": (C.c_int, [VP, I64, I32, I64, VP, VP, VP, C.c_float, VP, VP]),
     "sdp_assign_units": (C.c_int, [C.POINTER(C.c_uint32), I32, VP, I32, I32, I32, I32, I32, VP, VP, VP]),
     "sdp_permutation": (C.c_int, [C.POINTER(C.c_uint32), I32, VP, I32, I32, VP, VP]),

@@ -249,10 +249,20 @@ class _SplitHeads(torch.autograd.Function):
         return g.view(b * t, 3 * nh * hd), None, None, None, None
 
 
+_CS_PARTS: list = []
+
+
+def _col_sum_parts() -> int:
+    if not _CS_PARTS:
+        _CS_PARTS.append(N.lib().sdp_col_sum_parts())
+    return _CS_PARTS[0]
+
+
 class _Linear(torch.autograd.Function):
     """addmm(bias, x, w) (HF Conv1D: w is [in, out]) whose backward takes the
-    bias gradient as ones @ dy on cuBLAS instead of dy.sum(0): torch's
-    reduce kernel ran 19 us per [8192, <=3072] bf16 gradient, 4 per block."""
+    bias gradient with libsdp's column sum (ones @ dy on cuBLAS otherwise)
+    instead of dy.sum(0): torch's reduce kernel ran 19 us per [8192, <=3072]
+    bf16 gradient, 4 per block."""
 
     @staticmethod
     def forward(ctx, bias, x, w):
@@ -266,8 +276,15 @@ class _Linear(torch.autograd.Function):
         dw = x.t() @ dy if ctx.needs_input_grad[2] else None
         db = None
         if ctx.needs_input_grad[0]:
-            ones = torch.ones((1, dy.shape[0]), dtype=dy.dtype, device=dy.device)
-            db = (ones @ dy).view(-1)
+            n = dy.shape[1]
+            if dy.dtype == torch.bfloat16 and dy.is_cuda and n % 8 == 0 and dy.is_contiguous() \
+                    and dy.data_ptr() % 16 == 0:  # libsdp column sum (deterministic two-stage)
+                db = torch.empty(n, dtype=dy.dtype, device=dy.device)
+                scratch = torch.empty(n * _col_sum_parts(), dtype=torch.float32, device=dy.device)
+                N.call("sdp_col_sum_bf16", ptr(dy), dy.shape[0], n, ptr(db), ptr(scratch), stream_ptr(dy.device))
+            else:
+                ones = torch.ones((1, dy.shape[0]), dtype=dy.dtype, device=dy.device)
+                db = (ones @ dy).view(-1)
         return db, dx, dw
 
 

@@ -300,3 +300,27 @@ def test_widthwise_bf16_per_parameter_leaves_match_single_leaf(cuda):
             assert torch.equal(got, want), (w, (got - want).abs().max().item())
     finally:
         torch.backends.cudnn.deterministic = prev
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 768), (8192, 3072), (100, 2304), (3, 64)])
+def test_col_sum_bf16_matches_fp32_sum(cuda, rows, cols):
+    """libsdp column sums (the GPT-2 bias gradients) vs an fp64 sum of the
+    same bf16 values: within bf16 rounding of the exact sum; deterministic."""
+    import ctypes as C
+    from paper_2507_09029_b200 import _native as N
+    from paper_2507_09029_b200._device import ptr, stream_ptr
+    g = torch.Generator(device=cuda)
+    g.manual_seed(rows + cols)
+    x = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    parts = N.lib().sdp_col_sum_parts()
+
+    def run():
+        out = torch.empty(cols, dtype=torch.bfloat16, device=cuda)
+        scratch = torch.empty(cols * parts, dtype=torch.float32, device=cuda)
+        N.call("sdp_col_sum_bf16", ptr(x), rows, cols, ptr(out), ptr(scratch), stream_ptr(cuda))
+        return out
+
+    a, b = run(), run()
+    assert torch.equal(a, b)
+    ref = x.double().sum(0)
+    assert (a.double() - ref).abs().le(2 ** -7 * ref.abs() + 1e-3 * rows ** 0.5).all()
