@@ -364,6 +364,15 @@ int sdp_layer_norm_bwd_parts(int64_t rows, int cols);
 int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
                        const float* mean, const float* rstd, void* dx_bf16, void* dgamma_bf16, void* dbeta_bf16,
                        float* scratch, int parts, void* stream);
+/* Residual-fused forms (GPT-2 blocks): the forward normalises
+ * sum = bf16(a + b) and also writes `sum` (the residual stream); the
+ * backward adds the residual branch's gradient `dres` into dx. */
+int sdp_add_layer_norm_fwd(const void* a_bf16, const void* b_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                           const void* beta_bf16, float eps, void* sum_bf16, void* y_bf16, float* mean, float* rstd,
+                           void* stream);
+int sdp_layer_norm_bwd_res(const void* dy_bf16, const void* x_bf16, const void* dres_bf16, int64_t rows, int cols,
+                           const void* gamma_bf16, const float* mean, const float* rstd, void* dx_bf16,
+                           void* dgamma_bf16, void* dbeta_bf16, float* scratch, int parts, void* stream);
 
 /* Attention-head gradient merge (train._SplitHeads backward): dq, dk, dv
  * [batch, heads, seq, head_dim] with element strides (stride_batch,

@@ -118,6 +118,8 @@ SIGNATURES = {
     "sdp_layer_norm_fwd": (C.c_int, [VP, I64, I32, VP, VP, C.c_float, VP, VP, VP, VP]),
     "sdp_layer_norm_bwd_parts": (C.c_int, [I64, I32]),
     "sdp_layer_norm_bwd": (C.c_int, [VP, VP, I64, I32, VP, VP, VP, VP, VP, VP, VP, I32, VP]),
+    "sdp_add_layer_norm_fwd": (C.c_int, [VP, VP, I64, I32, VP, VP, C.c_float, VP, VP, VP, VP, VP]),
+    "sdp_layer_norm_bwd_res": (C.c_int, [VP, VP, VP, I64, I32, VP, VP, VP, VP, VP, VP, VP, I32, VP]),
     "sdp_merge_heads": (C.c_int, [VP, VP, VP, I64, I64, I32, I32, I32, I64, I64, I64, VP, VP]),
     "sdp_conv_grads_to_oihw": (C.c_int, [VP, I32, I32, VP, VP, VP]),
     "sdp_conv_grad_max_block": (C.c_int, []),

@@ -60,7 +60,9 @@ __global__ void __launch_bounds__(kLnThreads) k_ln_fwd(const __nv_bfloat16* __re
                                                         const __nv_bfloat16* __restrict__ gamma,
                                                         const __nv_bfloat16* __restrict__ beta, float eps,
                                                         __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
-                                                        float* __restrict__ rstd) {
+                                                        float* __restrict__ rstd,
+                                                        const __nv_bfloat16* __restrict__ x2,
+                                                        __nv_bfloat16* __restrict__ sum_out) {
   constexpr int cols = 256 * V;
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * kLnWarps + (threadIdx.x >> 5);
@@ -69,6 +71,20 @@ __global__ void __launch_bounds__(kLnThreads) k_ln_fwd(const __nv_bfloat16* __re
   float v[V][8];
 #pragma unroll
   for (int k = 0; k < V; ++k) unpack8(ld_nc_v4(xr + 32 * k + lane), v[k]);
+  if (x2) {  // fused residual add: s = bf16(x + x2) is both an output and the normalised row
+    const uint4* x2r = reinterpret_cast<const uint4*>(x2 + row * cols);
+    uint4* sr = reinterpret_cast<uint4*>(sum_out + row * cols);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float w[8];
+      unpack8(ld_nc_v4(x2r + 32 * k + lane), w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[k][i] += w[i];
+      const uint4 packed = pack8(v[k]);
+      sr[32 * k + lane] = packed;
+      unpack8(packed, v[k]);  // the rounded sum, as an unfused bf16 add would hand over
+    }
+  }
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k)
@@ -106,7 +122,8 @@ __global__ void __launch_bounds__(kLnThreads, (V <= 3 ? 2 : 1)) k_ln_bwd(const _
                                                         const __nv_bfloat16* __restrict__ gamma,
                                                         const float* __restrict__ mean,
                                                         const float* __restrict__ rstd,
-                                                        __nv_bfloat16* __restrict__ dx, float* __restrict__ part) {
+                                                        __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
+                                                        const __nv_bfloat16* __restrict__ dres) {
   constexpr int cols = 256 * V;
   __shared__ float s_dg[kLnWarps / 2][cols];
   __shared__ float s_db[kLnWarps / 2][cols];
@@ -148,11 +165,18 @@ __global__ void __launch_bounds__(kLnThreads, (V <= 3 ? 2 : 1)) k_ln_bwd(const _
     s1 = warp_sum(s1) * (1.f / cols);
     s2 = warp_sum(s2) * (1.f / cols);
     uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       float o[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = r * (d[k][i] - s1 - xh[k][i] * s2);
+      if (rr) {  // fused gradient accumulation of the residual branch
+        float e[8];
+        unpack8(ld_nc_v4(rr + 32 * k + lane), e);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += e[i];
+      }
       dxr[32 * k + lane] = pack8(o);
     }
   }
@@ -241,11 +265,18 @@ using namespace sdp;
 
 extern "C" {
 
-int sdp_layer_norm_fwd(const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
-                       const void* beta_bf16, float eps, void* y_bf16, float* mean, float* rstd, void* stream) {
+static int ln_fwd(const void* x_bf16, const void* x2_bf16, void* sum_bf16, int64_t rows, int cols,
+                  const void* gamma_bf16, const void* beta_bf16, float eps, void* y_bf16, float* mean, float* rstd,
+                  void* stream) {
   if (int rc = ln_check(rows, cols, x_bf16, y_bf16)) return rc;
   if (int rc = ln_check(rows, cols, gamma_bf16, beta_bf16)) return rc;
+  if (x2_bf16 || sum_bf16) {
+    if (!x2_bf16 || !sum_bf16) return set_error(SDP_ERR_USAGE, "fused add needs both the addend and the sum buffer");
+    if (int rc = ln_check(rows, cols, x2_bf16, sum_bf16)) return rc;
+  }
   if (rows == 0) return SDP_OK;
+  auto x2b = static_cast<const __nv_bfloat16*>(x2_bf16);
+  auto sb = static_cast<__nv_bfloat16*>(sum_bf16);
   const unsigned grid = static_cast<unsigned>((rows + kLnWarps - 1) / kLnWarps);
   cudaStream_t s = as_stream(stream);
   auto xb = static_cast<const __nv_bfloat16*>(x_bf16);
@@ -254,12 +285,23 @@ int sdp_layer_norm_fwd(const void* x_bf16, int64_t rows, int cols, const void* g
   auto yb = static_cast<__nv_bfloat16*>(y_bf16);
   switch (cols / 256) {
 #define SDP_LN_FWD(V) \
-  case V: k_ln_fwd<V><<<grid, kLnThreads, 0, s>>>(xb, rows, gb, bb, eps, yb, mean, rstd); break;
+  case V: k_ln_fwd<V><<<grid, kLnThreads, 0, s>>>(xb, rows, gb, bb, eps, yb, mean, rstd, x2b, sb); break;
     SDP_LN_FWD(1) SDP_LN_FWD(2) SDP_LN_FWD(3) SDP_LN_FWD(4) SDP_LN_FWD(5) SDP_LN_FWD(6) SDP_LN_FWD(7) SDP_LN_FWD(8)
 #undef SDP_LN_FWD
   }
   SDP_LAUNCH_CHECK();
   return SDP_OK;
+}
+
+int sdp_layer_norm_fwd(const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                       const void* beta_bf16, float eps, void* y_bf16, float* mean, float* rstd, void* stream) {
+  return ln_fwd(x_bf16, nullptr, nullptr, rows, cols, gamma_bf16, beta_bf16, eps, y_bf16, mean, rstd, stream);
+}
+
+int sdp_add_layer_norm_fwd(const void* a_bf16, const void* b_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                           const void* beta_bf16, float eps, void* sum_bf16, void* y_bf16, float* mean, float* rstd,
+                           void* stream) {
+  return ln_fwd(a_bf16, b_bf16, sum_bf16, rows, cols, gamma_bf16, beta_bf16, eps, y_bf16, mean, rstd, stream);
 }
 
 int sdp_layer_norm_bwd_parts(int64_t rows, int cols) {
@@ -278,9 +320,12 @@ int sdp_layer_norm_bwd_parts(int64_t rows, int cols) {
   return static_cast<int>(need < slots ? (need > 0 ? need : 1) : slots);
 }
 
-int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
-                       const float* mean, const float* rstd, void* dx_bf16, void* dgamma_bf16, void* dbeta_bf16,
-                       float* scratch, int parts, void* stream) {
+static int ln_bwd(const void* dy_bf16, const void* x_bf16, const void* dres_bf16, int64_t rows, int cols,
+                  const void* gamma_bf16, const float* mean, const float* rstd, void* dx_bf16, void* dgamma_bf16,
+                  void* dbeta_bf16, float* scratch, int parts, void* stream) {
+  if (dres_bf16)
+    if (int rc = ln_check(rows, cols, dres_bf16, dres_bf16)) return rc;
+  auto rb = static_cast<const __nv_bfloat16*>(dres_bf16);
   if (int rc = ln_check(rows, cols, x_bf16, dy_bf16)) return rc;
   if (int rc = ln_check(rows, cols, dx_bf16, gamma_bf16)) return rc;
   if (parts <= 0) return set_error(SDP_ERR_USAGE, "layer norm backward needs parts > 0");
@@ -292,7 +337,7 @@ int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, in
   if (rows > 0) {
     switch (cols / 256) {
 #define SDP_LN_BWD(V) \
-  case V: k_ln_bwd<V><<<parts, kLnThreads, 0, s>>>(db, xb, rows, gb, mean, rstd, dxb, scratch); break;
+  case V: k_ln_bwd<V><<<parts, kLnThreads, 0, s>>>(db, xb, rows, gb, mean, rstd, dxb, scratch, rb); break;
       SDP_LN_BWD(1) SDP_LN_BWD(2) SDP_LN_BWD(3) SDP_LN_BWD(4)
 #undef SDP_LN_BWD
       default:
@@ -306,6 +351,20 @@ int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, in
                                                    static_cast<__nv_bfloat16*>(dbeta_bf16));
   SDP_LAUNCH_CHECK();
   return SDP_OK;
+}
+
+int sdp_layer_norm_bwd(const void* dy_bf16, const void* x_bf16, int64_t rows, int cols, const void* gamma_bf16,
+                       const float* mean, const float* rstd, void* dx_bf16, void* dgamma_bf16, void* dbeta_bf16,
+                       float* scratch, int parts, void* stream) {
+  return ln_bwd(dy_bf16, x_bf16, nullptr, rows, cols, gamma_bf16, mean, rstd, dx_bf16, dgamma_bf16, dbeta_bf16,
+                scratch, parts, stream);
+}
+
+int sdp_layer_norm_bwd_res(const void* dy_bf16, const void* x_bf16, const void* dres_bf16, int64_t rows, int cols,
+                           const void* gamma_bf16, const float* mean, const float* rstd, void* dx_bf16,
+                           void* dgamma_bf16, void* dbeta_bf16, float* scratch, int parts, void* stream) {
+  return ln_bwd(dy_bf16, x_bf16, dres_bf16, rows, cols, gamma_bf16, mean, rstd, dx_bf16, dgamma_bf16, dbeta_bf16,
+                scratch, parts, stream);
 }
 
 }  // extern "C"

@@ -186,6 +186,62 @@ class _LayerNormBF16(torch.autograd.Function):
         return dx, dw, db, None
 
 
+class _AddLayerNormBF16(torch.autograd.Function):
+    """(s, LN(s)) with s = a + b in bf16, on libsdp's residual-fused row
+    kernels: one pass writes the residual stream and its normalisation, and
+    the backward adds the residual branch's gradient into dx -- the two
+    bf16 adds of an unfused block (forward sum, backward accumulation) go
+    away."""
+
+    @staticmethod
+    def forward(ctx, a, b, w, bias, eps):
+        cols = a.shape[-1]
+        rows = a.numel() // cols
+        s = torch.empty_like(a)
+        y = torch.empty_like(a)
+        mean = torch.empty(rows, dtype=torch.float32, device=a.device)
+        rstd = torch.empty(rows, dtype=torch.float32, device=a.device)
+        N.call("sdp_add_layer_norm_fwd", ptr(a), ptr(b), rows, cols, ptr(w), ptr(bias), C.c_float(eps), ptr(s),
+               ptr(y), ptr(mean), ptr(rstd), stream_ptr(a.device))
+        ctx.save_for_backward(s, w, mean, rstd)
+        return s, y
+
+    @staticmethod
+    def backward(ctx, ds, dy):
+        s, w, mean, rstd = ctx.saved_tensors
+        cols = s.shape[-1]
+        rows = s.numel() // cols
+        dy = _aligned16(dy if dy is not None else torch.zeros_like(s))
+        key = (rows, cols, s.device)
+        parts = _LN_PARTS.get(key)
+        if parts is None:
+            parts = _LN_PARTS[key] = N.lib().sdp_layer_norm_bwd_parts(rows, cols)
+        scratch = torch.empty(2 * cols * parts, dtype=torch.float32, device=s.device)
+        dx = torch.empty_like(s)
+        dw = torch.empty(cols, dtype=torch.bfloat16, device=s.device)
+        db = torch.empty(cols, dtype=torch.bfloat16, device=s.device)
+        if ds is None:
+            N.call("sdp_layer_norm_bwd", ptr(dy), ptr(s), rows, cols, ptr(w), ptr(mean), ptr(rstd), ptr(dx),
+                   ptr(dw), ptr(db), ptr(scratch), parts, stream_ptr(s.device))
+        else:
+            ds = _aligned16(ds)
+            N.call("sdp_layer_norm_bwd_res", ptr(dy), ptr(s), ptr(ds), rows, cols, ptr(w), ptr(mean), ptr(rstd),
+                   ptr(dx), ptr(dw), ptr(db), ptr(scratch), parts, stream_ptr(s.device))
+        return dx, dx, dw, db, None
+
+
+def _add_layer_norm(a, b, shape, w, bias, eps: float = 1e-5):
+    """(a + b, LayerNorm(a + b)); fused on libsdp under bf16 autocast."""
+    if a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16 and torch.is_autocast_enabled("cuda"):
+        with torch.autocast("cuda", enabled=False):
+            wb, bb = w.to(a.dtype), bias.to(a.dtype)
+            if (_ln_native(a, wb, bb) and len(shape) == 1 and a.shape == b.shape
+                    and a.data_ptr() % 16 == 0 and b.data_ptr() % 16 == 0 and a.is_contiguous() and b.is_contiguous()):
+                return _AddLayerNormBF16.apply(a, b, _aligned16(wb), _aligned16(bb), eps)
+    s = a + b
+    return s, _layer_norm(s, shape, w, bias, eps)
+
+
 def _ln_native(x, w, b) -> bool:
     cols = x.shape[-1]
     return (x.is_cuda and x.dtype == torch.bfloat16 and cols % 256 == 0 and cols <= 1024
@@ -311,27 +367,34 @@ class GPT2Small:
         b, t = tokens.shape
         e, nh = self.d_model, self.n_head
         h = F.embedding(tokens, params["wte"]) + params["wpe"][:t][None]
+        pend = None  # (r, m): the residual stream is r + m, not yet added
         for i in range(self.n_layer):
             live = True if worker is None else bool(worker.block_active[i])
             if not live and block_mode == "skip":
                 continue
             p = f"h{i}"
-            a = _layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
+            if pend is None:
+                a = _layer_norm(h, (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
+            else:  # the previous block's residual add fused into this LayerNorm
+                h, a = _add_layer_norm(pend[0], pend[1], (e,), params[f"{p}.ln_1.w"], params[f"{p}.ln_1.b"])
+                pend = None
             qkv = _addmm(params[f"{p}.attn.c_attn.b"], a.reshape(b * t, e), params[f"{p}.attn.c_attn.w"])
             q, k, v = _SplitHeads.apply(qkv, b, t, nh, e // nh)
             y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             y = y.transpose(1, 2).reshape(b * t, e)
             y = _addmm(params[f"{p}.attn.c_proj.b"], y, params[f"{p}.attn.c_proj.w"]).view(b, t, e)
-            r = h + y
-            m = _layer_norm(r, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
+            r, m = _add_layer_norm(h, y, (e,), params[f"{p}.ln_2.w"], params[f"{p}.ln_2.b"])
             m = F.gelu(_addmm(params[f"{p}.mlp.c_fc.b"], m.reshape(b * t, e), params[f"{p}.mlp.c_fc.w"]),
                        approximate="tanh")
             m = _addmm(params[f"{p}.mlp.c_proj.b"], m, params[f"{p}.mlp.c_proj.w"]).view(b, t, e)
             if live:
-                h = r + m  # (h + attn) + mlp, as GPT-2 adds its two residual branches
+                pend = (r, m)  # h = (h + attn) + mlp, added by the next LayerNorm
             else:  # block_mode "multiply": the dropped block's output scaled by 0
                 h = h + (y + m) * 0.0
-        h = _layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
+        if pend is None:
+            h = _layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
+        else:
+            _, h = _add_layer_norm(pend[0], pend[1], (e,), params["ln_f.w"], params["ln_f.b"])
         return LMHead(h, params["wte"])  # tied head, logits h @ wte.T left to lm_loss
 
 

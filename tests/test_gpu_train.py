@@ -324,3 +324,31 @@ def test_col_sum_bf16_matches_fp32_sum(cuda, rows, cols):
     assert torch.equal(a, b)
     ref = x.double().sum(0)
     assert (a.double() - ref).abs().le(2 ** -7 * ref.abs() + 1e-3 * rows ** 0.5).all()
+
+
+def test_add_layer_norm_bf16_fused_matches_unfused(cuda):
+    """train._AddLayerNormBF16 (libsdp residual-fused LayerNorm): the sum and
+    the normalised rows equal the unfused bf16 add + LayerNorm kernels bit for
+    bit; the gradients (dx with the residual branch's gradient folded in)
+    agree with the unfused autograd to bf16 rounding."""
+    from paper_2507_09029_b200 import train
+    rows, cols = 4096, 768
+    g = torch.Generator(device=cuda)
+    g.manual_seed(9)
+    a = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    b = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    w = (1 + 0.1 * torch.randn(cols, generator=g, device=cuda)).bfloat16()
+    bias = (0.1 * torch.randn(cols, generator=g, device=cuda)).bfloat16()
+    ds = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    dy = torch.randn(rows, cols, generator=g, device=cuda).bfloat16()
+    fa, fb, fw, fbias = (t.clone().requires_grad_(True) for t in (a, b, w, bias))
+    s, y = train._AddLayerNormBF16.apply(fa, fb, fw, fbias, 1e-5)
+    torch.autograd.backward([s, y], [ds, dy])
+    ua, ub, uw, ubias = (t.clone().requires_grad_(True) for t in (a, b, w, bias))
+    us = ua + ub
+    uy = train._LayerNormBF16.apply(us, uw, ubias, 1e-5)
+    torch.autograd.backward([us, uy], [ds, dy])
+    assert torch.equal(s, us) and torch.equal(y, uy)
+    for got, want in ((fa.grad, ua.grad), (fb.grad, ub.grad)):
+        assert (got.float() - want.float()).abs().le(2 ** -7 * want.float().abs() + 2e-2).all()
+    assert torch.equal(fw.grad, uw.grad) and torch.equal(fbias.grad, ubias.grad)
