@@ -395,7 +395,9 @@ class GPT2Small:
             h = _layer_norm(h, (e,), params["ln_f.w"], params["ln_f.b"])
         else:
             _, h = _add_layer_norm(pend[0], pend[1], (e,), params["ln_f.w"], params["ln_f.b"])
-        return LMHead(h, params["wte"])  # tied head, logits h @ wte.T left to lm_loss
+        # tied head, logits h @ wte.T left to lm_loss; "__wte_padded": the
+        # head weight padded for the GEMMs, built once per step by the trainer
+        return LMHead(h, params["wte"], params.get("__wte_padded"))
 
 
 @dataclass
@@ -406,6 +408,7 @@ class LMHead:
     that want them)."""
     h: torch.Tensor
     wte: torch.Tensor
+    padded: torch.Tensor | None = None  # wte padded to the head GEMM's vocabulary (no grad)
 
     def logits(self) -> torch.Tensor:
         return self.h @ self.wte.t()
@@ -443,7 +446,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
         return wp
 
     @staticmethod
-    def forward(ctx, h, w, t):
+    def forward(ctx, h, w, t, wp=None):
         cdt = _LinearCrossEntropy._cdt(h)
         t = t.contiguous()
         n, v = h.shape[0], w.shape[0]
@@ -452,7 +455,11 @@ class _LinearCrossEntropy(torch.autograd.Function):
         rows = torch.empty(n, dtype=acc, device=h.device)
         hc = h.to(cdt)
         fused = cdt == torch.bfloat16
-        wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
+        if fused and wp is not None and wp.dtype == cdt:  # padded once per step by the trainer
+            wc = wp
+        else:
+            wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
+        ctx.wp = wc if fused and wp is not None and wp.dtype == cdt else None
         with torch.autocast("cuda", enabled=False):
             for s in range(0, n, _LinearCrossEntropy.CHUNK):
                 e = min(n, s + _LinearCrossEntropy.CHUNK)
@@ -476,7 +483,10 @@ class _LinearCrossEntropy(torch.autograd.Function):
         acc = lse.dtype
         fused = cdt == torch.bfloat16
         hc = h.to(cdt)
-        wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
+        if ctx.wp is not None:
+            wc = ctx.wp
+        else:
+            wc = _LinearCrossEntropy._padded(w, cdt) if fused else w.to(cdt)
         gh = torch.empty(h.shape, dtype=cdt, device=h.device)
         gw = torch.zeros(wc.shape, dtype=acc, device=w.device)
         g32 = g.detach().to(torch.float32).reshape(1).contiguous()
@@ -498,7 +508,7 @@ class _LinearCrossEntropy(torch.autograd.Function):
                     torch.addmm(gw, dl.t(), hc[s:e], out_dtype=torch.float32, out=gw)
                 else:
                     gw += (dl.t() @ hc[s:e]).to(acc)
-        return gh.to(h.dtype), gw[:v].to(w.dtype), None
+        return gh.to(h.dtype), gw[:v].to(w.dtype), None, None
 
 
 def lm_loss(out, tokens):
@@ -506,7 +516,8 @@ def lm_loss(out, tokens):
     given logits [B, T, V]."""
     if isinstance(out, LMHead):
         e = out.h.shape[-1]
-        return _LinearCrossEntropy.apply(out.h[:, :-1].reshape(-1, e), out.wte, tokens[:, 1:].reshape(-1))
+        return _LinearCrossEntropy.apply(out.h[:, :-1].reshape(-1, e), out.wte, tokens[:, 1:].reshape(-1),
+                                         out.padded)
     acc = torch.promote_types(out.dtype, torch.float32)  # fp32, or fp64 for fp64 logits
     return F.cross_entropy(out[:, :-1].reshape(-1, out.shape[-1]).to(acc), tokens[:, 1:].reshape(-1))
 
@@ -826,10 +837,13 @@ class SubnetTrainer(_GradStore):
         topo = self.model.topology
         src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
         out = {}
-        for k, v in param_views(topo, src).items():
+        views = param_views(topo, src)
+        for k, v in views.items():
             if self.autocast and v.dim() == 4 and v.is_cuda:
                 v = v.contiguous(memory_format=torch.channels_last)
             out[k] = v.requires_grad_(True)
+        if self.autocast and isinstance(self.model.arch, GPT2Small):  # the tied head, padded once for all workers
+            out["__wte_padded"] = _LinearCrossEntropy._padded(views["wte"], torch.bfloat16)
         return out
 
     def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
