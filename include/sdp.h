@@ -399,6 +399,10 @@ typedef struct {
 int sdp_conv_grads_to_oihw(const sdp_conv_grad_desc* descs, int n_desc, int max_out_channels, const void* src_bf16,
                            float* dst, void* stream);
 int sdp_conv_grad_max_block(void);
+/* The reverse direction for the training copy: bf16 OIHW -> bf16 OHWI
+ * (channels-last) for every descriptor, same table layout. */
+int sdp_conv_weights_to_ohwi(const sdp_conv_grad_desc* descs, int n_desc, int max_out_channels, const void* src_bf16,
+                             void* dst_bf16, void* stream);
 
 /* Column sums of a bf16 [rows, cols] matrix into bf16 [cols] with fp32
  * accumulation (GPT-2 projection bias gradients, train._Linear); cols a

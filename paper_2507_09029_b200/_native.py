@@ -123,6 +123,7 @@ SIGNATURES = {
     "sdp_merge_heads": (C.c_int, [VP, VP, VP, I64, I64, I32, I32, I32, I64, I64, I64, VP, VP]),
     "sdp_conv_grads_to_oihw": (C.c_int, [VP, I32, I32, VP, VP, VP]),
     "sdp_conv_grad_max_block": (C.c_int, []),
+    "sdp_conv_weights_to_ohwi": (C.c_int, [VP, I32, I32, VP, VP, VP]),
     "sdp_col_sum_parts": (C.c_int, []),
     "sdp_col_sum_bf16": (C.c_int, [VP, I64, I32, VP, VP, VP]),
     "sdp_ce_rows_bwd": (C.c_int, [VP, I64, I32, I64, VP, VP, VP, C.c_float, VP, VP]),

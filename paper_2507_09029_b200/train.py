@@ -598,9 +598,25 @@ class _GradStore:
         src = self.theta_bf16 if src is None else src
         cvec = self.transfers[w].to_compact(src) if self.slayout else sub.gather(src)
         views = sub.views(cvec)
+        if getattr(self, "_cg_max", None) is None:
+            self._cg_max = N.lib().sdp_conv_grad_max_block()
+        # conv weights to channels-last in ONE launch (sdp_conv_weights_to_ohwi)
+        # instead of one cuDNN-side conversion per weight
+        conv_w = [k for k, v in views.items()
+                  if v.dim() == 4 and v.numel() > 0 and v.shape[1] * v.shape[2] * v.shape[3] <= self._cg_max]
+        cl = None
+        if conv_w:
+            cl = torch.empty_like(cvec)
+            descs, max_o = self._conv_table(("w", w, tuple(conv_w)), [views[k] for k in conv_w])
+            N.call("sdp_conv_weights_to_ohwi", ptr(descs), len(conv_w), max_o, ptr(cvec), ptr(cl),
+                   stream_ptr(cvec.device))
+        cset_w = set(conv_w)
         params = {}
         for k, v in views.items():
-            if v.dim() == 4 and v.numel() > 0:
+            if k in cset_w:
+                o, i, kh, kw = v.shape
+                v = cl.as_strided((o, i, kh, kw), (i * kh * kw, 1, kw * i, i), v.storage_offset())
+            elif v.dim() == 4 and v.numel() > 0:
                 v = v.contiguous(memory_format=torch.channels_last)
             params[k] = v.requires_grad_(True)
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=True, cache_enabled=cache):
@@ -634,18 +650,7 @@ class _GradStore:
         g32 = self._cbuf32[:max(1, n)]
         g32.copy_(self._cbuf[:max(1, n)])  # conv slots are OHWI here; rewritten below
         if conv:
-            key = (w, tuple(conv))
-            if not hasattr(self, "_ccdescs"):
-                self._ccdescs = {}
-            if key not in self._ccdescs:
-                dt = np.dtype([("offset", "<i8"), ("out", "<i4"), ("inp", "<i4"), ("k", "<i4"), ("pad", "<i4")])
-                arr = np.zeros(len(conv), dtype=dt)
-                for j, k in enumerate(conv):
-                    sh = slots[k].shape
-                    arr[j] = (slots[k].storage_offset(), sh[0], sh[1], sh[2] * sh[3], 0)
-                self._ccdescs[key] = (torch.from_numpy(arr.view(np.uint8).copy()).to(cvec.device),
-                                      int(arr["out"].max()))
-            descs, max_o = self._ccdescs[key]
+            descs, max_o = self._conv_table(("g", w, tuple(conv)), [slots[k] for k in conv])
             N.call("sdp_conv_grads_to_oihw", ptr(descs), len(conv), max_o, ptr(self._cbuf), ptr(g32),
                    stream_ptr(cvec.device))
         if self.slayout:
@@ -653,6 +658,21 @@ class _GradStore:
         else:
             sub.scatter(g32, self.grads[w])
         return loss.detach()
+
+    def _conv_table(self, key, views: list):
+        """Device descriptor table (sdp_conv_grad_desc) of conv weights given as
+        views of one flat buffer (offset = storage offset), cached by key."""
+        if not hasattr(self, "_ctables"):
+            self._ctables = {}
+        if key not in self._ctables:
+            dt = np.dtype([("offset", "<i8"), ("out", "<i4"), ("inp", "<i4"), ("k", "<i4"), ("pad", "<i4")])
+            arr = np.zeros(len(views), dtype=dt)
+            for j, v in enumerate(views):
+                sh = v.shape
+                arr[j] = (v.storage_offset(), sh[0], sh[1], sh[2] * sh[3], 0)
+            self._ctables[key] = (torch.from_numpy(arr.view(np.uint8).copy()).to(views[0].device),
+                                  int(arr["out"].max()))
+        return self._ctables[key]
 
     def _store_grads(self, w: int, names: list, gs) -> None:
         """Parameter gradients -> worker w's fp32 replica.  bf16 gradients go
