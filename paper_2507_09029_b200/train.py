@@ -858,8 +858,24 @@ class SubnetTrainer(_GradStore):
         src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
         out = {}
         views = param_views(topo, src)
+        conv_w = []
+        if self.autocast and src.is_cuda and src.dtype == torch.bfloat16:
+            if getattr(self, "_cg_max", None) is None:
+                self._cg_max = N.lib().sdp_conv_grad_max_block()
+            conv_w = [k for k, v in views.items()
+                      if v.dim() == 4 and v.numel() > 0 and v.shape[1] * v.shape[2] * v.shape[3] <= self._cg_max]
+        cl = None
+        if conv_w:  # every conv weight to channels-last in one launch
+            cl = torch.empty_like(src)
+            descs, max_o = self._conv_table(("step",), [views[k] for k in conv_w])
+            N.call("sdp_conv_weights_to_ohwi", ptr(descs), len(conv_w), max_o, ptr(src), ptr(cl),
+                   stream_ptr(src.device))
+        cset = set(conv_w)
         for k, v in views.items():
-            if self.autocast and v.dim() == 4 and v.is_cuda:
+            if k in cset:
+                o, i, kh, kw = v.shape
+                v = cl.as_strided((o, i, kh, kw), (i * kh * kw, 1, kw * i, i), v.storage_offset())
+            elif self.autocast and v.dim() == 4 and v.is_cuda:
                 v = v.contiguous(memory_format=torch.channels_last)
             out[k] = v.requires_grad_(True)
         if self.autocast and isinstance(self.model.arch, GPT2Small):  # the tied head, padded once for all workers
