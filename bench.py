@@ -24,7 +24,6 @@ import argparse
 import concurrent.futures
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -45,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet18")
+    ap.add_argument("--workload", default="gpt2")
     ap.add_argument("--n-logical", type=int, default=8)
     ap.add_argument("--p", type=int, default=4)
     ap.add_argument("--strategy", default="block")
@@ -86,106 +85,126 @@ def traffic_for(tag: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled
+    every 2 ms from a thread (the timed region of a 20-step sync run is only a
+    few tens of ms; nvidia-smi -lms 50 caught one sample), nvidia-smi as the
+    fallback."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.sm: list[float] = []
+        self.reasons: set = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+                while not self._stop.is_set():
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = int(get_r(h))
+                    for bit, nm in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(nm)
+                    time.sleep(0.002)
+
+            self._t = threading.Thread(target=poll, daemon=True)
             self._t.start()
-            time.sleep(0.15)
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            time.sleep(0.06)
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML, 2 ms poll"}
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm: the reference algorithm (engine.py:71-74) ported to numpy
-# f64 (oracle/oracle.py, verified bit-exact against the reference), split
-# over host threads by contiguous element ranges.
+# CPU reference arm: the reference's OWN engine.aggregate (engine.py:60-79),
+# staged into oracle/_ref by oracle/build_ref.py (pure Python; it travels to
+# the GPU box with the snapshot) and called unmodified.  numpy ufuncs run on
+# one core, so the all-threads form hands each host thread a contiguous range
+# of the vector, with a reference MaskAssignment over that range (its own
+# constructor, masking.py:188-207) -- every element still goes through the
+# reference's code.
 # ---------------------------------------------------------------------------
 
-def cpu_aggregate_threads(grads, masks, divisor, lo, hi, threads):
-    chunks = np.linspace(lo, hi, threads + 1).astype(np.int64)
-    out = np.empty(hi - lo, dtype=np.float64)
+def reference_pkg():
+    from oracle import build_ref  # checker / baseline only
+    return build_ref.import_reference()
 
-    def run(k):
-        a, b = chunks[k], chunks[k + 1]
-        from oracle.oracle import aggregate_f64
-        out[a - lo:b - lo] = aggregate_f64([g[a:b] for g in grads], masks[:, a:b], divisor[a:b])
 
-    if threads == 1:
-        run(0)
-    else:
-        with concurrent.futures.ThreadPoolExecutor(threads) as ex:
-            list(ex.map(run, range(threads)))
+def reference_assignment(topo, strategy: str, n: int, p: int, seed: int = 1):
+    """The reference's build_assignment (masking.py:305-359) on the same
+    topology, declared through the reference's own types."""
+    from oracle import build_ref
+    S = reference_pkg()
+    return S.build_assignment(build_ref.to_reference_topology(topo), strategy, n, p, seed)
+
+
+def reference_grads(a, hi: int, seed: int = 1000):
+    """N float64 gradients over [0, hi): fp32 normals, zero off-mask (the
+    reference's nullity), upcast as the reference takes them."""
+    rng = np.random.default_rng(seed)
+    return [(rng.standard_normal(hi, dtype=np.float32) * a.param_masks[w, :hi]).astype(np.float64)
+            for w in range(a.n_workers)]
+
+
+def reference_chunks(a, hi: int, parts: int):
+    """Contiguous ranges of [0, hi) with a reference MaskAssignment each."""
+    import types
+    S = reference_pkg()
+    MA = S.masking.MaskAssignment
+    bounds = np.linspace(0, hi, parts + 1).astype(np.int64)
+    out = []
+    for lo, up in zip(bounds[:-1], bounds[1:]):
+        lo, up = int(lo), int(up)
+        if up <= lo:
+            continue
+        ca = MA(a.n_workers, a.replication, a.strategy, a.seed, types.SimpleNamespace(total=up - lo),
+                a.unit_workers, a.param_masks[:, lo:up], a.governors[lo:up])
+        out.append((lo, up, ca))
     return out
 
 
-def host_workload(topo, strategy, n, p, seed=1):
-    from oracle import oracle as O
-    a = O.build_assignment(topo, strategy, n, p, seed)
-    rng = np.random.default_rng(1000)
-    grads = [(rng.standard_normal(topo.total, dtype=np.float32) * a.param_masks[w]).astype(np.float64)
-             for w in range(n)]
-    owned = int(a.coverage.sum())
-    return a, grads, owned
+def reference_aggregate(chunks, grads, pool=None):
+    """One reference engine.aggregate call per chunk (all chunks = one step)."""
+    S = reference_pkg()
+
+    def run(c):
+        lo, up, ca = c
+        return S.engine.aggregate([g[lo:up] for g in grads], ca).gbar
+
+    if pool is None:
+        return [run(c) for c in chunks]
+    return list(pool.map(run, chunks))
 
 
-def time_cpu(grads, masks, divisor, owned_per_elem, threads, budget_s, max_reps=1000):
-    """Bounded sample: whole-vector calls until the budget is spent (>= 1 call);
-    if one call exceeds the budget, a contiguous prefix sized to fit."""
-    d = masks.shape[1]
-    t0 = time.perf_counter()
-    cpu_aggregate_threads(grads, masks, divisor, 0, min(d, 1 << 20), threads)
-    est = (time.perf_counter() - t0) * d / min(d, 1 << 20)
-    hi = d if est <= budget_s else max(1 << 16, int(d * budget_s / est))
-    reps = max(1, min(max_reps, int(budget_s / max(est * hi / d, 1e-6))))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        cpu_aggregate_threads(grads, masks, divisor, 0, hi, threads)
-    dt = (time.perf_counter() - t0) / reps
-    nbytes = float(owned_per_elem[:hi].sum()) * 4
-    return nbytes / dt / 1e9, dt, hi, reps
+def _probe_seconds_per_elem(a, threads: int) -> float:
+    m = min(a.topology.total, 1 << 20)
+    g = reference_grads(a, m)
+    ch = reference_chunks(a, m, threads)
+    with concurrent.futures.ThreadPoolExecutor(threads) as pool:
+        reference_aggregate(ch, g, pool if threads > 1 else None)
+        t0 = time.perf_counter()
+        reference_aggregate(ch, g, pool if threads > 1 else None)
+        return (time.perf_counter() - t0) / m
 
 
 def run_reference(args):
@@ -193,30 +212,29 @@ def run_reference(args):
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
     topo, tag = workload(args.workload)
-    a, grads, owned = host_workload(topo, args.strategy, args.n_logical, args.p)
-    threads = os.cpu_count() or 1
-    per_elem = a.coverage
-    # size each step so warmup + steps end within ~2 minutes
-    budget_total = 120.0
     d = topo.total
-    t0 = time.perf_counter()
-    cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, min(d, 1 << 20), threads)
-    est_full = (time.perf_counter() - t0) * d / min(d, 1 << 20)
-    per_step = budget_total / max(1, args.steps + args.warmup)
-    hi = d if est_full <= per_step else max(1 << 16, int(d * per_step / est_full))
-    for _ in range(args.warmup):
-        cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, hi, threads)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_aggregate_threads(grads, a.param_masks, a.divisor, 0, hi, threads)
-        times.append(time.perf_counter() - t0)
+    a = reference_assignment(topo, args.strategy, args.n_logical, args.p)
+    threads = os.cpu_count() or 1
+    # size each step so warmup + steps end within ~2 minutes
+    per_step = 120.0 / max(1, args.steps + args.warmup)
+    est = _probe_seconds_per_elem(a, threads) * d
+    hi = d if est <= per_step else max(1 << 16, int(d * per_step / est))
+    grads = reference_grads(a, hi)
+    chunks = reference_chunks(a, hi, threads)
+    with concurrent.futures.ThreadPoolExecutor(threads) as pool:
+        for _ in range(args.warmup):
+            reference_aggregate(chunks, grads, pool)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            reference_aggregate(chunks, grads, pool)
+            times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
-    nbytes = float(per_elem[:hi].sum()) * 4
+    nbytes = float(a.coverage[:hi].sum()) * 4
     value = nbytes / dt / 1e9
-    sample = (f"{'whole vector' if hi == d else f'first {hi} of {d} elements'} per step; "
-              f"numpy f64 port of engine.aggregate (oracle/oracle.py:aggregate_f64), "
-              f"{threads} threads over contiguous element ranges")
+    sample = (f"{'whole vector' if hi == d else f'first {hi} of {d} elements'} per step; the reference's own "
+              f"subnetdp.engine.aggregate (oracle/_ref, unmodified, float64), {threads} host threads each "
+              f"calling it on a contiguous range")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -224,7 +242,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": tag, "d": d, "n_logical": args.n_logical, "p": args.p,
                    "strategy": args.strategy, "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -350,18 +368,21 @@ def run_ours(args):
     cpu = None
     train = None
     builder = None
-    if world > 1 and not args.no_train and args.workload == "resnet18":
+    if world > 1 and not args.no_train and args.workload in ("gpt2", "resnet18"):
         train = run_train_multi(args, dev, rank, world, red_dev)
     if rank == 0 and world == 1:
         e2e = run_e2e(args, a, dev, total_bytes)
-        if not args.no_train and args.workload == "resnet18":
-            train = run_train(args, dev)
-            train["c4_gpt2"] = run_train_gpt2(args, dev)
+        if not args.no_train and args.workload in ("gpt2", "resnet18"):
+            train = {"c4_gpt2": run_train_gpt2(args, dev), "c2_c3_resnet18": run_train(args, dev)}
+            if args.n_logical == 8 and args.p == 4:
+                c1 = argparse.Namespace(**{**vars(args), "n_logical": 4, "p": 2})
+                train["c1_mini_resnet"] = run_train_c1(c1, dev)
         if not args.no_train and args.workload == "c1":
             train = run_train_c1(args, dev)
         if not args.no_cpu_baseline:
-            cpu = run_cpu_baseline(args, topo)
-            builder = run_mask_builder(args, topo, dev)
+            cpu, ref_a = run_cpu_baseline(args, topo)
+            builder = run_mask_builder(args, topo, dev, ref_a)
+            del ref_a
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -537,10 +558,53 @@ def run_train_c1(args, dev, batch: int = 8):
         out[f"{tag}_loss_last"] = float(loss.item())
         del tr, model, a
         torch.cuda.empty_cache()
-    out["reference_cpu_samples_per_s"] = 69.8
-    out["reference_cpu_note"] = ("SURVEY.md §8(d)/F9: the reference's engine at C1 on N CPU threads in the survey "
-                                 "container (the reference is not installed on the GPU box, so not re-timed here)")
+    out["reference_cpu"] = run_reference_c1(n, p, batch)
+    out["reference_cpu_samples_per_s"] = out["reference_cpu"]["samples_per_s"]
     return out
+
+
+def run_reference_c1(n: int = 4, p: int = 2, batch: int = 8, steps: int = 6) -> dict:
+    """The reference's own training step at configs[0] timed on this host:
+    mini-ResNet 26 ch x 8 blocks, synthetic blobs 32x32 (seed 7), N=4, P=2,
+    batch 8/worker, block dropping, OPENBLAS 1 thread per worker thread and
+    engine threads = N (SURVEY F9's fastest setting).  Set-up and step body
+    are engine.run's (engine.py:155-223) calling the reference's functions
+    from oracle/_ref unmodified -- the worker fan-out (_worker_step), aggregate
+    and optimizer.update -- without run()'s held-out evaluation, which is not
+    part of a training step."""
+    from threadpoolctl import threadpool_limits
+    S = reference_pkg()
+    C, E = S.config, S.engine
+    cfg = C.ExperimentConfig(
+        model=C.ModelConfig(kind="mini_resnet", channels=26, blocks=8, classes=10, norm_groups=2,
+                            in_channels=3, image_hw=(32, 32)),
+        dataset=C.DatasetConfig(kind="synthetic-blobs", height=32, width=32, channels=3, classes=10, seed=7),
+        n=n, p=p, strategy="block", batch_per_worker=batch, seed=1, threads=n)
+    dataset = S.data.load_dataset(cfg.dataset)
+    model = cfg.model.build(cfg.seed)
+    a = E.build_assignment(model.topology, cfg.strategy, cfg.n, cfg.p, cfg.seed)
+    model.theta = E.masked_kaiming_init(model, a, cfg.seed)
+    opt = E.make_optimizer(cfg.optimizer.kind, model.topology.total, momentum=cfg.optimizer.momentum)
+    streams = np.random.SeedSequence(cfg.seed).spawn(cfg.n)
+    workers = [E.WorkerState(i, a.worker_view(i), np.random.default_rng(streams[i])) for i in range(cfg.n)]
+    layers = (model.topology.default_alignment_layer,)
+    times, losses = [], []
+    with threadpool_limits(1, "blas"), concurrent.futures.ThreadPoolExecutor(cfg.threads) as pool:
+        for t in range(steps + 1):
+            t0 = time.perf_counter()
+            futs = [pool.submit(E._worker_step, model, w, dataset, cfg.batch_per_worker, t, layers, False)
+                    for w in workers]
+            reports = [f.result() for f in futs]
+            agg = E.aggregate([r.grad for r in reports], a)
+            opt.update(model.theta, agg.gbar, 0.02)
+            times.append(time.perf_counter() - t0)
+            losses.append(float(np.mean([r.loss for r in reports])))
+    dt = float(np.mean(times[1:]))  # the first step warms the BLAS / thread pool
+    return {"samples_per_s": n * batch / dt, "ms_per_step": dt * 1e3, "cores": n, "steps_timed": steps,
+            "loss_first": losses[0], "loss_last": losses[-1],
+            "how": f"reference step body (engine.py:203-223: _worker_step fan-out, aggregate, optimizer.update; "
+                   f"oracle/_ref unmodified), lr 0.02, OPENBLAS 1 thread, engine threads={n}; "
+                   f"host has {os.cpu_count()} cores"}
 
 
 def run_train_multi(args, dev, rank: int, world: int, red_dev):
@@ -693,14 +757,14 @@ def run_train_gpt2(args, dev, micro_batch: int = 8, seq: int = 1024):
     return out
 
 
-def run_mask_builder(args, topo, dev):
+def run_mask_builder(args, topo, dev, ref_a=None):
     """build_assignment through the public API on the GPU (seeded
     assignment + element expansion + tables, synchronised) and its kernels
-    alone, beside the CPU restatement of the reference's build_assignment on
-    1 core -- checked bit-exact against each other."""
+    alone, beside the reference's own build_assignment (masking.py:305-359,
+    oracle/_ref, 1 core) on the same topology -- checked bit-exact against
+    each other (per-element owner sets)."""
     import torch
 
-    from oracle import oracle as O  # noqa: F401  (checker/baseline only)
     from paper_2507_09029_b200 import masking
     n, p = args.n_logical, args.p
     masking.build_assignment(topo, args.strategy, n, p, seed=1)
@@ -727,29 +791,50 @@ def run_mask_builder(args, topo, dev):
         torch.cuda.synchronize()
         kern[name] = s.elapsed_time(e) / 5 * 1e3
     t0 = time.perf_counter()
-    o = O.build_assignment(topo, args.strategy, n, p, 1)
-    cpu_s = time.perf_counter() - t0
-    exact = bool(np.array_equal(a.owner_mask.cpu().numpy().astype(np.uint64), o.owner_bits)
-                 and np.array_equal(a.coverage.cpu().numpy(), o.coverage))
+    ra = reference_assignment(topo, args.strategy, n, p) if ref_a is None else ref_a
+    cpu_s = time.perf_counter() - t0 if ref_a is None else getattr(ra, "_bench_build_s", None)
+    bits = np.zeros(topo.total, dtype=np.uint8 if n <= 8 else np.uint64)
+    for w in range(n):
+        bits |= ra.param_masks[w].astype(bits.dtype) << bits.dtype.type(w)
+    ours = a.owner_mask.cpu().numpy()
+    exact = bool(np.array_equal(ours.astype(np.uint64), bits.astype(np.uint64))
+                 and np.array_equal(a.coverage.cpu().numpy(), ra.coverage)
+                 and np.array_equal(a.governors.cpu().numpy(), ra.governors))
     return {"workload": f"build_assignment({args.workload}, {args.strategy}, N={n}, P={p}, seed=1)",
             "api_ms": float(np.median(api)) * 1e3,
             "stage_us": {k: round(v, 1) for k, v in kern.items()},
             "stage_timing": "CUDA events around each stage's host call (k_assign includes its group-table "
-                            "upload; ncu kernel time 8 us)",
-            "cpu_restatement_ms": cpu_s * 1e3, "cpu_cores": 1,
-            "cpu_kind": "port (oracle/oracle.py:build_assignment, numpy; the reference itself is not on the box)",
-            "bit_exact": exact}
+                            "upload)",
+            "reference_cpu_ms": None if cpu_s is None else cpu_s * 1e3, "reference_cpu_cores": 1,
+            "reference_kind": "reference (subnetdp.masking.build_assignment from oracle/_ref, unmodified)",
+            "bit_exact_vs_reference": exact}
 
 
 def run_cpu_baseline(args, topo):
-    from oracle import oracle as O  # noqa: F401  (checker/baseline only)
-    a, grads, owned = host_workload(topo, args.strategy, args.n_logical, args.p)
-    value, dt, hi, reps = time_cpu(grads, a.param_masks, a.divisor, a.coverage, 1, budget_s=10.0)
+    """The reference's own engine.aggregate on ONE core (numpy ufuncs are
+    single-threaded) over a bounded prefix of the same workload."""
+    t0 = time.perf_counter()
+    a = reference_assignment(topo, args.strategy, args.n_logical, args.p)
+    a._bench_build_s = time.perf_counter() - t0
     d = topo.total
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{reps} calls over {'the whole vector' if hi == d else f'{hi} of {d} elements'}"
-                      f", numpy f64 port of engine.aggregate on 1 thread (host has {os.cpu_count()} cores)",
-            "ms_per_call": dt * 1e3}
+    budget = 10.0  # seconds of timed calls; one call is sized to ~2.5 s
+    est = _probe_seconds_per_elem(a, 1) * d
+    hi = d if est <= budget / 4 else max(1 << 16, int(d * budget / 4 / est))
+    grads = reference_grads(a, hi)
+    chunks = reference_chunks(a, hi, 1)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        reference_aggregate(chunks, grads)
+        reps += 1
+        if time.perf_counter() - t0 >= budget / 2 or reps >= 1000:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    value = float(a.coverage[:hi].sum()) * 4 / dt / 1e9
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{reps} calls over {'the whole vector' if hi == d else f'the first {hi} of {d} elements'}"
+                      f" of the reference's own subnetdp.engine.aggregate (oracle/_ref, float64) on 1 thread "
+                      f"(host has {os.cpu_count()} cores)",
+            "ms_per_call": dt * 1e3}, a
 
 
 def main():

@@ -236,6 +236,11 @@ int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity,
                         const void* grad, double lr, double momentum,
                         void* theta_bf16, uint32_t* status, void* stream);
 
+/* Finite check that runs BEFORE an optimizer update (optim.py:78-80 raises
+ * NumericalError before touching theta): ORs SDP_STATUS_NONFINITE into
+ * *status if any of x[0..total) is Inf or NaN. */
+int sdp_check_finite(int dtype, int64_t total, const void* x, uint32_t* status, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Extraction / write-back (models.py:333-382)                               */
 /* ------------------------------------------------------------------------ */

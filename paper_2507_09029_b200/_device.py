@@ -66,3 +66,42 @@ def sdp_dtype(t: torch.dtype) -> int:
     if t == torch.float64:
         return N.DTYPE_F64
     raise TypeError(f"owner sync runs on float32 or float64 buffers, got {t}")
+
+
+_INPLACE_DUNDERS = frozenset({"__setitem__", "__iadd__", "__isub__", "__imul__", "__itruediv__",
+                              "__ifloordiv__", "__imod__", "__ipow__", "__ilshift__", "__irshift__",
+                              "__iand__", "__ior__", "__ixor__", "__imatmul__"})
+
+
+class ReadOnlyTensor(torch.Tensor):
+    """A device array the caller may read but not write: the reference freezes
+    an assignment's arrays (masking.py:206-207, `setflags(write=False)`), so an
+    in-place op, item assignment or `out=` into one raises ValueError exactly as
+    writing a read-only numpy array does.  Views taken from it stay read-only;
+    every other result is a plain tensor.  libsdp reads it through data_ptr()."""
+
+    @classmethod
+    def __torch_function__(cls, func, types, args=(), kwargs=None):
+        kwargs = kwargs or {}
+        name = getattr(func, "__name__", "")
+        first = args[0] if args else None
+        if isinstance(first, ReadOnlyTensor) and (
+                name in _INPLACE_DUNDERS or (name.endswith("_") and not name.startswith("_"))):
+            raise ValueError(f"assignment array is read-only ({name})")
+        out = kwargs.get("out")
+        if out is not None and any(isinstance(o, ReadOnlyTensor)
+                                   for o in (out if isinstance(out, (tuple, list)) else (out,))):
+            raise ValueError("assignment array is read-only (out=)")
+        with torch._C.DisableTorchFunctionSubclass():
+            ret = func(*args, **kwargs)
+        if isinstance(first, ReadOnlyTensor) and isinstance(ret, torch.Tensor) and not \
+                isinstance(ret, ReadOnlyTensor) and ret._is_view() and ret.numel() and \
+                ret.untyped_storage().data_ptr() == first.untyped_storage().data_ptr():
+            ret = ret.as_subclass(ReadOnlyTensor)
+        return ret
+
+
+def read_only(t: torch.Tensor | None) -> torch.Tensor | None:
+    if t is None or isinstance(t, ReadOnlyTensor):
+        return t
+    return t.as_subclass(ReadOnlyTensor)

@@ -465,6 +465,15 @@ __global__ void k_nesterov(int64_t total, T* __restrict__ theta, T* __restrict__
     atomicOr(status, SDP_STATUS_NONFINITE);
 }
 
+template <typename T>
+__global__ void k_check_finite(int64_t total, const T* __restrict__ x, uint32_t* status) {
+  bool bad = false;
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !finite(__ldcs(x + j));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, SDP_STATUS_NONFINITE);
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace sdp
@@ -599,6 +608,21 @@ int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity, c
     k_nesterov<double><<<grid, 256, 0, s>>>(total, static_cast<double*>(theta), static_cast<double*>(velocity),
                                             static_cast<const double*>(grad), lr, momentum,
                                             static_cast<__nv_bfloat16*>(theta_bf16), status);
+  else
+    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_check_finite(int dtype, int64_t total, const void* x, uint32_t* status, void* stream) {
+  if (total <= 0) return SDP_OK;
+  if (!x || !status) return set_error(SDP_ERR_USAGE, "null buffer");
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sm_count() * 8));
+  cudaStream_t s = as_stream(stream);
+  if (dtype == SDP_DTYPE_F32)
+    k_check_finite<float><<<grid, 256, 0, s>>>(total, static_cast<const float*>(x), status);
+  else if (dtype == SDP_DTYPE_F64)
+    k_check_finite<double><<<grid, 256, 0, s>>>(total, static_cast<const double*>(x), status);
   else
     return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
   SDP_LAUNCH_CHECK();

@@ -329,6 +329,26 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     a.out_bf16 = None if out_bf16 is None else out_bf16.data_ptr()
     if nesterov is not None and adam is not None:
         raise UsageError("choose one fused optimizer")
+    opt = nesterov if nesterov is not None else adam
+    if opt is not None:
+        keys = ("theta", "velocity") if nesterov is not None else ("theta", "m", "v")
+        for k in keys:
+            t = opt.get(k)
+            if not torch.is_tensor(t) or t.dtype != dt or t.numel() != d or t.device != dev or not _aligned(t):
+                raise UsageError(f"fused optimizer buffer {k!r} must be a contiguous, 16-byte aligned [{d}] "
+                                 f"{dt} tensor on {dev} (the replicas' dtype)")
+        tb = opt.get("theta_bf16")
+        if tb is not None and (tb.dtype != torch.bfloat16 or tb.numel() != d or tb.device != dev
+                               or not tb.is_contiguous()):
+            raise UsageError(f"theta_bf16 must be a contiguous [{d}] bfloat16 tensor on {dev}")
+    for nm, t, want in (("out", out, dt), ("out_bf16", out_bf16, torch.bfloat16)):
+        if t is not None and (t.dtype != want or t.numel() != d or not t.is_contiguous()):
+            raise UsageError(f"{nm} must be a contiguous [{d}] {want} tensor")
+    if shadows_bf16 is not None:
+        for sh in shadows_bf16:
+            if sh is not None and (sh.dtype != torch.bfloat16 or sh.numel() != d or sh.device != dev
+                                   or not sh.is_contiguous()):
+                raise UsageError(f"bf16 shadows must be contiguous [{d}] bfloat16 tensors on {dev}")
     if nesterov is not None:
         flags |= N.SYNC_NESTEROV
         a.theta = nesterov["theta"].data_ptr()
@@ -363,8 +383,18 @@ def aggregate(grads, assignment) -> AggregatedGradient:
     Workers are accumulated in ascending id order from +0; uncovered entries get
     0.  float64 inputs reproduce the reference bit for bit; float32 inputs follow
     the same recurrence in fp32.  numpy inputs are copied to the device and the
-    mean is returned as numpy (the host-buffer end-to-end path).
+    mean is returned as numpy (the host-buffer end-to-end path).  `assignment`
+    may be this package's device MaskAssignment or the reference's own (numpy)
+    one, so engine.run (engine.py:222) can call this unchanged.
     """
+    from . import masking
+    if masking.is_reference_assignment(assignment):
+        # the reference's own MaskAssignment (engine.run hands us that one):
+        # packed onto the device once, cached per object; the result carries
+        # the reference's frozen divisor, as engine.py:79 returns it
+        ref = assignment
+        out = aggregate(grads, masking.from_reference(ref))
+        return AggregatedGradient(gbar=out.gbar, divisor=ref.divisor)
     n, d = assignment.n_workers, assignment.topology.total
     if not torch.is_tensor(grads) and len(grads) != n:
         raise ProtocolError(f"aggregate received {len(grads)} gradients for {n} workers")
@@ -407,7 +437,9 @@ class _PinnedResults:
     (numpy views collapse their base onto the buffer, so its reference count
     is exact), which keeps the reference's fresh-result semantics
     (engine.py:60-79) while steady-state calls skip cudaHostAlloc (~30 ms for
-    44 MB)."""
+    44 MB).  The caller receives a fresh view made INSIDE the lock, so the
+    buffer's count has already risen when a concurrent caller looks at it:
+    two callers never share a buffer."""
 
     def __init__(self, cap: int = 4):
         self.cap = cap
@@ -415,18 +447,20 @@ class _PinnedResults:
         self.lock = threading.Lock()
 
     def get(self, d: int, dt: torch.dtype) -> tuple[np.ndarray, torch.Tensor]:
-        with self.lock:  # concurrent callers never receive the same free buffer
-            return self._get(d, dt)
+        with self.lock:
+            base, t = self._get(d, dt)
+            return base[:], t  # the lease: a view holding a reference to the buffer
+
+    @staticmethod
+    def _alloc(d: int, dt: torch.dtype) -> torch.Tensor:
+        return torch.empty(d, dtype=dt, pin_memory=True)
 
     def _get(self, d: int, dt: torch.dtype) -> tuple[np.ndarray, torch.Tensor]:
         lst = self.bufs.setdefault((d, dt), [])
-        if not lst:  # double-buffer from the start: `out = aggregate(...)` loops hold one
-            t = torch.empty(d, dtype=dt, pin_memory=True)
-            lst.append((t.numpy(), t))
-        for i in range(len(lst)):
-            if sys.getrefcount(lst[i][0]) == 2:  # the pool's list + this call's argument
-                return lst[i]
-        t = torch.empty(d, dtype=dt, pin_memory=True)
+        for entry in lst:
+            if sys.getrefcount(entry[0]) == 2:  # the pool's tuple + the call's argument: no lease out
+                return entry
+        t = self._alloc(d, dt)
         entry = (t.numpy(), t)
         lst.append(entry)
         if len(lst) > self.cap:
@@ -515,23 +549,49 @@ def dt_np(dt: torch.dtype):
 
 class SgdNesterov:
     """optim.SgdNesterov (optim.py:71-87) over a device theta, on libsdp's
-    k_nesterov: v = mu v + g; theta -= lr (g + mu v); NumericalError on a
-    non-finite gradient."""
+    k_nesterov: v = mu v + g; theta -= lr (g + mu v).  Like the reference
+    (optim.py:78-80) a non-finite gradient raises NumericalError BEFORE theta
+    or the velocity is touched: libsdp's k_check_finite scans the gradient
+    first and the update kernel runs only if it is finite.
+
+    The velocity takes theta's dtype and device on the first update unless
+    `dtype` is given (the reference's theta is float64); every update checks
+    that theta, velocity and gradient agree in dtype, size and device."""
 
     kind = "sgd-nesterov"
 
-    def __init__(self, dim: int, momentum: float = 0.9, dtype=torch.float32, device_=None):
+    def __init__(self, dim: int, momentum: float = 0.9, dtype=None, device_=None):
+        self.dim = int(dim)
         self.momentum = momentum
-        self.velocity = torch.zeros(dim, dtype=dtype, device=device(device_))
+        self._device = device_
+        self.velocity = None if dtype is None else torch.zeros(dim, dtype=dtype, device=device(device_))
+
+    def _check(self, theta: torch.Tensor, grad: torch.Tensor, theta_bf16) -> None:
+        if self.velocity is None:
+            self.velocity = torch.zeros(self.dim, dtype=theta.dtype, device=theta.device)
+        for nm, t in (("theta", theta), ("velocity", self.velocity), ("grad", grad)):
+            if not torch.is_tensor(t) or t.dtype != theta.dtype or t.numel() != self.dim \
+                    or t.device != theta.device or not t.is_contiguous():
+                raise UsageError(f"SgdNesterov: {nm} must be a contiguous [{self.dim}] {theta.dtype} tensor on "
+                                 f"{theta.device} (got {getattr(t, 'dtype', type(t))}, "
+                                 f"{getattr(t, 'numel', lambda: '?')()} elements, {getattr(t, 'device', '?')})")
+        if theta.dtype not in (torch.float32, torch.float64) or theta.device.type != "cuda":
+            raise UsageError("SgdNesterov: theta must be a float32 / float64 CUDA tensor")
+        if theta_bf16 is not None and (theta_bf16.dtype != torch.bfloat16 or theta_bf16.numel() != self.dim
+                                       or theta_bf16.device != theta.device or not theta_bf16.is_contiguous()):
+            raise UsageError(f"SgdNesterov: theta_bf16 must be a contiguous [{self.dim}] bfloat16 tensor")
 
     def update(self, theta: torch.Tensor, grad: torch.Tensor, lr: float,
                theta_bf16: torch.Tensor | None = None) -> None:
+        self._check(theta, grad, theta_bf16)
         status = torch.zeros(1, dtype=torch.int32, device=theta.device)
-        N.call("sdp_nesterov_update", sdp_dtype(theta.dtype), theta.numel(), ptr(theta),
-               ptr(self.velocity), ptr(grad), float(lr), float(self.momentum), ptr(theta_bf16),
-               ptr(status), stream_ptr(theta.device))
+        s = stream_ptr(theta.device)
+        N.call("sdp_check_finite", sdp_dtype(grad.dtype), grad.numel(), ptr(grad), ptr(status), s)
         if int(status.item()) & N.STATUS_NONFINITE:
             raise NumericalError("aggregated gradient contains non-finite values")
+        N.call("sdp_nesterov_update", sdp_dtype(theta.dtype), theta.numel(), ptr(theta),
+               ptr(self.velocity), ptr(grad), float(lr), float(self.momentum), ptr(theta_bf16),
+               None, s)
 
     def state_elements(self) -> int:
-        return self.velocity.numel()
+        return self.dim

@@ -32,8 +32,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._device import MASK_TORCH_DTYPE, device, mask_bytes_for, ptr, stream_ptr, upload_struct
-from .errors import ConfigError, TopologyError, ValidationError
+from ._device import MASK_TORCH_DTYPE, device, mask_bytes_for, ptr, read_only, stream_ptr, upload_struct
+from .errors import ConfigError, TopologyError, UsageError, ValidationError
 from .topology import ModelTopology, UnitTable, unit_table
 
 KIND_CHANNEL = "channel"
@@ -270,7 +270,7 @@ class MaskAssignment:
 
     def __init__(self, n_workers, replication, strategy, seed, topology, unit_workers,
                  param_masks, governors, *, _tables=None, _owner_mask=None, _coverage=None,
-                 _divisor=None, _active_counts=None, _unit_bits=None):
+                 _divisor=None, _active_counts=None, _unit_bits=None, _device=None):
         self.n_workers = int(n_workers)
         self.replication = int(replication)
         self.strategy = strategy
@@ -282,7 +282,7 @@ class MaskAssignment:
         if _owner_mask is None:
             # explicit [N, d] masks (tests, hand-built assignments): pack on device
             pm = torch.as_tensor(np.asarray(param_masks) if not torch.is_tensor(param_masks) else param_masks)
-            dev = device(pm.device if pm.is_cuda else None)
+            dev = device(pm.device if pm.is_cuda else _device)
             pm = pm.to(dev, dtype=torch.bool)
             mb = mask_bytes_for(self.n_workers)
             packed = torch.zeros(pm.shape[1], dtype=torch.int64, device=dev)
@@ -302,6 +302,11 @@ class MaskAssignment:
             self.divisor = _divisor
             self.governors = governors
             self._active_counts = _active_counts
+        # the reference freezes these (masking.py:206-207): read-only views
+        self.owner_mask = read_only(self.owner_mask)
+        self.coverage = read_only(self.coverage)
+        self.divisor = read_only(self.divisor)
+        self.governors = read_only(self.governors)
         self.mask_bytes = mask_bytes_for(self.n_workers)
         self._uncovered = None
         self._plans: dict = {}
@@ -331,7 +336,7 @@ class MaskAssignment:
             self._param_masks = _expand(self.topology, self._tables, self._unit_bits, self.n_workers,
                                         self.device, want_param_masks=True,
                                         want_stats=False)["param_masks"]
-        return self._param_masks
+        return read_only(self._param_masks)
 
     @property
     def always_active(self) -> torch.Tensor:
@@ -417,6 +422,79 @@ class MaskAssignment:
         if key not in self._plans:
             self._plans[key] = SyncPlan(self, **kw)
         return self._plans[key]
+
+
+def _reference_module(name: str):
+    """subnetdp.<name> of the reference package, when the caller has it."""
+    import importlib
+    try:
+        return importlib.import_module(f"subnetdp.{name}")
+    except ImportError as exc:
+        raise UsageError("the reference package `subnetdp` is not importable here") from exc
+
+
+def is_reference_assignment(obj) -> bool:
+    """A reference MaskAssignment (numpy arrays, masking.py:188-207)."""
+    return not isinstance(obj, MaskAssignment) and hasattr(obj, "param_masks") \
+        and isinstance(getattr(obj, "param_masks"), np.ndarray)
+
+
+_FROM_REF: dict = {}
+
+
+def from_reference(ref, device_=None) -> MaskAssignment:
+    """A reference MaskAssignment as a device one: its [N, d] masks packed into
+    the per-element owner bitmask on the GPU, governors and unit_workers kept.
+    Cached per reference object (the reference freezes its arrays,
+    masking.py:206-207, so the cache can never go stale)."""
+    import weakref
+    key = id(ref)
+    hit = _FROM_REF.get(key)
+    if hit is not None and hit[0]() is ref:
+        return hit[1]
+    uw = {StructuralUnit.from_key(u.key()): tuple(w) for u, w in ref.unit_workers.items()}
+    ours = MaskAssignment(ref.n_workers, ref.replication, ref.strategy, ref.seed, ref.topology, uw,
+                          np.asarray(ref.param_masks), np.asarray(ref.governors), _device=device(device_))
+    try:
+        wr = weakref.ref(ref, lambda _, k=key: _FROM_REF.pop(k, None))
+    except TypeError:  # not weak-referenceable: no caching
+        return ours
+    _FROM_REF[key] = (wr, ours)
+    return ours
+
+
+def reference_topology(topology):
+    """`topology` declared through the reference's own types (field-for-field
+    equal dataclasses, reference topology.py:16-84)."""
+    T = _reference_module("topology")
+    if isinstance(topology, T.ModelTopology):
+        return topology
+    return T.ModelTopology(
+        params=tuple(T.ParamSpec(p.name, tuple(p.shape), p.offset, p.size, p.kind, p.layer_id)
+                     for p in topology.params),
+        channel_layers=tuple(T.ChannelLayerSpec(c.layer_id, c.channels, c.norm_groups, c.maskable,
+                                                tuple(c.own_slices), tuple(c.consumer_slices))
+                             for c in topology.channel_layers),
+        blocks=tuple(T.BlockSpec(b.block_id, b.index, tuple(b.param_names), b.has_skip, b.maskable,
+                                 b.activation_per_sample) for b in topology.blocks),
+        base_activation_per_sample=topology.base_activation_per_sample,
+        input_shape=tuple(topology.input_shape),
+        default_alignment_layer=topology.default_alignment_layer)
+
+
+def to_reference(assignment: MaskAssignment, topology=None):
+    """The GPU-built assignment as the reference's own MaskAssignment (numpy,
+    frozen by its constructor, masking.py:188-207), for callers that hand it to
+    the reference's loop (validate, masked_kaiming_init, worker_view,
+    save_assignment; engine.py:167-185).  `topology`: the caller's reference
+    topology object (default: this assignment's, converted)."""
+    M = _reference_module("masking")
+    topo = reference_topology(assignment.topology if topology is None else topology)
+    uw = {M.StructuralUnit.from_key(u.key()): tuple(w) for u, w in assignment.unit_workers.items()}
+    return M.MaskAssignment(
+        n_workers=assignment.n_workers, replication=assignment.replication, strategy=assignment.strategy,
+        seed=assignment.seed, topology=topo, unit_workers=uw,
+        param_masks=assignment.param_masks.cpu().numpy(), governors=assignment.governors.cpu().numpy())
 
 
 def build_assignment(topology: ModelTopology, strategy: str, n_workers: int, replication: int,
@@ -539,14 +617,22 @@ def assignment_from_dict(doc: dict, topology: ModelTopology, device_=None) -> Ma
         if strategy == "neuron":
             if unit.ref not in t.layer_base:
                 raise TopologyError(f"unit {key} refers to a non-maskable or unknown layer")
-            uid = t.layer_base[unit.ref] + unit.index
+            channels = topology.channel_layer(unit.ref).channels
+            idx = unit.index
+            # numpy indexing semantics of the reference (masking.py:479):
+            # negative indices wrap, anything outside [-C, C) is an IndexError
+            if not -channels <= idx < channels:
+                raise IndexError(f"unit {key}: index {idx} is out of bounds for layer "
+                                 f"{unit.ref} with {channels} channels")
+            uid = t.layer_base[unit.ref] + idx % channels
         else:
             if unit.ref not in t.block_unit:
                 raise TopologyError(f"unit {key} refers to an unknown block")
             uid = t.block_unit[unit.ref]
         b = 0
         for w in ws:
-            b |= 1 << w
+            if 0 <= w < n_workers:  # the reference only deactivates workers in range(n)
+                b |= 1 << w
         bits[uid] = b
         unit_workers[unit] = ws
     ub = torch.from_numpy(bits.view(np.int64)).to(dev)

@@ -25,6 +25,7 @@ import torch.nn.functional as F
 from . import _native as N
 from . import engine, masking, zoo
 from ._device import ptr, stream_ptr
+from .errors import NumericalError
 from .models import _channels_last_bf16, group_norm
 from .topology import GlobalModel
 
@@ -778,16 +779,24 @@ class SubnetTrainer(_GradStore):
         # sync_layout: keep theta / velocity / gradient replicas permuted into the
         # window-class-major layout (layout.py) so the sync sees uniform tiles
         self.slayout = None
+        # master: the fp32 theta the fused update writes.  In the reference
+        # layout it IS model.theta (same storage); in the sync layout it is a
+        # private permuted copy and model.theta is left in the reference
+        # layout (write_back() refreshes it, theta() returns it permuted back),
+        # so checkpoint.save_checkpoint(model, ...) never sees a permuted vector.
+        self.master = model.theta
         if sync_layout and self.compact:
             from .layout import SyncLayout, WorkerTransfer
             self.slayout = SyncLayout(assignment)
             self.transfers = [WorkerTransfer(self.slayout, s) for s in self.subs]
-            model.theta = self.slayout.to_sync(model.theta)
+            self.master = self.slayout.to_sync(model.theta)
         self.velocity = torch.zeros(d, device=dev)
-        self.theta_bf16 = model.theta.to(torch.bfloat16)
+        self.theta_bf16 = self.master.to(torch.bfloat16)
         self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
         self.lr, self.momentum, self.autocast = lr, momentum, autocast
         self.plan = self.slayout.plan() if self.slayout else assignment.sync_plan()
+        # status word of the fused sync (SDP_SYNC_CHECK_FINITE): read by check()
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self._prep = None
 
     def _live_params(self, w: int) -> list:
@@ -799,13 +808,29 @@ class SubnetTrainer(_GradStore):
 
     def theta(self) -> torch.Tensor:
         """theta in the reference's flat layout."""
-        return self.slayout.from_sync(self.model.theta) if self.slayout else self.model.theta
+        return self.slayout.from_sync(self.master) if self.slayout else self.master
+
+    def write_back(self) -> None:
+        """Refresh model.theta (reference layout) from the trainer's master."""
+        if self.slayout is not None:
+            self.model.theta.copy_(self.slayout.from_sync(self.master))
+
+    def check(self) -> None:
+        """Raise NumericalError if any step since the last check produced a
+        non-finite mean (the reference raises before updating, optim.py:78-80;
+        the fused sync+update cannot roll back, so theta already holds the
+        non-finite step when this fires -- call it at every loss read)."""
+        st = int(self.status.item())
+        if st & N.STATUS_NONFINITE:
+            self.status.zero_()
+            raise NumericalError("training aborted: the aggregated gradient contains non-finite values")
 
     def _sync(self):
         if self._prep is None:
             self._prep = engine.PreparedSync(
-                self.grads, self.assignment, writeback=False, plan=self.plan,
-                nesterov={"theta": self.model.theta, "velocity": self.velocity, "lr": self.lr,
+                self.grads, self.assignment, writeback=False, plan=self.plan, check_finite=True,
+                status=self.status,
+                nesterov={"theta": self.master, "velocity": self.velocity, "lr": self.lr,
                           "momentum": self.momentum, "theta_bf16": self.theta_bf16})
         self._prep.args.lr = float(self.lr)
         self._prep.launch()
@@ -832,9 +857,9 @@ class SubnetTrainer(_GradStore):
 
     def _capture(self, batches, warmup: int = 2) -> None:
         self._static = [(x.clone(), y.clone()) for x, y in batches]
-        state = [self.model.theta, self.velocity, self.theta_bf16]
+        state = [self.master, self.velocity, self.theta_bf16]
         saved = [t.clone() for t in state]
-        side = torch.cuda.Stream(self.model.theta.device)
+        side = torch.cuda.Stream(self.master.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # autograd / cuDNN warm-up outside the capture
             for _ in range(warmup):
@@ -855,7 +880,7 @@ class SubnetTrainer(_GradStore):
         for every worker).  The leaves are shared by the N workers;
         torch.autograd.grad returns each worker's gradients separately."""
         topo = self.model.topology
-        src = (self.theta_bf16 if self.autocast else self.model.theta).detach()
+        src = (self.theta_bf16 if self.autocast else self.master).detach()
         out = {}
         views = param_views(topo, src)
         conv_w = []
@@ -893,7 +918,7 @@ class SubnetTrainer(_GradStore):
             if self.compact:
                 sub = self.subs[w]
                 # the worker trains on the bf16 copy the previous sync wrote
-                src = self.theta_bf16 if self.autocast else self.model.theta
+                src = self.theta_bf16 if self.autocast else self.master
                 if self.slayout:  # the worker's blocks of the permuted theta
                     leaf = self.transfers[w].to_compact(src).requires_grad_(True)
                 else:
