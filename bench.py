@@ -261,9 +261,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # test hook: every rank on GPU 0 (CUDA IPC within one device) with gloo plumbing
+    # test hook: ranks share the visible GPUs round-robin (all on GPU 0 on a
+    # 1-GPU box: CUDA IPC within one device), gloo plumbing
     if os.environ.get("SDP_BENCH_SAME_DEVICE") == "1":
-        local = 0
+        local = local % torch.cuda.device_count()
     backend = os.environ.get("SDP_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define SDP_ABI_VERSION 1
+#define SDP_ABI_VERSION 2
 
 /* status codes (errors.py:8-45) */
 #define SDP_OK 0
@@ -175,6 +175,10 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
 #define SDP_SYNC_CHECK_FINITE 0x4    /* optim.py:79-80 isfinite(gbar) -> status */
 #define SDP_SYNC_NESTEROV 0x8        /* fused optim.py:81-84 update on theta/vel */
 #define SDP_SYNC_ADAM 0x10           /* fused optim.py:101-109 update on theta/m/v */
+#define SDP_SYNC_LOCAL_UPDATE 0x20   /* NESTEROV / ADAM run as a third phase on the
+                                        rank's local workers' (compact) state, after
+                                        the exit barrier, instead of in the leader's
+                                        epilogue on one flat theta */
 
 /* status word bits written (atomicOr) by the kernel */
 #define SDP_STATUS_UNCOVERED_LEAK 0x1
@@ -221,7 +225,40 @@ typedef struct {
    * it back after its exit barrier, so the launch can be replayed from a
    * CUDA graph; `epoch` above is then ignored. */
   uint32_t* epoch_counters;
+  /* compact owned-block storage, optional (SURVEY §7 hard part 7): worker w
+   * keeps only the tiles whose owner union contains w; its replica / bf16
+   * shadow of tile t starts at element slots[w * slot_stride + t] * tile of
+   * its (compact) buffer, -1 = not stored.  NULL = every replica is the flat
+   * [d] layout (tile t at t * tile).  These are the per-owner offsets of the
+   * block descriptors: one int32 per (worker, tile). */
+  const int32_t* slots;
+  int64_t slot_stride;
+  /* SDP_SYNC_LOCAL_UPDATE: CTA b applies the optimizer to
+   * updates[b * updates_per_cta ...] (len 0 = hole) after its exit barrier --
+   * exactly the tiles whose leader ran in CTA b on some rank, so the pairwise
+   * per-CTA barrier already orders their write-back before the update. */
+  const struct sdp_update_desc* updates;
+  int32_t updates_per_cta;
+  int32_t pad2_;
+  const struct sdp_worker_state* states;  /* device array indexed by sdp_update_desc.state */
 } sdp_sync_args;
+
+/* One local worker's optimizer state, all in its compact storage layout. */
+typedef struct sdp_worker_state {
+  void* theta;          /* dtype, compact */
+  void* velocity;       /* Nesterov v / Adam m */
+  void* second_moment;  /* Adam v (NULL for Nesterov) */
+  void* theta_bf16;     /* bf16 training copy, or NULL */
+  const void* grad;     /* the worker's replica: holds the mean after the sync */
+} sdp_worker_state;
+
+/* One stored tile of one local worker: elements [slot*tile, slot*tile+len). */
+typedef struct sdp_update_desc {
+  uint32_t state;
+  uint32_t slot;
+  uint32_t len;
+  uint32_t pad_;
+} sdp_update_desc;
 
 /* Launch the owner-subset sync.  For every element j with owner set O_j:
  *   acc = +0; for w in O_j ascending: acc += replicas[w][j];

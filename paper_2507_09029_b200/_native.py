@@ -15,7 +15,7 @@ from pathlib import Path
 from .errors import STATUS_CLASSES, NativeLibraryMissing, SubnetError
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libsdp.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_WORKERS = 64
 
 # status words (SDP_STATUS_*)
@@ -29,6 +29,7 @@ SYNC_CHECK_UNCOVERED = 0x2
 SYNC_CHECK_FINITE = 0x4
 SYNC_NESTEROV = 0x8
 SYNC_ADAM = 0x10
+SYNC_LOCAL_UPDATE = 0x20
 
 SCATTER_ZERO_FILL = 0x1
 SCATTER_ACCUMULATE = 0x2
@@ -99,7 +100,19 @@ class SyncArgs(C.Structure):
         ("one_minus_beta2", C.c_double), ("bias1", C.c_double), ("bias2", C.c_double),
         ("eps", C.c_double),
         ("epoch_counters", C.c_void_p),
+        ("slots", C.c_void_p), ("slot_stride", C.c_int64),
+        ("updates", C.c_void_p), ("updates_per_cta", C.c_int32), ("pad2_", C.c_int32),
+        ("states", C.c_void_p),
     ]
+
+
+class WorkerState(C.Structure):
+    _fields_ = [("theta", C.c_void_p), ("velocity", C.c_void_p), ("second_moment", C.c_void_p),
+                ("theta_bf16", C.c_void_p), ("grad", C.c_void_p)]
+
+
+class UpdateDesc(C.Structure):
+    _fields_ = [("state", C.c_uint32), ("slot", C.c_uint32), ("len", C.c_uint32), ("pad_", C.c_uint32)]
 
 
 VP, I32, I64, U64, DBL = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double

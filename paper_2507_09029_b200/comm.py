@@ -106,14 +106,15 @@ class PeerGroup:
 
     def __init__(self, assignment, rank: int, world: int, device, all_gather,
                  dtype=torch.float32, shadows: bool = True, max_grid: int | None = None,
-                 timeout_cycles: int = 20_000_000_000, owner_mask: torch.Tensor | None = None):
+                 timeout_cycles: int = 20_000_000_000, owner_mask: torch.Tensor | None = None,
+                 compact: bool = False):
+        """compact: every worker's replica (and shadow) holds only the tiles it
+        owns (storage.CompactLayout); the kernel finds each owner's copy of a
+        tile through the slot table (sdp_sync_args.slots)."""
         self.assignment = assignment
         self.layout = rank_layout(assignment.n_workers, world, rank)
         self.device = torch.device(device)
         d = assignment.topology.total
-        self.replicas = {w: torch.zeros(d, dtype=dtype, device=self.device) for w in self.layout.local_workers}
-        self.shadows = ({w: torch.zeros(d, dtype=torch.bfloat16, device=self.device)
-                         for w in self.layout.local_workers} if shadows else {})
         # owner_mask: the sync-space mask of a layout.SyncLayout when replicas are
         # kept window-class-major (width-wise assignments)
         self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True, max_grid=max_grid,
@@ -123,6 +124,14 @@ class PeerGroup:
         if self.plan.grid != self.grid:
             self.plan = SyncPlan(assignment, world=world, rank=rank, resident=True,
                                  force_grid=self.grid, owner_mask=owner_mask)
+        self.compact = None
+        if compact:
+            from .storage import CompactLayout
+            self.compact = CompactLayout(self.plan)
+        size = {w: (self.compact.length(w) if self.compact else d) for w in self.layout.local_workers}
+        self.replicas = {w: torch.zeros(size[w], dtype=dtype, device=self.device) for w in self.layout.local_workers}
+        self.shadows = ({w: torch.zeros(size[w], dtype=torch.bfloat16, device=self.device)
+                         for w in self.layout.local_workers} if shadows else {})
         self.pad = torch.zeros(self.grid * PAD_WORDS_PER_CTA, dtype=torch.int32, device=self.device)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._imported: list[int] = []
@@ -157,6 +166,9 @@ class PeerGroup:
         # in a CUDA graph replays with fresh flag values every time
         self.epochs = torch.zeros(self.grid, dtype=torch.int32, device=self.device)
         self.args.epoch_counters = self.epochs.data_ptr()
+        if self.compact is not None:
+            self.args.slots = self.compact.slots.data_ptr()
+            self.args.slot_stride = self.compact.slot_stride
         self._fn = N.lib().sdp_owner_sync
 
     def launch(self, stream=None) -> None:

@@ -59,6 +59,9 @@ __device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
                : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+// Coherent (L2) loads of data another CTA / GPU wrote during this launch.
+__device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // Peer (NVLink) replicas may be written by the peer between launches, so the
 // non-coherent path is only valid within one launch -- which is all we need:
 // every launch is bracketed by the cross-GPU barrier.

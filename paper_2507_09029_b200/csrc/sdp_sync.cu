@@ -81,7 +81,7 @@ __device__ __forceinline__ __nv_bfloat16 to_bf16(double x) { return __double2bfl
 __device__ __forceinline__ bool finite(float x) { return isfinite(x); }
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 
-// Kernel parameter block (lives in the constant bank; ~1.2 KB).
+// Kernel parameter block (lives in the constant bank; ~1.3 KB).
 struct SyncParams {
   const void* owner_mask;
   const sdp_tile_desc* tiles;
@@ -99,6 +99,11 @@ struct SyncParams {
   double beta1, beta2, omb1, omb2, bias1, bias2, eps;   // Adam scalars
   int64_t total;
   int64_t timeout_cycles;
+  const int32_t* slots;                                 // compact storage (or null)
+  int64_t slot_stride;
+  const sdp_update_desc* updates;                       // LOCAL_UPDATE phase
+  const sdp_worker_state* states;
+  int32_t updates_per_cta;
   int32_t n_workers, tile, n_tiles, tiles_per_cta, flags, rank, world;
   uint32_t epoch;
   bool has_shadow;
@@ -151,6 +156,12 @@ __device__ __forceinline__ void optim_step(const SyncParams& p, T g, T& th, T& s
   }
 }
 
+// The leader's epilogue applies the optimizer to the flat theta only when the
+// update is not a separate local phase.
+__device__ __forceinline__ bool epilogue_optim(const SyncParams& p) {
+  return (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) && !(p.flags & SDP_SYNC_LOCAL_UPDATE);
+}
+
 template <typename T>
 __device__ __forceinline__ void nesterov_elem(const SyncParams& p, int64_t j, T g) {
   T* th = static_cast<T*>(p.theta);
@@ -164,57 +175,84 @@ __device__ __forceinline__ void nesterov_elem(const SyncParams& p, int64_t j, T 
   if (p.theta_bf16) static_cast<__nv_bfloat16*>(p.theta_bf16)[j] = to_bf16(t);
 }
 
-template <typename T>
-__device__ __forceinline__ void emit_scalar(const SyncParams& p, int64_t j, uint64_t m, T mean);
-
-// Scalar path: one element, owner set `m` (partial tiles, unaligned tails).
-template <typename T>
-__device__ __forceinline__ void sync_elem(const SyncParams& p, int64_t j, uint64_t m, uint32_t& st) {
-  T acc = static_cast<T>(0);
-  for (uint64_t b = m; b; b &= b - 1) {
-    const int w = __ffsll(static_cast<long long>(b)) - 1;
-    acc = add_rn(acc, static_cast<const T*>(p.replicas[w])[j]);
-  }
-  const int c = __popcll(m);
-  const T mean = div_rn(acc, static_cast<T>(c > 0 ? c : 1));
-  if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
-    for (int w = 0; w < p.n_workers; ++w)
-      if (!finite(static_cast<const T*>(p.replicas[w])[j])) st |= SDP_STATUS_UNCOVERED_LEAK;
-  }
-  if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean)) st |= SDP_STATUS_NONFINITE;
-  emit_scalar<T>(p, j, m, mean);
+// Replica / shadow of worker w for tile `tix`: the flat layout (tile tix at
+// tix*tile) or the compact owned-tile layout (slot table); null = not stored.
+template <typename T, bool CS>
+__device__ __forceinline__ T* rep_tile(const SyncParams& p, int w, uint32_t tix) {
+  T* base = static_cast<T*>(p.replicas[w]);
+  if constexpr (!CS) return base + static_cast<int64_t>(tix) * p.tile;
+  const int32_t sl = __ldg(p.slots + static_cast<int64_t>(w) * p.slot_stride + tix);
+  return sl < 0 ? nullptr : base + static_cast<int64_t>(sl) * p.tile;
+}
+template <bool CS>
+__device__ __forceinline__ __nv_bfloat16* shadow_tile(const SyncParams& p, int w, uint32_t tix) {
+  __nv_bfloat16* base = static_cast<__nv_bfloat16*>(p.shadow[w]);
+  if (!base) return nullptr;
+  if constexpr (!CS) return base + static_cast<int64_t>(tix) * p.tile;
+  const int32_t sl = __ldg(p.slots + static_cast<int64_t>(w) * p.slot_stride + tix);
+  return sl < 0 ? nullptr : base + static_cast<int64_t>(sl) * p.tile;
 }
 
-// Epilogue for one element with owner set `m`.
-template <typename T>
-__device__ __forceinline__ void emit_scalar(const SyncParams& p, int64_t j, uint64_t m, T mean) {
+// Epilogue for one element (tile tix, flat start s, offset o) with owner set m.
+template <typename T, bool CS>
+__device__ __forceinline__ void emit_scalar(const SyncParams& p, uint32_t tix, int64_t s, int o, uint64_t m,
+                                            T mean) {
+  const int64_t j = s + o;
   if (p.out) static_cast<T*>(p.out)[j] = mean;
   if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[j] = to_bf16(mean);
   if (p.flags & SDP_SYNC_WRITEBACK) {
     for (uint64_t b = m; b; b &= b - 1) {
       const int w = __ffsll(static_cast<long long>(b)) - 1;
-      static_cast<T*>(p.replicas[w])[j] = mean;
-      if (p.has_shadow && p.shadow[w]) static_cast<__nv_bfloat16*>(p.shadow[w])[j] = to_bf16(mean);
+      rep_tile<T, CS>(p, w, tix)[o] = mean;
+      if (p.has_shadow) {
+        __nv_bfloat16* sh = shadow_tile<CS>(p, w, tix);
+        if (sh) sh[o] = to_bf16(mean);
+      }
     }
   }
-  if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) nesterov_elem<T>(p, j, mean);
+  if (epilogue_optim(p)) nesterov_elem<T>(p, j, mean);
+}
+
+// Scalar path: one element, owner set `m` (partial tiles, unaligned tails).
+template <typename T, bool CS>
+__device__ __forceinline__ void sync_elem(const SyncParams& p, uint32_t tix, int64_t s, int o, uint64_t m,
+                                          uint32_t& st) {
+  T acc = static_cast<T>(0);
+  for (uint64_t b = m; b; b &= b - 1) {
+    const int w = __ffsll(static_cast<long long>(b)) - 1;
+    acc = add_rn(acc, rep_tile<const T, CS>(p, w, tix)[o]);
+  }
+  const int c = __popcll(m);
+  const T mean = div_rn(acc, static_cast<T>(c > 0 ? c : 1));
+  if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+    for (int w = 0; w < p.n_workers; ++w) {
+      const T* g = rep_tile<const T, CS>(p, w, tix);
+      if (g && !finite(g[o])) st |= SDP_STATUS_UNCOVERED_LEAK;
+    }
+  }
+  if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean)) st |= SDP_STATUS_NONFINITE;
+  emit_scalar<T, CS>(p, tix, s, o, m, mean);
 }
 
 // Epilogue for one vector of VN consecutive elements with a common owner set.
-template <typename T>
-__device__ __forceinline__ void emit_vec(const SyncParams& p, int64_t j, uint64_t bits,
+template <typename T, bool CS>
+__device__ __forceinline__ void emit_vec(const SyncParams& p, uint32_t tix, int64_t s, int o, uint64_t bits,
                                          const typename V<T>::type& mean) {
   constexpr int VN = V<T>::N;
+  const int64_t j = s + o;
   if (p.out) V<T>::st(static_cast<T*>(p.out) + j, mean);
   if (p.out_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.out_bf16) + j, mean);
   if (p.flags & SDP_SYNC_WRITEBACK) {
     for (uint64_t b = bits; b; b &= b - 1) {
       const int w = __ffsll(static_cast<long long>(b)) - 1;
-      V<T>::st(static_cast<T*>(p.replicas[w]) + j, mean);
-      if (p.has_shadow && p.shadow[w]) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.shadow[w]) + j, mean);
+      V<T>::st(rep_tile<T, CS>(p, w, tix) + o, mean);
+      if (p.has_shadow) {
+        __nv_bfloat16* sh = shadow_tile<CS>(p, w, tix);
+        if (sh) V<T>::st_bf16(sh + o, mean);
+      }
     }
   }
-  if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
+  if (epilogue_optim(p)) {
     T* thp = static_cast<T*>(p.theta) + j;
     T* s1p = static_cast<T*>(p.velocity) + j;
     T* s2p = p.second_moment ? static_cast<T*>(p.second_moment) + j : nullptr;
@@ -231,8 +269,8 @@ __device__ __forceinline__ void emit_vec(const SyncParams& p, int64_t j, uint64_
 
 // Uniform tile: every element has owner set `bits`.  R vectors per thread per
 // round, owners consumed two at a time so 2R 16-B loads are in flight.
-template <typename T, int R>
-__device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s, uint64_t bits,
+template <typename T, int R, bool CS>
+__device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, uint32_t tix, int64_t s, uint64_t bits,
                                                   uint32_t& st) {
   constexpr int VN = V<T>::N;
   using Vt = typename V<T>::type;
@@ -245,9 +283,9 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
     for (int k = 0; k < R; ++k)
 #pragma unroll
       for (int e = 0; e < VN; ++e) acc[k].x[e] = static_cast<T>(0);
-    int64_t jv[R];
+    int ov[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) jv[k] = s + r0 + (k * kSyncThreads + threadIdx.x) * VN;
+    for (int k = 0; k < R; ++k) ov[k] = r0 + (k * kSyncThreads + threadIdx.x) * VN;
     // Owners in ascending order, K at a time: all K*R 16-B loads of a batch are
     // issued before the first add (K = 2 for R >= 2, 4 for R = 1: fits the
     // 64-register budget of 4 resident CTAs per SM without spills).
@@ -261,14 +299,14 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
         on[q] = b != 0;
         const int w = on[q] ? __ffsll(static_cast<long long>(b)) - 1 : 0;
         if (on[q]) b &= b - 1;
-        g[q] = static_cast<const T*>(p.replicas[w]);
+        g[q] = on[q] ? rep_tile<const T, CS>(p, w, tix) : nullptr;
       }
       Vt a[K][R];
 #pragma unroll
       for (int q = 0; q < K; ++q)
 #pragma unroll
         for (int k = 0; k < R; ++k)
-          if (on[q]) a[q][k] = V<T>::ld(g[q] + jv[k]);
+          if (on[q]) a[q][k] = V<T>::ld(g[q] + ov[k]);
 #pragma unroll
       for (int q = 0; q < K; ++q)
         if (on[q]) {
@@ -288,13 +326,15 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
       }
       if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
         for (int w = 0; w < p.n_workers; ++w) {
-          Vt g = V<T>::ld(static_cast<const T*>(p.replicas[w]) + jv[k]);
+          const T* gw = rep_tile<const T, CS>(p, w, tix);
+          if (!gw) continue;
+          Vt g = V<T>::ld(gw + ov[k]);
 #pragma unroll
           for (int e = 0; e < VN; ++e)
             if (!finite(g.x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
         }
       }
-      emit_vec<T>(p, jv[k], bits, mean);
+      emit_vec<T, CS>(p, tix, s, ov[k], bits, mean);
     }
   }
 }
@@ -306,21 +346,21 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, int64_t s
 // per-lane predicates -- every load and store is a coalesced, predicated
 // access that touches only owned elements, and each element adds exactly its
 // own owners in ascending order.
-template <typename T, int MB, int R>
-__device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, uint64_t tile_union,
-                                                uint32_t& st) {
+template <typename T, int MB, int R, bool CS>
+__device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, uint32_t tix, int64_t s,
+                                                uint64_t tile_union, uint32_t& st) {
   constexpr int EL = 4;  // elements per thread per round
   using M = typename MaskT<MB>::T;
-  const M* mask = static_cast<const M*>(p.owner_mask);
+  const M* mask = static_cast<const M*>(p.owner_mask) + s;
   const bool wb = (p.flags & SDP_SYNC_WRITEBACK) != 0;
   for (int r0 = 0; r0 < p.tile; r0 += EL * kSyncThreads) {
-    int64_t j[EL];
+    int o[EL];
     uint64_t m[EL];
     T acc[EL];
 #pragma unroll
     for (int u = 0; u < EL; ++u) {
-      j[u] = s + r0 + u * kSyncThreads + threadIdx.x;
-      m[u] = static_cast<uint64_t>(__ldg(mask + j[u]));
+      o[u] = r0 + u * kSyncThreads + threadIdx.x;
+      m[u] = static_cast<uint64_t>(__ldg(mask + o[u]));
       acc[u] = static_cast<T>(0);
     }
     uint64_t b = tile_union;
@@ -330,13 +370,13 @@ __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, 
       const bool two = b != 0;
       const int w1 = two ? __ffsll(static_cast<long long>(b)) - 1 : w0;
       if (two) b &= b - 1;
-      const T* g0 = static_cast<const T*>(p.replicas[w0]);
-      const T* g1 = static_cast<const T*>(p.replicas[w1]);
+      const T* g0 = rep_tile<const T, CS>(p, w0, tix);
+      const T* g1 = rep_tile<const T, CS>(p, w1, tix);
       T a[EL], c[EL];
 #pragma unroll
       for (int u = 0; u < EL; ++u) {
-        a[u] = ((m[u] >> w0) & 1ull) ? __ldcs(g0 + j[u]) : static_cast<T>(0);
-        c[u] = (two && ((m[u] >> w1) & 1ull)) ? __ldcs(g1 + j[u]) : static_cast<T>(0);
+        a[u] = ((m[u] >> w0) & 1ull) ? __ldcs(g0 + o[u]) : static_cast<T>(0);
+        c[u] = (two && ((m[u] >> w1) & 1ull)) ? __ldcs(g1 + o[u]) : static_cast<T>(0);
       }
 #pragma unroll
       for (int u = 0; u < EL; ++u) {
@@ -351,51 +391,107 @@ __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, int64_t s, 
       mean[u] = div_rn(acc[u], static_cast<T>(cnt > 0 ? cnt : 1));
       if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean[u])) st |= SDP_STATUS_NONFINITE;
       if (cnt == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
-        for (int w = 0; w < p.n_workers; ++w)
-          if (!finite(static_cast<const T*>(p.replicas[w])[j[u]])) st |= SDP_STATUS_UNCOVERED_LEAK;
+        for (int w = 0; w < p.n_workers; ++w) {
+          const T* gw = rep_tile<const T, CS>(p, w, tix);
+          if (gw && !finite(gw[o[u]])) st |= SDP_STATUS_UNCOVERED_LEAK;
+        }
       }
-      if (p.out) static_cast<T*>(p.out)[j[u]] = mean[u];
-      if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[j[u]] = to_bf16(mean[u]);
+      if (p.out) static_cast<T*>(p.out)[s + o[u]] = mean[u];
+      if (p.out_bf16) static_cast<__nv_bfloat16*>(p.out_bf16)[s + o[u]] = to_bf16(mean[u]);
     }
     if (wb) {
       for (uint64_t bb = tile_union; bb; bb &= bb - 1) {
         const int w = __ffsll(static_cast<long long>(bb)) - 1;
-        T* rep = static_cast<T*>(p.replicas[w]);
-        __nv_bfloat16* sh = p.has_shadow ? static_cast<__nv_bfloat16*>(p.shadow[w]) : nullptr;
+        T* rep = rep_tile<T, CS>(p, w, tix);
+        __nv_bfloat16* sh = p.has_shadow ? shadow_tile<CS>(p, w, tix) : nullptr;
 #pragma unroll
         for (int u = 0; u < EL; ++u)
           if ((m[u] >> w) & 1ull) {
-            rep[j[u]] = mean[u];
-            if (sh) sh[j[u]] = to_bf16(mean[u]);
+            rep[o[u]] = mean[u];
+            if (sh) sh[o[u]] = to_bf16(mean[u]);
           }
       }
     }
-    if (p.flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
+    if (epilogue_optim(p)) {
 #pragma unroll
-      for (int u = 0; u < EL; ++u) nesterov_elem<T>(p, j[u], mean[u]);
+      for (int u = 0; u < EL; ++u) nesterov_elem<T>(p, s + o[u], mean[u]);
     }
   }
 }
 
-template <typename T, int MB, int R>
+template <typename T, int MB, int R, bool CS>
 __device__ __forceinline__ void run_tile(const SyncParams& p, const sdp_tile_desc& d, uint32_t& st) {
   const int len = static_cast<int>(d.len_flags & SDP_TILE_LEN_MASK);
   if (len == 0) return;
-  const int64_t s = static_cast<int64_t>(d.tile_index) * p.tile;
+  const uint32_t tix = d.tile_index;
+  const int64_t s = static_cast<int64_t>(tix) * p.tile;
   const bool uniform = (d.len_flags & SDP_TILE_UNIFORM) != 0;
   if (len == p.tile) {
-    if (uniform) sync_uniform_tile<T, R>(p, s, d.owner_bits, st);
-    else sync_mixed_tile<T, MB, (R > 2 ? 2 : R)>(p, s, d.owner_bits, st);
+    if (uniform) sync_uniform_tile<T, R, CS>(p, tix, s, d.owner_bits, st);
+    else sync_mixed_tile<T, MB, (R > 2 ? 2 : R), CS>(p, tix, s, d.owner_bits, st);
   } else {
     const typename MaskT<MB>::T* mask = static_cast<const typename MaskT<MB>::T*>(p.owner_mask);
     for (int e = threadIdx.x; e < len; e += kSyncThreads) {
       const uint64_t m = uniform ? d.owner_bits : static_cast<uint64_t>(mask[s + e]);
-      sync_elem<T>(p, s + e, m, st);
+      sync_elem<T, CS>(p, tix, s, e, m, st);
     }
   }
 }
 
-template <typename T, int MB, int R>
+// Third phase (SDP_SYNC_LOCAL_UPDATE): the optimizer on this rank's local
+// workers' stored tiles whose leader ran in this CTA index (on any rank).  The
+// gradient is the worker's own replica, which now holds the mean (written by
+// the leader, possibly over NVLink, ordered by the exit barrier): read through
+// L2 (ld.global.cg), never the non-coherent path.
+template <typename T>
+__device__ __forceinline__ void local_update(const SyncParams& p, uint32_t& st) {
+  constexpr int VN = V<T>::N;
+  using Vt = typename V<T>::type;
+  const sdp_update_desc* ud = p.updates + static_cast<int64_t>(blockIdx.x) * p.updates_per_cta;
+  for (int k = 0; k < p.updates_per_cta; ++k) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(ud + k));
+    const int len = static_cast<int>(raw.z);
+    if (len == 0) continue;
+    const sdp_worker_state& ws = p.states[raw.x];
+    const int64_t base = static_cast<int64_t>(raw.y) * p.tile;
+    T* th = static_cast<T*>(ws.theta) + base;
+    T* s1 = static_cast<T*>(ws.velocity) + base;
+    T* s2 = ws.second_moment ? static_cast<T*>(ws.second_moment) + base : nullptr;
+    const T* g = static_cast<const T*>(ws.grad) + base;
+    __nv_bfloat16* tb = ws.theta_bf16 ? static_cast<__nv_bfloat16*>(ws.theta_bf16) + base : nullptr;
+    const int nv = len / VN * VN;
+    for (int o = threadIdx.x * VN; o < nv; o += kSyncThreads * VN) {
+      Vt gv, tv = V<T>::ld_rw(th + o), v1 = V<T>::ld_rw(s1 + o), v2 = v1;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) gv.x[e] = ld_cg(g + o + e);
+      if (s2) v2 = V<T>::ld_rw(s2 + o);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(gv.x[e])) st |= SDP_STATUS_NONFINITE;
+        optim_step<T>(p, gv.x[e], tv.x[e], v1.x[e], v2.x[e]);
+      }
+      V<T>::st(s1 + o, v1);
+      if (s2) V<T>::st(s2 + o, v2);
+      V<T>::st(th + o, tv);
+      if (tb) V<T>::st_bf16(tb + o, tv);
+    }
+    for (int o = nv + threadIdx.x; o < len; o += kSyncThreads) {
+      const T gg = ld_cg(g + o);
+      T t = th[o], a = s1[o], b = s2 ? s2[o] : static_cast<T>(0);
+      if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(gg)) st |= SDP_STATUS_NONFINITE;
+      optim_step<T>(p, gg, t, a, b);
+      s1[o] = a;
+      if (s2) s2[o] = b;
+      th[o] = t;
+      if (tb) tb[o] = to_bf16(t);
+    }
+  }
+}
+
+// CS: compact owned-tile storage (slot table); LU: the SDP_SYNC_LOCAL_UPDATE
+// phase.  Both are template flags so the plain flat sync keeps its lean,
+// spill-free code (a runtime slot-table branch cost it 2% at C4).
+template <typename T, int MB, int R, bool CS, bool LU>
 __global__ void __launch_bounds__(kSyncThreads, 4)
 k_owner_sync(const __grid_constant__ SyncParams p) {
   __shared__ alignas(16) sdp_tile_desc s_desc[kStage];
@@ -415,33 +511,37 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
       d.owner_bits = (static_cast<uint64_t>(raw.y) << 32) | raw.x;
       d.tile_index = raw.z;
       d.len_flags = raw.w;
-      run_tile<T, MB, R>(p, d, st);
+      run_tile<T, MB, R, CS>(p, d, st);
     }
-    if (st && p.status) atomicOr(p.status, st);
-    if (p.world > 1) cross_rank_barrier(p, 2u * ep + 2u);
-    if (p.epoch_ctr && threadIdx.x == 0) p.epoch_ctr[blockIdx.x] = ep;
-    return;
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  for (int k0 = 0; k0 < count; k0 += kStage) {
-    const int nk = min(kStage, count - k0);
+  } else {
     if (threadIdx.x == 0) {
-      const uint32_t bytes = static_cast<uint32_t>(nk * sizeof(sdp_tile_desc));
-      mbar_arrive_expect_tx(&s_bar, bytes);
-      bulk_g2s(s_desc, p.tiles + first + k0, bytes, &s_bar);
+      mbar_init(&s_bar, 1);
+      fence_mbar_init();
     }
-    mbar_wait(&s_bar, phase);
-    phase ^= 1;
-    for (int k = 0; k < nk; ++k) run_tile<T, MB, R>(p, s_desc[k], st);
-    __syncthreads();  // s_desc is overwritten by the next stage
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int k0 = 0; k0 < count; k0 += kStage) {
+      const int nk = min(kStage, count - k0);
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = static_cast<uint32_t>(nk * sizeof(sdp_tile_desc));
+        mbar_arrive_expect_tx(&s_bar, bytes);
+        bulk_g2s(s_desc, p.tiles + first + k0, bytes, &s_bar);
+      }
+      mbar_wait(&s_bar, phase);
+      phase ^= 1;
+      for (int k = 0; k < nk; ++k) run_tile<T, MB, R, CS>(p, s_desc[k], st);
+      __syncthreads();  // s_desc is overwritten by the next stage
+    }
+  }
+  bool ok = true;
+  if (p.world > 1) ok = cross_rank_barrier(p, 2u * ep + 2u);
+  if constexpr (LU) {
+    if (ok) {
+      if (p.world == 1) __syncthreads();  // this CTA's own write-back is the only producer
+      local_update<T>(p, st);
+    }
   }
   if (st && p.status) atomicOr(p.status, st);
-  if (p.world > 1) cross_rank_barrier(p, 2u * ep + 2u);
   if (p.epoch_ctr && threadIdx.x == 0) p.epoch_ctr[blockIdx.x] = ep;
 }
 
@@ -507,13 +607,23 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
     return set_error(SDP_ERR_USAGE, "output buffers are not 16-byte aligned");
   if ((a->flags & SDP_SYNC_NESTEROV) && (a->flags & SDP_SYNC_ADAM))
     return set_error(SDP_ERR_CONFIG, "choose one fused optimizer: Nesterov or Adam");
-  if (a->flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
+  const bool local_update = (a->flags & SDP_SYNC_LOCAL_UPDATE) != 0;
+  if (local_update) {
+    if (!(a->flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)))
+      return set_error(SDP_ERR_CONFIG, "SDP_SYNC_LOCAL_UPDATE needs SDP_SYNC_NESTEROV or SDP_SYNC_ADAM");
+    if (a->updates_per_cta < 0 || (a->updates_per_cta > 0 && (!a->updates || !a->states)))
+      return set_error(SDP_ERR_USAGE, "local update phase needs its update table and worker states");
+    if (a->updates && !aligned16(a->updates)) return set_error(SDP_ERR_USAGE, "update table must be 16-byte aligned");
+    if (!a->slots) return set_error(SDP_ERR_USAGE, "SDP_SYNC_LOCAL_UPDATE runs on compact storage: slots is NULL");
+  } else if (a->flags & (SDP_SYNC_NESTEROV | SDP_SYNC_ADAM)) {
     if (!a->theta || !a->velocity || !aligned16(a->theta) || !aligned16(a->velocity))
       return set_error(SDP_ERR_USAGE, "fused optimizer needs 16-byte aligned theta and moment buffers");
   }
-  if (a->flags & SDP_SYNC_ADAM) {
+  if ((a->flags & SDP_SYNC_ADAM) && !local_update) {
     if (!a->second_moment || !aligned16(a->second_moment))
       return set_error(SDP_ERR_USAGE, "fused Adam needs a 16-byte aligned second-moment buffer");
+  }
+  if (a->flags & SDP_SYNC_ADAM) {
     if (!(a->bias1 > 0.0) || !(a->bias2 > 0.0))
       return set_error(SDP_ERR_CONFIG, "Adam bias corrections must be positive (step >= 1)");
   }
@@ -559,6 +669,13 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   p.world = a->world;
   p.epoch = a->epoch;
   p.epoch_ctr = a->world > 1 ? a->epoch_counters : nullptr;
+  p.slots = a->slots;
+  p.slot_stride = a->slot_stride;
+  p.updates = local_update ? a->updates : nullptr;
+  p.states = local_update ? a->states : nullptr;
+  p.updates_per_cta = local_update ? a->updates_per_cta : 0;
+  if (a->slots && a->slot_stride < (a->total + a->tile - 1) / a->tile)
+    return set_error(SDP_ERR_USAGE, "slot_stride %lld is below the tile count", (long long)a->slot_stride);
 
   const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
   cudaStream_t s = as_stream(stream);
@@ -567,11 +684,21 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   const int vn = a->dtype == SDP_DTYPE_F32 ? 4 : 2;
   const int rounds = a->tile / (vn * kSyncThreads);
   const int R = rounds % 4 == 0 ? 4 : (rounds % 2 == 0 ? 2 : 1);
-#define SDP_SYNC_LAUNCH(T, MB)                                                    \
-  switch (R) {                                                                    \
-    case 4: k_owner_sync<T, MB, 4><<<grid, kSyncThreads, 0, s>>>(p); break;       \
-    case 2: k_owner_sync<T, MB, 2><<<grid, kSyncThreads, 0, s>>>(p); break;       \
-    default: k_owner_sync<T, MB, 1><<<grid, kSyncThreads, 0, s>>>(p); break;      \
+  // the compact / local-update instantiations run at most R = 2 (register budget)
+  const bool compact = a->slots != nullptr;
+#define SDP_SYNC_LAUNCH(T, MB)                                                              \
+  if (local_update) {                                                                       \
+    if (R >= 2) k_owner_sync<T, MB, 2, true, true><<<grid, kSyncThreads, 0, s>>>(p);         \
+    else k_owner_sync<T, MB, 1, true, true><<<grid, kSyncThreads, 0, s>>>(p);                \
+  } else if (compact) {                                                                     \
+    if (R >= 2) k_owner_sync<T, MB, 2, true, false><<<grid, kSyncThreads, 0, s>>>(p);        \
+    else k_owner_sync<T, MB, 1, true, false><<<grid, kSyncThreads, 0, s>>>(p);               \
+  } else {                                                                                  \
+    switch (R) {                                                                            \
+      case 4: k_owner_sync<T, MB, 4, false, false><<<grid, kSyncThreads, 0, s>>>(p); break;  \
+      case 2: k_owner_sync<T, MB, 2, false, false><<<grid, kSyncThreads, 0, s>>>(p); break;  \
+      default: k_owner_sync<T, MB, 1, false, false><<<grid, kSyncThreads, 0, s>>>(p); break; \
+    }                                                                                       \
   }
   if (a->dtype == SDP_DTYPE_F32) {
     switch (mb) {

@@ -28,6 +28,7 @@ import torch
 from . import _native as N
 from ._device import device, ptr, sdp_dtype, stream_ptr, upload_struct
 from .errors import NumericalError, ProtocolError, UsageError
+from .storage import dispatch_order, leader_cta
 
 TILE = 2048              # elements per sync tile (8 KB of fp32 per replica); measured
                          # best on B200 for 11M..268M buffers (tools/sync_probe.py)
@@ -149,10 +150,10 @@ class SyncPlan:
         self.n_uniform = int(((tiles["len_flags"] & N.TILE_UNIFORM) != 0).sum())
         nw = assignment.n_workers
         self.gpu_of_worker = gpu_of_worker(nw, world)
-        if world > 1:
-            mine = tiles[tile_leaders(tiles, self.gpu_of_worker, world) == rank]
-        else:
-            mine = tiles
+        self.leaders = (tile_leaders(tiles, self.gpu_of_worker, world) if world > 1
+                        else np.zeros(len(tiles), dtype=np.int64))
+        self.order = order
+        mine = tiles[self.leaders == rank] if world > 1 else tiles
         if tile_lo is not None or tile_hi is not None:  # a chunk of the vector (pipelined host path)
             lo, hi = tile_lo or 0, n_tiles if tile_hi is None else tile_hi
             mine = mine[(mine["tile_index"] >= lo) & (mine["tile_index"] < hi)]
@@ -160,16 +161,7 @@ class SyncPlan:
         # lane-per-element mixed tiles are the slow ones, so they go out in the
         # first wave instead of forming the tail (same-box A/B, tools/c3_ab.py:
         # C3 sync layout 63.6 -> 60.1 us, C2 unchanged)
-        if order != "index":
-            uni = (mine["len_flags"] & N.TILE_UNIFORM) != 0
-            if order == "mixed_first":
-                key = uni.astype(np.int64)
-            elif order == "cost":  # heaviest first: owners read, x5 for lane-per-element tiles
-                pc = np.bitwise_count(mine["owner_bits"]).astype(np.int64)
-                key = -(pc * np.where(uni, 1, 5))
-            else:
-                raise ValueError(f"unknown tile order {order!r}")
-            mine = mine[np.argsort(key, kind="stable")]
+        mine = mine[dispatch_order(mine, order)]
         self.n_tiles = len(mine)
         # every CTA must be co-resident for the cross-rank flag barrier
         self.grid = plan_grid(self.n_tiles, _sm_count(), resident or world > 1,
@@ -191,6 +183,12 @@ class SyncPlan:
             padded[:d] = sum((m >> w) & 1 for w in range(assignment.n_workers))
         self.tile_owned = padded.view(-1, tile).sum(dim=1).cpu().numpy()
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
+
+    def leader_cta(self) -> np.ndarray:
+        """CTA index that reduces each tile on its leader rank (same grid on
+        every rank); the local-update phase of a compact trainer runs a tile's
+        optimizer step in that CTA index after the pairwise exit barrier."""
+        return leader_cta(self.all_tiles, self.leaders, self.world, self.grid, self.order)
 
     def worker_ranges(self, w: int) -> list[tuple[int, int]]:
         """Element ranges (start, length) of worker w's replica the kernel reads:
@@ -294,21 +292,30 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
           shadows_bf16=None, check_uncovered: bool = False, check_finite: bool = False,
           nesterov: dict | None = None, adam: dict | None = None,
           status: torch.Tensor | None = None, plan: SyncPlan | None = None,
-          zero_copy: bool = False) -> N.SyncArgs:
+          zero_copy: bool = False, compact=None, local_update: dict | None = None) -> N.SyncArgs:
     """zero_copy: replicas (and `out`) may be pinned host tensors, which the
-    kernel reads (writes) over PCIe through their unified addresses."""
+    kernel reads (writes) over PCIe through their unified addresses.
+    compact: a storage.CompactLayout of `plan` -- replica / shadow w holds only
+    the tiles w owns (length compact.length(w)).
+    local_update: {"states": device sdp_worker_state array, "updates": device
+    sdp_update_desc table, "per_cta": int} -- the Nesterov / Adam of `nesterov`
+    / `adam` (their scalars) applied to each worker's own state after the sync
+    (SDP_SYNC_LOCAL_UPDATE) instead of to one flat theta."""
     n, d = assignment.n_workers, assignment.topology.total
-    reps = _as_replica_list(replicas, n, d)
+    reps = _as_replica_list(replicas, n, d) if compact is None else list(replicas)
+    if compact is not None and len(reps) != n:
+        raise ProtocolError(f"owner sync received {len(reps)} replicas for {n} workers")
     dt = reps[0].dtype
     dev = assignment.device
 
     def placed(t):
         return t.device == dev or (zero_copy and _device_readable(t))
 
-    for r in reps:
-        if r.dtype != dt or r.numel() != d or not placed(r) or not _aligned(r):
+    for w, r in enumerate(reps):
+        size = d if compact is None else compact.length(w)
+        if r.dtype != dt or r.numel() != size or not placed(r) or not _aligned(r):
             raise UsageError("replicas must be contiguous, 16-byte aligned, same dtype, "
-                             f"[{d}] on {dev}" + (" or pinned host memory" if zero_copy else ""))
+                             f"[{size}] on {dev}" + (" or pinned host memory" if zero_copy else ""))
     if out is not None and not placed(out):
         raise UsageError(f"out must be on {dev}" + (" or in pinned host memory" if zero_copy else ""))
     plan = plan or assignment.sync_plan()
@@ -330,7 +337,7 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     if nesterov is not None and adam is not None:
         raise UsageError("choose one fused optimizer")
     opt = nesterov if nesterov is not None else adam
-    if opt is not None:
+    if opt is not None and local_update is None:
         keys = ("theta", "velocity") if nesterov is not None else ("theta", "m", "v")
         for k in keys:
             t = opt.get(k)
@@ -345,16 +352,21 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
         if t is not None and (t.dtype != want or t.numel() != d or not t.is_contiguous()):
             raise UsageError(f"{nm} must be a contiguous [{d}] {want} tensor")
     if shadows_bf16 is not None:
-        for sh in shadows_bf16:
-            if sh is not None and (sh.dtype != torch.bfloat16 or sh.numel() != d or sh.device != dev
+        for w, sh in enumerate(shadows_bf16):
+            size = d if compact is None else compact.length(w)
+            if sh is not None and (sh.dtype != torch.bfloat16 or sh.numel() != size or sh.device != dev
                                    or not sh.is_contiguous()):
-                raise UsageError(f"bf16 shadows must be contiguous [{d}] bfloat16 tensors on {dev}")
+                raise UsageError(f"bf16 shadows must be contiguous [{size}] bfloat16 tensors on {dev}")
+    if local_update is not None and nesterov is None and adam is None:
+        raise UsageError("local_update needs the nesterov= or adam= scalars")
+    flat_opt = local_update is None
     if nesterov is not None:
         flags |= N.SYNC_NESTEROV
-        a.theta = nesterov["theta"].data_ptr()
-        a.velocity = nesterov["velocity"].data_ptr()
-        tb = nesterov.get("theta_bf16")
-        a.theta_bf16 = None if tb is None else tb.data_ptr()
+        if flat_opt:
+            a.theta = nesterov["theta"].data_ptr()
+            a.velocity = nesterov["velocity"].data_ptr()
+            tb = nesterov.get("theta_bf16")
+            a.theta_bf16 = None if tb is None else tb.data_ptr()
         a.lr = float(nesterov["lr"])
         a.momentum = float(nesterov.get("momentum", 0.9))
     if adam is not None:
@@ -362,16 +374,25 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
         flags |= N.SYNC_ADAM
         b1, b2 = float(adam.get("beta1", 0.9)), float(adam.get("beta2", 0.999))
         t = int(adam["t"])
-        a.theta = adam["theta"].data_ptr()
-        a.velocity = adam["m"].data_ptr()
-        a.second_moment = adam["v"].data_ptr()
-        tb = adam.get("theta_bf16")
-        a.theta_bf16 = None if tb is None else tb.data_ptr()
+        if flat_opt:
+            a.theta = adam["theta"].data_ptr()
+            a.velocity = adam["m"].data_ptr()
+            a.second_moment = adam["v"].data_ptr()
+            tb = adam.get("theta_bf16")
+            a.theta_bf16 = None if tb is None else tb.data_ptr()
         a.lr = float(adam["lr"])
         a.beta1, a.beta2 = b1, b2
         a.one_minus_beta1, a.one_minus_beta2 = 1 - b1, 1 - b2
         a.bias1, a.bias2 = 1 - b1 ** t, 1 - b2 ** t
         a.eps = float(adam.get("eps", 1e-8))
+    if compact is not None:
+        a.slots = compact.slots.data_ptr()
+        a.slot_stride = compact.slot_stride
+    if local_update is not None:
+        flags |= N.SYNC_LOCAL_UPDATE
+        a.states = local_update["states"].data_ptr()
+        a.updates = local_update["updates"].data_ptr()
+        a.updates_per_cta = int(local_update["per_cta"])
     a.status = None if status is None else status.data_ptr()
     a.flags = flags
     return a

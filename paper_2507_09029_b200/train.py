@@ -25,7 +25,7 @@ import torch.nn.functional as F
 from . import _native as N
 from . import engine, masking, zoo
 from ._device import ptr, stream_ptr
-from .errors import NumericalError
+from .errors import NumericalError, UsageError
 from .models import _channels_last_bf16, group_norm
 from .topology import GlobalModel
 
@@ -973,12 +973,20 @@ class PeerTrainer(_GradStore):
 
     def __init__(self, model: GlobalModel, assignment, rank: int, world: int, device, all_gather,
                  lr: float = 0.1, momentum: float = 0.9, autocast: bool = True, loss_fn=None,
-                 timeout_cycles: int = 20_000_000_000, graphed: bool = False):
+                 timeout_cycles: int = 20_000_000_000, graphed: bool = False,
+                 compact_storage: bool | None = None):
         """graphed: capture the rank's whole step (local workers' fwd/bwd, the
         peer-mapped sync, the Nesterov updates) in one CUDA graph, as
         SubnetTrainer does.  The sync kernel keeps its cross-rank barrier
         epochs on the device (comm.PeerGroup.epochs), so replays stay in step
-        as long as every rank calls step() the same number of times."""
+        as long as every rank calls step() the same number of times.
+
+        compact_storage (default: on for block assignments): each local
+        worker keeps theta, velocity, the bf16 copy and its gradient replica
+        ONLY for the tiles it owns (storage.CompactLayout; dropped blocks have
+        no storage), and the step's optimizer runs inside the sync launch as
+        its local-update phase (SDP_SYNC_LOCAL_UPDATE): one libsdp launch per
+        rank per step for sync + Nesterov + bf16 cast."""
         from . import comm
         self.model, self.assignment = model, assignment
         self.lr, self.momentum, self.autocast = lr, momentum, autocast
@@ -987,6 +995,12 @@ class PeerTrainer(_GradStore):
         self.loss_fn = loss_fn or (lambda logits, y: F.cross_entropy(logits.float(), y))
         self.device = torch.device(device)
         self.compact = assignment.strategy == "neuron"
+        if compact_storage is None:
+            compact_storage = not self.compact
+        if compact_storage and self.compact:
+            raise UsageError("compact owned-tile storage covers block assignments; width-wise workers "
+                             "keep window-class-major replicas")
+        self.compact_storage = bool(compact_storage)
         self.slayout = None
         theta0 = model.theta.to(self.device)
         if self.compact:
@@ -996,15 +1010,21 @@ class PeerTrainer(_GradStore):
             theta0 = self.slayout.to_sync(theta0)
         self.group = comm.PeerGroup(assignment, rank, world, self.device, all_gather, shadows=False,
                                     timeout_cycles=timeout_cycles,
-                                    owner_mask=None if self.slayout is None else self.slayout.owner_mask)
+                                    owner_mask=None if self.slayout is None else self.slayout.owner_mask,
+                                    compact=self.compact_storage)
         self.local = self.group.layout.local_workers
         self.views = {w: assignment.worker_view(w) for w in self.local}
         if self.compact:
             self.subs = {w: SubnetLayout(assignment, w) for w in self.local}
             self.transfers = {w: WorkerTransfer(self.slayout, self.subs[w]) for w in self.local}
-        self.theta = {w: theta0.clone() for w in self.local}
-        self.velocity = {w: torch.zeros_like(theta0) for w in self.local}
-        self.theta_bf16 = {w: theta0.to(torch.bfloat16) for w in self.local}
+        if self.compact_storage:
+            lay = self.group.compact
+            self.theta = {w: lay.gather(w, theta0) for w in self.local}
+        else:
+            self.theta = {w: theta0.clone() for w in self.local}
+        del theta0
+        self.velocity = {w: torch.zeros_like(self.theta[w]) for w in self.local}
+        self.theta_bf16 = {w: self.theta[w].to(torch.bfloat16) for w in self.local}
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         # the gradient replicas are the peer-mapped ones; parameters of a
         # worker's dropped blocks are never written (the replica keeps zeros
@@ -1012,6 +1032,19 @@ class PeerTrainer(_GradStore):
         self.grads = self.group.replicas
         if not self.compact:
             self._live = {w: live_params(model.topology, self.views[w]) for w in self.local}
+        if self.compact_storage:
+            from .storage import worker_states
+            topo = model.topology
+            self._specs = {w: [topo.index[k] for k in self._live[w]] for w in self.local}
+            self._states = worker_states([(self.theta[w], self.velocity[w], None, self.theta_bf16[w],
+                                           self.grads[w]) for w in self.local], self.device)
+            self._updates, per_cta = lay.update_table(self.local, self.group.plan.leader_cta(), self.group.grid)
+            a = self.group.args
+            a.flags |= N.SYNC_NESTEROV | N.SYNC_LOCAL_UPDATE | N.SYNC_CHECK_FINITE
+            a.momentum = float(momentum)
+            a.updates = self._updates.data_ptr()
+            a.updates_per_cta = per_cta
+            a.states = self._states.data_ptr()
 
     def step(self, batches: dict) -> torch.Tensor:
         """batches: {local worker: (x, y)}; returns the local workers' mean loss."""
@@ -1048,7 +1081,54 @@ class PeerTrainer(_GradStore):
             self._static_loss = self._step_eager(self._static, cache=False)
         self._graph_lr = self.lr
 
+    def _step_compact_storage(self, batches: dict, cache: bool) -> torch.Tensor:
+        """Block workers on owned-tile storage: the live parameters are views
+        of the worker's compact bf16 copy (one contiguous range each), their
+        gradients go straight into the worker's compact fp32 replica, and ONE
+        sync launch per rank averages, applies Nesterov to every local owner's
+        compact theta / velocity and writes its bf16 copy."""
+        lay = self.group.compact
+        losses = []
+        for w in self.local:
+            x, y = batches[w]
+            src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
+            params = {}
+            for k, v in lay.views(w, src, self._specs[w]).items():
+                if self.autocast and v.dim() == 4:  # channels-last conv weights (cuDNN NHWC)
+                    v = v.contiguous(memory_format=torch.channels_last)
+                params[k] = v.requires_grad_(True)
+            if self.autocast and isinstance(self.model.arch, GPT2Small):
+                params["__wte_padded"] = _LinearCrossEntropy._padded(params["wte"].detach(), torch.bfloat16)
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
+                loss = self.loss_fn(self.model.arch.forward(params, x, self.views[w]), y)
+            names = self._live[w]
+            gs = torch.autograd.grad(loss, [params[k] for k in names])
+            slots = lay.views(w, self.grads[w], self._specs[w])
+            torch._foreach_copy_([slots[k] for k in names], list(gs))
+            losses.append(loss.detach())
+        self.group.args.lr = float(self.lr)
+        self.group.launch()  # sync + local Nesterov + bf16 cast, one launch
+        return torch.stack(losses).mean()
+
+    def check(self) -> None:
+        """Raise on a cross-rank barrier timeout or a non-finite mean (the
+        fused update cannot roll back: call it at every loss read)."""
+        self.group.check()
+        st = int(self.group.status.item()) | int(self.status.item())
+        if st & N.STATUS_NONFINITE:
+            self.group.status.zero_()
+            self.status.zero_()
+            raise NumericalError("training aborted: the aggregated gradient contains non-finite values")
+
+    def state_bytes(self) -> int:
+        """Bytes of this rank's per-worker training state (theta, velocity,
+        bf16 copy, gradient replica)."""
+        return sum(t.numel() * t.element_size() for w in self.local
+                   for t in (self.theta[w], self.velocity[w], self.theta_bf16[w], self.grads[w]))
+
     def _step_eager(self, batches: dict, cache: bool = True) -> torch.Tensor:
+        if self.compact_storage:
+            return self._step_compact_storage(batches, cache)
         topo = self.model.topology
         losses = []
         for w in self.local:
@@ -1078,14 +1158,18 @@ class PeerTrainer(_GradStore):
                 self._store_grads(w, names, gs)
             losses.append(loss.detach())
         self.group.launch()  # peer-mapped owner sync: replicas[w] <- mean on w's elements
-        for w in self.local:
+        for w in self.local:  # width-wise: replicas in the sync layout, update per worker
             N.call("sdp_nesterov_update", N.DTYPE_F32, self.theta[w].numel(), ptr(self.theta[w]),
                    ptr(self.velocity[w]), ptr(self.group.replicas[w]), float(self.lr), float(self.momentum),
                    ptr(self.theta_bf16[w]), ptr(self.status), stream_ptr(self.device))
         return torch.stack(losses).mean()
 
     def theta_of(self, w: int) -> torch.Tensor:
-        """Worker w's parameter copy in the reference's flat layout."""
+        """Worker w's parameter copy in the reference's flat layout (compact
+        storage: elements of tiles w does not store read 0)."""
+        if self.compact_storage:
+            d = self.model.topology.total
+            return self.group.compact.scatter(w, self.theta[w], torch.zeros(d, device=self.device))
         return self.slayout.from_sync(self.theta[w]) if self.slayout else self.theta[w]
 
     def close(self) -> None:

@@ -73,7 +73,11 @@ int main(void) {
   printf("sdp_group_desc %zu\n", sizeof(sdp_group_desc));
   F(sdp_sync_args, owner_mask) F(sdp_sync_args, replicas) F(sdp_sync_args, shadow_bf16)
   F(sdp_sync_args, lr) F(sdp_sync_args, status) F(sdp_sync_args, signal_pads)
-  F(sdp_sync_args, epoch) F(sdp_sync_args, timeout_cycles)
+  F(sdp_sync_args, epoch) F(sdp_sync_args, timeout_cycles) F(sdp_sync_args, epoch_counters)
+  F(sdp_sync_args, slots) F(sdp_sync_args, slot_stride) F(sdp_sync_args, updates)
+  F(sdp_sync_args, updates_per_cta) F(sdp_sync_args, states)
+  printf("sdp_worker_state %zu\n", sizeof(sdp_worker_state));
+  printf("sdp_update_desc %zu\n", sizeof(sdp_update_desc));
   F(sdp_slice_desc, rows) F(sdp_slice_desc, col_map) F(sdp_slice_desc, inner_shr)
   printf("sdp_slice_task %zu\n", sizeof(sdp_slice_task));
   return 0;
@@ -96,6 +100,8 @@ def test_struct_layouts_match_c(tmp_path):
     assert int(out["sdp_rule_desc"]) == C.sizeof(N.RuleDesc)
     assert int(out["sdp_group_desc"]) == C.sizeof(N.GroupDesc)
     assert int(out["sdp_slice_task"]) == C.sizeof(N.SliceTask) == 32
+    assert int(out["sdp_worker_state"]) == C.sizeof(N.WorkerState) == 40
+    assert int(out["sdp_update_desc"]) == C.sizeof(N.UpdateDesc) == 16
     from paper_2507_09029_b200.models import SLICE_DTYPE, TASK_DTYPE
     assert SLICE_DTYPE.itemsize == C.sizeof(N.SliceDesc) and TASK_DTYPE.itemsize == C.sizeof(N.SliceTask)
     for key, val in out.items():

@@ -1,5 +1,6 @@
 """bench.py's torchrun (N > 1) path end to end on ONE GPU: two ranks share
-device 0 (SDP_BENCH_SAME_DEVICE), plumbing over gloo, data path over CUDA IPC
+device 0 on a 1-GPU box (SDP_BENCH_SAME_DEVICE; ranks take GPUs round-robin when
+several are visible), plumbing over gloo, data path over CUDA IPC
 with the cross-rank flag barriers.  Timing is meaningless here (the two
 processes' kernels are time-sliced); the test checks the path runs and emits
 the contract's JSON line."""
@@ -25,7 +26,7 @@ def test_torchrun_two_ranks_same_device(cuda):
     env = dict(os.environ, SDP_BENCH_SAME_DEVICE="1", SDP_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "5", "--warmup", "3", "--train-steps", "2"]
+           "--gpus", "2", "--steps", "5", "--warmup", "3", "--train-steps", "2", "--workload", "resnet18"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]

@@ -22,7 +22,7 @@ CHILD = textwrap.dedent(r"""
     sys.path.insert(0, os.environ["REPO"])
     from paper_2507_09029_b200 import comm, masking, zoo
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(int(os.environ["RANK"]) % torch.cuda.device_count())  # own GPU when >= 2 are visible
     dist.init_process_group("gloo", rank=rank, world_size=world)
     def all_gather(obj):
         out = [None] * world
@@ -34,7 +34,7 @@ CHILD = textwrap.dedent(r"""
     if os.environ.get("LAYOUT") == "sync":
         from paper_2507_09029_b200.layout import SyncLayout
         lay = SyncLayout(a)
-    g = comm.PeerGroup(a, rank, world, torch.device("cuda", 0), all_gather, max_grid=4,
+    g = comm.PeerGroup(a, rank, world, torch.device("cuda", torch.cuda.current_device()), all_gather, max_grid=4,
                        timeout_cycles=10_000_000_000, owner_mask=None if lay is None else lay.owner_mask)
     gen = torch.Generator(device="cuda")
     for w, t in g.replicas.items():
@@ -113,13 +113,13 @@ TRAIN_CHILD = textwrap.dedent(r"""
     from paper_2507_09029_b200 import masking, train
     torch.backends.cudnn.deterministic = True
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(int(os.environ["RANK"]) % torch.cuda.device_count())  # own GPU when >= 2 are visible
     dist.init_process_group("gloo", rank=rank, world_size=world)
     def all_gather(obj):
         out = [None] * world
         dist.all_gather_object(out, obj)
         return out
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", torch.cuda.current_device())
     model = train.build_resnet18(dev, seed=5)
     a = masking.build_assignment(model.topology, os.environ["STRATEGY"], 4, 2, seed=1)
     tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=os.environ["AUTOCAST"] == "1",
@@ -211,7 +211,7 @@ LOCAL_CHILD = textwrap.dedent(r"""
     sys.path.insert(0, os.environ["REPO"])
     from paper_2507_09029_b200 import comm, masking, zoo
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(int(os.environ["RANK"]) % torch.cuda.device_count())  # own GPU when >= 2 are visible
     dist.init_process_group("gloo", rank=rank, world_size=world)
     topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (32, 32))
     a = masking.build_assignment(topo, os.environ["STRATEGY"], 4, 2, seed=1)
