@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--no-memory-ranks", action="store_true")
+    ap.add_argument("--memory-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -353,16 +355,22 @@ def run_ours(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
                 if not peaks.get("_fallback") else "fallback 6.65 TB/s (B200_PROFILING.md)"}
     if world > 1:
-        roofline.update(meta.get("roofline", {}))
-        # per direction each GPU carries ~ its own peer reads + peer writes
-        # (peers write into it what it writes to them); measured P2P peak 770 GB/s
-        nvl = meta.get("roofline", {}).get("nvlink_bytes_per_launch", 0)
-        roofline["nvlink_achieved_GBps"] = nvl / (float(times.mean()) / 1e3) / 1e9
-        roofline["nvlink_peak_GBps"] = 770.0
-        roofline["nvlink_frac"] = roofline["nvlink_achieved_GBps"] / 770.0
-        roofline["nvlink_peak_source"] = "B200_PROFILING.md measured peer copy per direction (900 nominal)"
-        probe = meta.get("roofline", {}).get("p2p_copy_GBps_measured")
-        if probe:  # this run's own ring peer-copy probe (all ranks at once)
+        rl = meta.get("roofline", {})
+        roofline.update(rl)
+        t_s = ms / 1e3  # the slowest rank's launch time (the collective ends with it)
+        # SURVEY §8(d) busbw: sum over my elements of 2(k-1)/k * 4 B, k = owner GPUs
+        busbw = rl.get("busbw_bytes_per_launch", 0) / t_s / 1e9
+        probe = rl.get("p2p_copy_GBps_measured")
+        roofline["busbw_GBps"] = busbw
+        roofline["busbw_frac_900"] = busbw / 900.0
+        roofline["busbw_frac_probe"] = busbw / probe if probe else None
+        # what the ports actually carried, per direction (the leader's peer
+        # reads and its writes of the mean + bf16 shadow, both ways)
+        link = max(rl.get("nvlink_tx_bytes_per_launch", 0), rl.get("nvlink_rx_bytes_per_launch", 0))
+        roofline["nvlink_achieved_GBps"] = link / t_s / 1e9
+        roofline["nvlink_frac"] = roofline["nvlink_achieved_GBps"] / 900.0
+        roofline["nvlink_peak_source"] = "900 GB/s per direction (NVLink 5 nominal); *_probe: this run's peer-copy probe"
+        if probe:
             roofline["nvlink_frac_of_run_probe"] = roofline["nvlink_achieved_GBps"] / probe
 
     e2e = None
@@ -375,6 +383,8 @@ def run_ours(args):
         e2e = run_e2e(args, a, dev, total_bytes)
         if not args.no_train and args.workload in ("gpt2", "resnet18"):
             train = {"c4_gpt2": run_train_gpt2(args, dev), "c2_c3_resnet18": run_train(args, dev)}
+            if not args.no_memory_ranks and args.n_logical == 8:
+                train["memory_n8_ranks"] = run_memory_ranks(args)
             if args.n_logical == 8 and args.p == 4:
                 c1 = argparse.Namespace(**{**vars(args), "n_logical": 4, "p": 2})
                 train["c1_mini_resnet"] = run_train_c1(c1, dev)
@@ -500,27 +510,14 @@ def run_train(args, dev):
         out[f"{tag}_ms_per_step"] = ms
         out[f"{tag}_samples_per_s_per_gpu"] = n * batch / (ms / 1e3)
         out[f"{tag}_loss_last"] = float(loss.item())
-        mems = [train.worker_memory(model, a, w if p < n else None, batch, dev)["peak_bytes"]
-                for w in (range(n) if p < n else [0])]
-        out[f"{tag}_peak_mem_per_worker_bytes"] = max(mems)  # the GPU that needs the most
-        out[f"{tag}_peak_mem_mean_bytes"] = float(np.mean(mems))  # the paper's per-worker average
+        tr.check()
         del tr, model, a
         torch.cuda.empty_cache()
-    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
-    out["mem_reduction_vs_dp_mean"] = 1 - out["subnet_peak_mem_mean_bytes"] / out["dp_peak_mem_per_worker_bytes"]
     out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
-    out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_worker_bytes"]
-                                            / out["dp_peak_mem_per_worker_bytes"])
-    out["widthwise_mem_reduction_vs_dp_mean"] = (1 - out["widthwise_peak_mem_mean_bytes"]
-                                                 / out["dp_peak_mem_per_worker_bytes"])
     out["configs"] = {"subnet": "configs[1] C2: block dropping P=4", "widthwise": "configs[2] C3: "
                       "channel-slice compact subnetworks (gather/scatter kernels) P=4",
                       "dp": "full-replica DP comparator (P=N)"}
-    out["note"] = ("peak memory = one worker's compact fp32 master + grad + momentum + bf16 copy + "
-                   "activations of its fwd/bwd, i.e. what a GPU holding that worker needs (N = G); "
-                   "*_peak_mem_per_worker_bytes / mem_reduction_vs_dp: the largest worker (block "
-                   "sizes are unequal: the window holding layer4.1 keeps most parameters); "
-                   "*_mean: averaged over the N workers, as PAPER.md reports per-worker savings")
+    out["memory"] = "peak memory per GPU: train.memory_n8_ranks (measured in 8 real rank processes)"
     return out
 
 
@@ -613,8 +610,8 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
     one process per GPU, the N = 8 workers placed contiguously (N/G per rank),
     train.PeerTrainer (local fwd/bwd, peer-mapped owner sync, local fused
     Nesterov + bf16 cast).  CUDA events over the timed steps, max over ranks;
-    peak memory = the largest local worker's step (train.worker_memory), max
-    over ranks."""
+    peak memory = torch.cuda.max_memory_allocated of each rank process over
+    its steps (after the full init vector is freed), max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -639,12 +636,15 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
         model = train.build_resnet18(dev)
         a = masking.build_assignment(model.topology, strategy, n, p, seed=1)
         tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.02, graphed=True)
+        model.theta = None  # the full init vector: the rank keeps only its workers' state
         gen = torch.Generator(device=dev)
         batches = {}
         for w in tr.local:
             gen.manual_seed(w)
             batches[w] = (torch.randn(batch, 3, 32, 32, generator=gen, device=dev),
                           torch.randint(0, 10, (batch,), generator=gen, device=dev))
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
         out[f"{tag}_loss_first"] = rmax(tr.step(batches).item())
         tr.step(batches)
         torch.cuda.synchronize()
@@ -661,16 +661,14 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
         out[f"{tag}_ms_per_step"] = ms
         out[f"{tag}_samples_per_s_per_gpu"] = n * batch / (ms / 1e3) / world
         out[f"{tag}_loss_last"] = rmax(loss.item())
-        mem = max(train.worker_memory(model, a, w if p < n else None, batch, dev)["peak_bytes"]
-                  for w in (tr.local if p < n else tr.local[:1]))
-        out[f"{tag}_peak_mem_per_worker_bytes"] = int(rmax(mem))
+        out[f"{tag}_peak_mem_per_gpu_bytes"] = int(rmax(torch.cuda.max_memory_allocated(dev)))
         tr.close()
         del tr, model, a
         torch.cuda.empty_cache()
         dist.barrier()
-    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
-    out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_worker_bytes"]
-                                            / out["dp_peak_mem_per_worker_bytes"])
+    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_gpu_bytes"] / out["dp_peak_mem_per_gpu_bytes"]
+    out["widthwise_mem_reduction_vs_dp"] = (1 - out["widthwise_peak_mem_per_gpu_bytes"]
+                                            / out["dp_peak_mem_per_gpu_bytes"])
     out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
     # configs[3] C4 at G GPUs: GPT-2 small, seq 1024, micro-batch 8 per worker
     g4 = {"workload": f"GPT-2 small 124M, seq 1024, N={n} workers on {world} GPUs x micro-batch 8, "
@@ -680,12 +678,15 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
         a = masking.build_assignment(model.topology, "block", n, p, seed=1)
         tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=1e-4, loss_fn=train.lm_loss,
                                graphed=True)
+        model.theta = None
         gen = torch.Generator(device=dev)
         batches = {}
         for w in tr.local:
             gen.manual_seed(w)
             t = torch.randint(0, 50257, (8, 1024), generator=gen, device=dev)
             batches[w] = (t, t)
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
         tr.step(batches)
         torch.cuda.synchronize()
         dist.barrier()
@@ -702,11 +703,13 @@ def run_train_multi(args, dev, rank: int, world: int, red_dev):
         g4[f"{tag}_ms_per_step"] = ms
         g4[f"{tag}_tokens_per_s_per_gpu"] = n * 8 * 1024 / (ms / 1e3) / world
         g4[f"{tag}_loss_last"] = rmax(loss.item())
+        g4[f"{tag}_peak_mem_per_gpu_bytes"] = int(rmax(torch.cuda.max_memory_allocated(dev)))
         tr.close()
         del tr, model, a
         torch.cuda.empty_cache()
         dist.barrier()
     g4["speedup_vs_dp_per_step"] = g4["dp_ms_per_step"] / g4["subnet_ms_per_step"]
+    g4["mem_reduction_vs_dp"] = 1 - g4["subnet_peak_mem_per_gpu_bytes"] / g4["dp_peak_mem_per_gpu_bytes"]
     out["c4_gpt2"] = g4
     return out
 
@@ -743,18 +746,11 @@ def run_train_gpt2(args, dev, micro_batch: int = 8, seq: int = 1024):
         out[f"{tag}_ms_per_step"] = ms
         out[f"{tag}_tokens_per_s_per_gpu"] = n * micro_batch * seq / (ms / 1e3)
         out[f"{tag}_loss_last"] = float(loss.item())
-        del tr
+        tr.check()
+        del tr, model, a
         torch.cuda.empty_cache()
-        mk = lambda: (batches[0][0], batches[0][1])  # noqa: E731
-        mems = [train.worker_memory(model, a, w if p < n else None, micro_batch, dev, mk, train.lm_loss)["peak_bytes"]
-                for w in (range(n) if p < n else (0,))]
-        out[f"{tag}_peak_mem_per_worker_bytes"] = max(mems)
-        out[f"{tag}_peak_mem_mean_bytes"] = float(np.mean(mems))
-        del model, a
-        torch.cuda.empty_cache()
-    out["mem_reduction_vs_dp"] = 1 - out["subnet_peak_mem_per_worker_bytes"] / out["dp_peak_mem_per_worker_bytes"]
-    out["mem_reduction_vs_dp_mean"] = 1 - out["subnet_peak_mem_mean_bytes"] / out["dp_peak_mem_per_worker_bytes"]
     out["speedup_vs_dp_per_step"] = out["dp_ms_per_step"] / out["subnet_ms_per_step"]
+    out["memory"] = "peak memory per GPU: train.memory_n8_ranks (measured in 8 real rank processes)"
     return out
 
 
@@ -838,8 +834,118 @@ def run_cpu_baseline(args, topo):
             "ms_per_call": dt * 1e3}, a
 
 
+def run_memory_child(args):
+    """One rank of the N = G = 8 memory run (launched by run_memory_ranks):
+    train.PeerTrainer with ONE worker on this rank, compact owned-tile
+    storage, fused sync + Nesterov + bf16 cast; peak = this process's
+    torch.cuda.max_memory_allocated over the training steps (all live state:
+    compact theta / velocity / bf16 copy / gradient replica, activations,
+    scratch), after the initial full theta that built the model was freed.
+    Subnet (P = 4) and full-replica DP (P = N = 8) run the same steps on the
+    same per-rank batches; their losses are reported side by side."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_09029_b200 import _native, masking, train
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _native.load()
+    dist.init_process_group("gloo")
+
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    res = {}
+    steps = max(2, args.train_steps // 2)
+    for wl in ("gpt2", "resnet18"):
+        for tag, p in (("subnet", args.p), ("dp", world)):
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            model = train.build_gpt2(dev) if wl == "gpt2" else train.build_resnet18(dev)
+            a = masking.build_assignment(model.topology, "block", world, p, seed=1)
+            kw = {"loss_fn": train.lm_loss, "lr": 1e-4} if wl == "gpt2" else {"lr": 0.02}
+            tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, graphed=False,
+                                   timeout_cycles=60_000_000_000, **kw)
+            model.theta = None  # the full init vector: every rank now holds only its compact state
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(rank)
+            if wl == "gpt2":
+                t = torch.randint(0, 50257, (8, 1024), generator=gen, device=dev)
+                batches = {w: (t, t) for w in tr.local}
+            else:
+                batches = {w: (torch.randn(64, 3, 32, 32, generator=gen, device=dev),
+                               torch.randint(0, 10, (64,), generator=gen, device=dev)) for w in tr.local}
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats(dev)
+            losses = []
+            for _ in range(steps):
+                losses.append(float(tr.step(batches).item()))
+            torch.cuda.synchronize()
+            tr.check()
+            res[f"{wl}_{tag}"] = {"peak_bytes": int(torch.cuda.max_memory_allocated(dev)),
+                                  "state_bytes": int(tr.state_bytes()),
+                                  "stored_params": int(sum(tr.theta[w].numel() for w in tr.local)),
+                                  "losses": losses}
+            tr.close()
+            del tr, model, a, batches
+            dist.barrier()
+    allr = all_gather(res)
+    if rank == 0:
+        print("MEMORY_RANKS " + json.dumps(allr), flush=True)
+    dist.destroy_process_group()
+
+
+def run_memory_ranks(args, world: int = 8) -> dict:
+    """BASELINE metric part 3 on the system that runs: peak memory per GPU at
+    N = G = 8 (one worker per rank), measured by torch.cuda.max_memory_allocated
+    inside each of 8 real PeerTrainer processes (torchrun, CUDA-IPC peer
+    mapping, the fused sync kernel with its cross-process barrier).  On a
+    1-GPU box the 8 processes share the device (time-sliced), which changes
+    nothing about each process's own allocations; step time is not measured
+    here."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, SDP_BENCH_SAME_DEVICE="1", SDP_DIST_BACKEND="gloo", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--memory-child",
+           "--p", str(args.p), "--train-steps", str(args.train_steps)]
+    import subprocess
+    t0 = time.perf_counter()
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    line = next((ln for ln in r.stdout.splitlines() if ln.startswith("MEMORY_RANKS ")), None)
+    if r.returncode != 0 or line is None:
+        return {"error": (r.stdout[-1500:] + r.stderr[-1500:])}
+    ranks = json.loads(line[len("MEMORY_RANKS "):])
+    out = {"how": f"{world} PeerTrainer processes (one worker each, N = G = {world}), compact owned-tile storage, "
+                  "fused sync+Nesterov+bf16; torch.cuda.max_memory_allocated per process over the training "
+                  "steps; ranks share one GPU here (time-sliced)",
+           "wall_s": round(time.perf_counter() - t0, 1)}
+    for key in ranks[0]:
+        peaks = [rk[key]["peak_bytes"] for rk in ranks]
+        out[key] = {"peak_bytes_max": max(peaks), "peak_bytes_mean": float(np.mean(peaks)),
+                    "peak_bytes_per_rank": peaks,
+                    "state_bytes_max": max(rk[key]["state_bytes"] for rk in ranks),
+                    "loss_per_step_rank_mean": [float(np.mean([rk[key]["losses"][i] for rk in ranks]))
+                                                for i in range(len(ranks[0][key]["losses"]))]}
+    for wl in ("gpt2", "resnet18"):
+        sub, dp = out[f"{wl}_subnet"], out[f"{wl}_dp"]
+        out[f"{wl}_mem_reduction_vs_dp"] = 1 - sub["peak_bytes_max"] / dp["peak_bytes_max"]
+        out[f"{wl}_mem_reduction_vs_dp_mean"] = 1 - sub["peak_bytes_mean"] / dp["peak_bytes_mean"]
+    return out
+
+
 def main():
     args = parse()
+    if args.memory_child:
+        run_memory_child(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

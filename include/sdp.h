@@ -162,9 +162,11 @@ typedef struct {
 
 /* Classify every tile of the flat vector (warp-shuffle AND/OR reduction).
  * tiles (device, out): ceil(total / tile) descriptors in tile order.
+ * owned (device, out, nullable): per tile, sum over its elements of |O_j|
+ * (the coverage sum, masking.py:203, without a [d] coverage table).
  * tile must be a multiple of 1024 and <= 1<<20. */
 int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
-                   int tile, sdp_tile_desc* tiles, void* stream);
+                   int tile, sdp_tile_desc* tiles, int64_t* owned, void* stream);
 
 #define SDP_DTYPE_F32 0
 #define SDP_DTYPE_F64 1

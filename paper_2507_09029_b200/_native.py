@@ -144,7 +144,7 @@ SIGNATURES = {
     "sdp_permutation": (C.c_int, [C.POINTER(C.c_uint32), I32, VP, I32, I32, VP, VP]),
     "sdp_build_masks": (C.c_int, [VP, I32, VP, I32, VP, I32, I64, VP, I32, VP, VP, VP, VP, VP, VP]),
     "sdp_worker_mask": (C.c_int, [VP, I32, I64, I32, VP, VP, VP]),
-    "sdp_plan_tiles": (C.c_int, [VP, I32, I64, I32, VP, VP]),
+    "sdp_plan_tiles": (C.c_int, [VP, I32, I64, I32, VP, VP, VP]),
     "sdp_owner_sync": (C.c_int, [C.POINTER(SyncArgs), VP]),
     "sdp_nesterov_update": (C.c_int, [I32, I64, VP, VP, VP, DBL, DBL, VP, VP, VP]),
     "sdp_check_finite": (C.c_int, [I32, I64, VP, VP, VP]),

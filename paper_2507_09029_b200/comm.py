@@ -286,10 +286,10 @@ def bench_setup(assignment, rank: int, world: int, device):
     torch.cuda.synchronize(device)
     dist.barrier()
     own = g.plan.owned_elems
-    nvl = _nvlink_bytes(g.plan, g.layout)
+    lb = link_bytes(g.plan, g.layout, shadows=True)
     meta = {"tiles": g.plan.n_tiles, "grid": g.grid, "tiles_per_cta": g.plan.tiles_per_cta,
-            "roofline": {"nvlink_bytes_per_launch": nvl,
-                         "nvlink_note": "bytes this rank moves over NVLink per launch (peer reads + peer writes)",
+            "roofline": {"nvlink_tx_bytes_per_launch": lb["tx"], "nvlink_rx_bytes_per_launch": lb["rx"],
+                         "busbw_bytes_per_launch": busbw_bytes(g.plan, g.layout),
                          "p2p_copy_GBps_measured": p2p}}
     return g.launch, own * 4, own * 10, meta
 
@@ -326,14 +326,44 @@ def p2p_copy_probe(rank: int, world: int, device, all_gather, mib: int = 512, re
     return gbps
 
 
-def _nvlink_bytes(plan: SyncPlan, layout: RankLayout) -> int:
-    """Peer bytes the leader moves: 4 B read + 6 B written per non-local owner."""
-    tiles = plan.mine
-    if len(tiles) == 0:
-        return 0
+def link_bytes(plan: SyncPlan, layout: RankLayout, shadows: bool) -> dict:
+    """Bytes this rank's NVLink ports carry per launch, per direction.  The
+    leader of a tile reads 4 B per element from every remote owner (their TX,
+    its RX) and writes 4 B (+ 2 B bf16 shadow) to every remote owner (its TX,
+    their RX); summed over every rank's led tiles (plan.leaders)."""
+    tiles = plan.all_tiles
     lens = (tiles["len_flags"] & N.TILE_LEN_MASK).astype(np.int64)
-    remote = np.zeros(len(tiles), dtype=np.int64)
+    bits = tiles["owner_bits"].astype(np.uint64)
+    me = layout.rank
+    wb = 4 + (2 if shadows else 0)
+    mine_remote = np.zeros(len(tiles), dtype=np.int64)   # my workers among the tile's owners
+    remote = np.zeros(len(tiles), dtype=np.int64)        # owners not on the leader's GPU
+    leader = plan.leaders
     for w in range(layout.n_workers):
-        if int(layout.gpu_of[w]) != layout.rank:
-            remote += ((tiles["owner_bits"] >> np.uint64(w)) & np.uint64(1)).astype(np.int64)
-    return int((lens * remote).sum() * 10)
+        on = ((bits >> np.uint64(w)) & np.uint64(1)).astype(bool)
+        g = int(layout.gpu_of[w])
+        remote += (on & (leader != g)).astype(np.int64)
+        if g == me:
+            mine_remote += (on & (leader != me)).astype(np.int64)
+    led = leader == me
+    rx = int((lens * remote)[led].sum() * 4 + (lens * mine_remote)[~led].sum() * wb)
+    tx = int((lens * remote)[led].sum() * wb + (lens * mine_remote)[~led].sum() * 4)
+    return {"tx": tx, "rx": rx}
+
+
+def busbw_bytes(plan: SyncPlan, layout: RankLayout) -> int:
+    """SURVEY §8(d) bus bytes of this rank per sync (the nccl-tests busbw
+    convention): sum over the elements j this rank's GPU owns of
+    2(k_j - 1)/k_j * 4 B, k_j = number of distinct GPUs owning j.  Tiles are
+    counted with their owner union (uniform tiles exactly; the few mixed
+    tiles of a block assignment approximately)."""
+    tiles = plan.all_tiles
+    lens = (tiles["len_flags"] & N.TILE_LEN_MASK).astype(np.float64)
+    bits = tiles["owner_bits"].astype(np.uint64)
+    gmask = np.zeros(len(tiles), dtype=np.int64)
+    for w in range(layout.n_workers):
+        on = ((bits >> np.uint64(w)) & np.uint64(1)).astype(bool)
+        gmask[on] |= 1 << int(layout.gpu_of[w])
+    k = np.bitwise_count(gmask.astype(np.uint64)).astype(np.float64)
+    mine = ((gmask >> layout.rank) & 1).astype(bool) & (k > 0)
+    return int((2 * (k[mine] - 1) / k[mine] * lens[mine] * 4).sum())

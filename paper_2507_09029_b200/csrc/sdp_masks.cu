@@ -668,7 +668,8 @@ __global__ void k_worker_mask(const typename MaskT<MB>::T* __restrict__ owner_ma
 // One warp per tile: uniform iff AND == OR over the tile's owner sets.
 template <int MB>
 __global__ void k_plan_tiles(const typename MaskT<MB>::T* __restrict__ owner_mask, int64_t total,
-                             int tile, int64_t n_tiles, sdp_tile_desc* __restrict__ tiles) {
+                             int tile, int64_t n_tiles, sdp_tile_desc* __restrict__ tiles,
+                             int64_t* __restrict__ owned) {
   using M = typename MaskT<MB>::T;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -677,6 +678,7 @@ __global__ void k_plan_tiles(const typename MaskT<MB>::T* __restrict__ owner_mas
     const int64_t s = t * tile;
     const int len = static_cast<int>(min(static_cast<int64_t>(tile), total - s));
     uint64_t a = ~0ull, o = 0;
+    uint32_t cnt = 0;  // sum of |O_j| over the tile (<= 2^20 * 64)
     const M* base = owner_mask + s;
     if (len == tile) {
       constexpr int per = 16 / MB;  // mask elements per 16-B vector
@@ -688,6 +690,7 @@ __global__ void k_plan_tiles(const typename MaskT<MB>::T* __restrict__ owner_mas
         for (int e = 0; e < per; ++e) {
           a &= static_cast<uint64_t>(m[e]);
           o |= static_cast<uint64_t>(m[e]);
+          cnt += __popcll(static_cast<uint64_t>(m[e]));
         }
       }
     } else {
@@ -695,7 +698,12 @@ __global__ void k_plan_tiles(const typename MaskT<MB>::T* __restrict__ owner_mas
         uint64_t m = static_cast<uint64_t>(base[e]);
         a &= m;
         o |= m;
+        cnt += __popcll(m);
       }
+    }
+    if (owned) {
+      const uint32_t c = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) owned[t] = c;
     }
     const uint32_t alo = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(a));
     const uint32_t ahi = __reduce_and_sync(0xffffffffu, static_cast<uint32_t>(a >> 32));
@@ -823,7 +831,7 @@ int sdp_worker_mask(const void* owner_mask, int mask_bytes, int64_t total, int w
 }
 
 int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total, int tile,
-                   sdp_tile_desc* tiles, void* stream) {
+                   sdp_tile_desc* tiles, int64_t* owned, void* stream) {
   if (check_mask_bytes(mask_bytes)) return SDP_ERR_CONFIG;
   if (tile < 1024 || tile > (1 << 20) || tile % 1024)
     return set_error(SDP_ERR_CONFIG, "tile must be a multiple of 1024 in [1024, 2^20], got %d", tile);
@@ -834,10 +842,10 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total, int ti
   const int grid = static_cast<int>(std::min<int64_t>((n_tiles + warps_per_cta - 1) / warps_per_cta, sm_count() * 8));
   cudaStream_t s = as_stream(stream);
   switch (mask_bytes) {
-    case 1: k_plan_tiles<1><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(owner_mask), total, tile, n_tiles, tiles); break;
-    case 2: k_plan_tiles<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(owner_mask), total, tile, n_tiles, tiles); break;
-    case 4: k_plan_tiles<4><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(owner_mask), total, tile, n_tiles, tiles); break;
-    default: k_plan_tiles<8><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(owner_mask), total, tile, n_tiles, tiles); break;
+    case 1: k_plan_tiles<1><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(owner_mask), total, tile, n_tiles, tiles, owned); break;
+    case 2: k_plan_tiles<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(owner_mask), total, tile, n_tiles, tiles, owned); break;
+    case 4: k_plan_tiles<4><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(owner_mask), total, tile, n_tiles, tiles, owned); break;
+    default: k_plan_tiles<8><<<grid, 256, 0, s>>>(static_cast<const uint64_t*>(owner_mask), total, tile, n_tiles, tiles, owned); break;
   }
   SDP_LAUNCH_CHECK();
   return SDP_OK;

@@ -143,9 +143,12 @@ class SyncPlan:
         self.owner_mask = assignment.owner_mask if owner_mask is None else owner_mask
         n_tiles = (d + tile - 1) // tile
         raw = torch.empty(max(1, n_tiles) * TILE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        owned = torch.zeros(max(1, n_tiles), dtype=torch.int64, device=dev)
         N.call("sdp_plan_tiles", ptr(self.owner_mask), assignment.mask_bytes, d, tile,
-               ptr(raw), stream_ptr(dev))
+               ptr(raw), ptr(owned), stream_ptr(dev))
         tiles = raw.cpu().numpy().view(TILE_DTYPE)[:n_tiles].copy()
+        # exact sum of |O_j| per tile (popcounts reduced in k_plan_tiles)
+        self.tile_owned = owned.cpu().numpy()[:n_tiles]
         self.all_tiles = tiles
         self.n_uniform = int(((tiles["len_flags"] & N.TILE_UNIFORM) != 0).sum())
         nw = assignment.n_workers
@@ -174,14 +177,6 @@ class SyncPlan:
             self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
         self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
-        # exact sum of |O_j| over this rank's elements (per-tile coverage sums)
-        padded = torch.zeros(max(1, n_tiles) * tile, dtype=torch.int64, device=dev)
-        if owner_mask is None:
-            padded[:d] = assignment.coverage
-        else:  # popcount of the permuted mask
-            m = self.owner_mask.to(torch.int64) & ((1 << assignment.n_workers) - 1)
-            padded[:d] = sum((m >> w) & 1 for w in range(assignment.n_workers))
-        self.tile_owned = padded.view(-1, tile).sum(dim=1).cpu().numpy()
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
     def leader_cta(self) -> np.ndarray:

@@ -149,21 +149,26 @@ class _DeviceTables:
 
 def _expand(topology: ModelTopology, tables: _DeviceTables, unit_bits: torch.Tensor,
             n_workers: int, dev: torch.device, *, want_param_masks: bool = False,
-            want_stats: bool = True):
-    """Run k_build_masks; returns dict of device tensors."""
+            want_stats: bool = True, want_owner: bool = True, want_counts: bool | None = None):
+    """Run k_build_masks; returns dict of device tensors.  want_stats: the
+    [d] coverage / divisor / governors tables (25 B per parameter);
+    want_counts (default: with the stats): per-worker active counts."""
     d = topology.total
     mb = mask_bytes_for(n_workers)
-    out = {"owner_mask": torch.empty(d, dtype=MASK_TORCH_DTYPE[mb], device=dev)}
+    out = {}
+    if want_owner:
+        out["owner_mask"] = torch.empty(d, dtype=MASK_TORCH_DTYPE[mb], device=dev)
     if want_param_masks:
         out["param_masks"] = torch.empty((n_workers, d), dtype=torch.bool, device=dev)
     if want_stats:
         out["coverage"] = torch.empty(d, dtype=torch.int64, device=dev)
         out["divisor"] = torch.empty(d, dtype=torch.float64, device=dev)
         out["governors"] = torch.empty(d, dtype=torch.int64, device=dev)
+    if want_stats if want_counts is None else want_counts:
         out["active_counts"] = torch.zeros(n_workers, dtype=torch.int64, device=dev)
     ub = unit_bits if unit_bits.numel() else torch.zeros(1, dtype=torch.int64, device=dev)
     N.call("sdp_build_masks", ptr(tables.params), tables.n_params, ptr(tables.rules),
-           tables.n_rules, ptr(ub), n_workers, d, ptr(out["owner_mask"]), mb,
+           tables.n_rules, ptr(ub), n_workers, d, ptr(out.get("owner_mask")), mb,
            ptr(out.get("param_masks")), ptr(out.get("coverage")), ptr(out.get("divisor")),
            ptr(out.get("governors")), ptr(out.get("active_counts")), stream_ptr(dev))
     return out
@@ -249,15 +254,46 @@ class _SubsetTopology:
 # MaskAssignment
 # ---------------------------------------------------------------------------
 
-@dataclass(frozen=True)
 class WorkerMaskView:
-    """Everything one worker needs to run a masked forward pass (masking.py:173-185)."""
+    """Everything one worker needs to run a masked forward pass (masking.py:173-185).
 
-    worker_id: int
-    param_mask: torch.Tensor       # float64 [d] on device, 0.0 / 1.0
-    param_mask_bool: torch.Tensor  # bool [d] on device
-    channel_active: dict           # layer id -> read-only numpy bool [C]
-    block_active: np.ndarray       # read-only numpy bool [num_blocks]
+    worker_id, channel_active (layer id -> read-only numpy bool [C]) and
+    block_active (read-only numpy bool [num_blocks]) are built at once; the
+    per-parameter masks param_mask (float64 [d], 0.0 / 1.0) and
+    param_mask_bool (bool [d]) are device tensors expanded by libsdp's
+    sdp_worker_mask on first access (9 B per parameter that a trainer, which
+    only needs the block / channel flags, never allocates)."""
+
+    __slots__ = ("worker_id", "channel_active", "block_active", "_owner_mask", "_mask_bytes", "_pm", "_pmb")
+
+    def __init__(self, worker_id, channel_active, block_active, *, owner_mask=None, mask_bytes=1,
+                 param_mask=None, param_mask_bool=None):
+        self.worker_id = worker_id
+        self.channel_active = channel_active
+        self.block_active = block_active
+        self._owner_mask, self._mask_bytes = owner_mask, mask_bytes
+        self._pm, self._pmb = param_mask, param_mask_bool
+
+    def _expand(self) -> None:
+        d = self._owner_mask.numel()
+        dev = self._owner_mask.device
+        mf = torch.empty(d, dtype=torch.float64, device=dev)
+        mu = torch.empty(d, dtype=torch.uint8, device=dev)
+        N.call("sdp_worker_mask", ptr(self._owner_mask), self._mask_bytes, d, self.worker_id, ptr(mf),
+               ptr(mu), stream_ptr(dev))
+        self._pm, self._pmb = read_only(mf), read_only(mu.view(torch.bool))
+
+    @property
+    def param_mask(self) -> torch.Tensor:
+        if self._pm is None:
+            self._expand()
+        return self._pm
+
+    @property
+    def param_mask_bool(self) -> torch.Tensor:
+        if self._pmb is None:
+            self._expand()
+        return self._pmb
 
     @property
     def active_params(self) -> int:
@@ -290,23 +326,24 @@ class MaskAssignment:
                 packed |= pm[w].to(torch.int64) << w
             self.owner_mask = packed.to(MASK_TORCH_DTYPE[mb]) if mb < 8 else packed
             self._param_masks = pm
-            self.coverage = pm.sum(dim=0, dtype=torch.int64)
-            self.divisor = self.coverage.clamp(min=1).to(torch.float64)
-            self.governors = torch.as_tensor(np.asarray(governors) if not torch.is_tensor(governors)
-                                             else governors).to(dev, dtype=torch.int64)
+            self._coverage = pm.sum(dim=0, dtype=torch.int64)
+            self._divisor = self._coverage.clamp(min=1).to(torch.float64)
+            self._governors = torch.as_tensor(np.asarray(governors) if not torch.is_tensor(governors)
+                                              else governors).to(dev, dtype=torch.int64)
             self._active_counts = pm.sum(dim=1, dtype=torch.int64)
         else:
+            # built on the device: only the 1-byte-per-parameter owner mask and
+            # the per-worker counts exist up front; the 25 B/parameter coverage /
+            # divisor / governors tables are expanded on first use (a training
+            # rank never needs them -- they were 3 GB per GPT-2 rank)
             self.owner_mask = _owner_mask
             self._param_masks = param_masks
-            self.coverage = _coverage
-            self.divisor = _divisor
-            self.governors = governors
+            self._coverage = _coverage
+            self._divisor = _divisor
+            self._governors = governors
             self._active_counts = _active_counts
         # the reference freezes these (masking.py:206-207): read-only views
         self.owner_mask = read_only(self.owner_mask)
-        self.coverage = read_only(self.coverage)
-        self.divisor = read_only(self.divisor)
-        self.governors = read_only(self.governors)
         self.mask_bytes = mask_bytes_for(self.n_workers)
         self._uncovered = None
         self._plans: dict = {}
@@ -315,6 +352,30 @@ class MaskAssignment:
     @property
     def device(self) -> torch.device:
         return self.owner_mask.device
+
+    def _stats(self) -> None:
+        if self._coverage is None or self._divisor is None or self._governors is None:
+            out = _expand(self.topology, self._tables, self._unit_bits, self.n_workers, self.device,
+                          want_owner=False, want_stats=True, want_counts=False)
+            self._coverage, self._divisor, self._governors = out["coverage"], out["divisor"], out["governors"]
+
+    @property
+    def coverage(self) -> torch.Tensor:
+        """int64 [d] owner count per parameter (masking.py:203)."""
+        self._stats()
+        return read_only(self._coverage)
+
+    @property
+    def divisor(self) -> torch.Tensor:
+        """float64 [d] max(coverage, 1) (masking.py:204)."""
+        self._stats()
+        return read_only(self._divisor)
+
+    @property
+    def governors(self) -> torch.Tensor:
+        """int64 [d] number of units governing each parameter (masking.py:288-302)."""
+        self._stats()
+        return read_only(self._governors)
 
     @property
     def unit_workers(self) -> dict[StructuralUnit, tuple[int, ...]]:
@@ -349,13 +410,14 @@ class MaskAssignment:
     @property
     def uncovered_params(self) -> int:
         if self._uncovered is None:
-            self._uncovered = int((self.coverage == 0).sum().item())
+            self._uncovered = int((self.owner_mask == 0).sum().item())
         return self._uncovered
 
     def owned_total(self) -> int:
-        """sum_j |O_j| -- replica elements one sync reads (cached)."""
+        """sum_j |O_j| -- replica elements one sync reads (cached; the per-worker
+        held counts sum to it, masking.py:442)."""
         if getattr(self, "_owned_total", None) is None:
-            self._owned_total = int(self.coverage.sum().item())
+            self._owned_total = int(self._active_counts.sum().item())
         return self._owned_total
 
     def host_divisor(self) -> np.ndarray:
@@ -384,12 +446,8 @@ class MaskAssignment:
         for arr in channel_active.values():
             arr.setflags(write=False)
         block_active.setflags(write=False)
-        d = self.topology.total
-        mf = torch.empty(d, dtype=torch.float64, device=self.device)
-        mu = torch.empty(d, dtype=torch.uint8, device=self.device)
-        N.call("sdp_worker_mask", ptr(self.owner_mask), self.mask_bytes, d, worker_id, ptr(mf),
-               ptr(mu), stream_ptr(self.device))
-        return WorkerMaskView(worker_id, mf, mu.view(torch.bool), channel_active, block_active)
+        return WorkerMaskView(worker_id, channel_active, block_active, owner_mask=self.owner_mask,
+                              mask_bytes=self.mask_bytes)
 
     def worker_views(self) -> list[WorkerMaskView]:
         return [self.worker_view(i) for i in range(self.n_workers)]
@@ -517,11 +575,11 @@ def build_assignment(topology: ModelTopology, strategy: str, n_workers: int, rep
     if any(size == 0 for _, size in t.groups):
         raise ConfigError("assign_grouped_units requires non-empty groups")
     unit_bits = _device_assign(t.groups, t.n_units, n_workers, replication, seed, dev)
-    out = _expand(topology, tables, unit_bits, n_workers, dev)
+    out = _expand(topology, tables, unit_bits, n_workers, dev, want_stats=False, want_counts=True)
     return MaskAssignment(
-        n_workers, replication, strategy, seed, topology, None, None, out["governors"],
-        _tables=tables, _owner_mask=out["owner_mask"], _coverage=out["coverage"],
-        _divisor=out["divisor"], _active_counts=out["active_counts"], _unit_bits=unit_bits)
+        n_workers, replication, strategy, seed, topology, None, None, None,
+        _tables=tables, _owner_mask=out["owner_mask"], _active_counts=out["active_counts"],
+        _unit_bits=unit_bits)
 
 
 @dataclass
@@ -636,12 +694,11 @@ def assignment_from_dict(doc: dict, topology: ModelTopology, device_=None) -> Ma
         bits[uid] = b
         unit_workers[unit] = ws
     ub = torch.from_numpy(bits.view(np.int64)).to(dev)
-    out = _expand(topology, tables, ub, n_workers, dev)
+    out = _expand(topology, tables, ub, n_workers, dev, want_stats=False, want_counts=True)
     return MaskAssignment(
         n_workers, int(doc["replication"]), strategy, int(doc.get("seed", 0)), topology,
-        unit_workers, None, out["governors"], _tables=tables, _owner_mask=out["owner_mask"],
-        _coverage=out["coverage"], _divisor=out["divisor"], _active_counts=out["active_counts"],
-        _unit_bits=ub)
+        unit_workers, None, None, _tables=tables, _owner_mask=out["owner_mask"],
+        _active_counts=out["active_counts"], _unit_bits=ub)
 
 
 def load_assignment(path, topology: ModelTopology, device_=None) -> MaskAssignment:

@@ -48,7 +48,7 @@ def test_status_codes_map_to_reference_exceptions():
     assert rc == 1
     with pytest.raises(E.ConfigError, match="replication"):
         N.check(rc)
-    rc = lib.sdp_plan_tiles(None, 3, 10, 4096, None, None)
+    rc = lib.sdp_plan_tiles(None, 3, 10, 4096, None, None, None)
     with pytest.raises(E.ConfigError, match="mask_bytes"):
         N.check(rc)
     a = N.SyncArgs()

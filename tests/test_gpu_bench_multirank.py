@@ -34,7 +34,8 @@ def test_torchrun_two_ranks_same_device(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["gpu_launches"] == 5 and d["value"] > 0
     assert "nvlink_frac" in d["roofline"] and d["roofline"]["p2p_copy_GBps_measured"] > 0
+    assert d["roofline"]["busbw_GBps"] > 0 and "busbw_frac_900" in d["roofline"] and "busbw_frac_probe" in d["roofline"]
     t = d["train"]  # PeerTrainer at world 2: C2 / C3 / DP samples/s and memory
     assert t["subnet_samples_per_s_per_gpu"] > 0 and t["widthwise_samples_per_s_per_gpu"] > 0
-    assert t["subnet_peak_mem_per_worker_bytes"] < t["dp_peak_mem_per_worker_bytes"]
+    assert t["subnet_peak_mem_per_gpu_bytes"] < t["dp_peak_mem_per_gpu_bytes"]
     assert t["c4_gpt2"]["subnet_tokens_per_s_per_gpu"] > 0 and t["c4_gpt2"]["dp_tokens_per_s_per_gpu"] > 0

@@ -50,3 +50,33 @@ def test_pool_concurrent_callers_get_distinct_buffers():
     for i in range(len(got)):
         for j in range(i + 1, len(got)):
             assert not np.shares_memory(got[i], got[j])
+
+
+def _fake_plan(owner_sets, tile_len, leaders):
+    import types
+
+    from paper_2507_09029_b200 import _native as N
+    dt = np.dtype([("owner_bits", "<u8"), ("tile_index", "<u4"), ("len_flags", "<u4")])
+    t = np.zeros(len(owner_sets), dtype=dt)
+    for i, ws in enumerate(owner_sets):
+        t[i] = (sum(1 << w for w in ws), i, tile_len | N.TILE_UNIFORM)
+    return types.SimpleNamespace(all_tiles=t, leaders=np.asarray(leaders))
+
+
+def test_busbw_and_link_bytes_accounting():
+    """busbw bytes = sum over my elements of 2(k-1)/k * 4 B
+    (k = owner GPUs); link bytes per direction = the leader's peer reads (4 B)
+    and its writes of the mean (+2 B shadow) to every remote owner."""
+    from paper_2507_09029_b200 import comm
+    lay = comm.rank_layout(8, 8, 0)  # one worker per GPU
+    plan = _fake_plan([(0, 1, 2, 3), (4, 5, 6, 7), tuple(range(8))], 1000, [0, 5, 1])
+    # rank 0 owns tiles 0 (k=4) and 2 (k=8)
+    assert comm.busbw_bytes(plan, lay) == int(2 * 3 / 4 * 1000 * 4 + 2 * 7 / 8 * 1000 * 4)
+    lb = comm.link_bytes(plan, lay, shadows=True)
+    # tile 0 led here: read 3 remote owners, write 3 x 6 B; tile 2 led by rank 1:
+    # rank 1 reads my copy (my TX 4 B) and writes the mean + shadow into it (my RX 6 B)
+    assert lb == {"rx": 3 * 1000 * 4 + 1000 * 6, "tx": 3 * 1000 * 6 + 1000 * 4}
+    lay2 = comm.rank_layout(8, 2, 0)  # workers 0-3 on GPU 0: tile 0 is GPU-local
+    plan2 = _fake_plan([(0, 1, 2, 3), (0, 4)], 1000, [0, 1])
+    assert comm.busbw_bytes(plan2, lay2) == int(2 * 1 / 2 * 1000 * 4)
+    assert comm.link_bytes(plan2, lay2, shadows=False) == {"rx": 1000 * 4, "tx": 1000 * 4}
