@@ -280,6 +280,9 @@ k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups
     const int2 gd = gi < kGroupStage ? s_groups[gi] : make_int2(groups[gi].first_unit, groups[gi].size);
     const int first = gd.x, n = gd.y;
     for (int k = threadIdx.x; k < n; k += blockDim.x) slot_of[first + k] = slot + k;
+    // every thread has read the previous group's s_i (its loop exit test)
+    // before thread 0 resets it (compute-sanitizer racecheck / synccheck)
+    __syncthreads();
     if (threadIdx.x == 0) {
       js[first] = -1;
       s_i = n - 1;
@@ -335,6 +338,7 @@ k_assign(SeedWords seed, const sdp_group_desc* __restrict__ groups, int n_groups
           i -= __popc(acc);
           p += consumed;
         }
+        __syncwarp();  // every lane of warp 0 read s_i / s_p at the top
         if (lane == 0) {
           s_i = i;
           s_p = p;
