@@ -377,24 +377,18 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
                        int groups, int max_group_channels, const void* gamma, const void* beta, float eps,
                        int flags, void* y_bf16, float* mean, float* rstd, void* stream);
 
-/* Backward of sdp_group_norm_fwd: dx (bf16, same layout); dgamma / dbeta fp32
- * [channels] are ACCUMULATED (zero them first). */
+/* Backward of sdp_group_norm_fwd: dx (bf16, same layout) and dgamma / dbeta
+ * [channels] WRITTEN in the affine dtype (SDP_GN_AFFINE_BF16: bf16, else
+ * fp32).  Deterministic: every CTA writes one partial row of fp32 dgamma /
+ * dbeta sums into `scratch` (no zeroing needed) and a second launch folds the
+ * rows in a fixed order -- no floating-point atomics, so repeated calls are
+ * bit-identical.  `scratch` holds at least sdp_group_norm_bwd_scratch(...)
+ * floats; calls sharing a scratch must be ordered (one stream).  batch > 0. */
+int sdp_group_norm_bwd_scratch(int batch, int hw, int channels, int max_group_channels, long long* floats);
 int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
                        int channels, const int32_t* group_starts, int groups, int max_group_channels,
                        const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
-                       float* dgamma, float* dbeta, void* stream);
-
-/* sdp_group_norm_bwd with the dgamma / dbeta epilogue fused: they
- * accumulate in `scratch` (2 x channels floats, zero between calls) and the
- * last CTA writes them to dgamma_out / dbeta_out in the affine dtype
- * (SDP_GN_AFFINE_BF16: bf16, else fp32), re-zeroes `scratch` and resets
- * `counter` (one uint32, zero between calls).  Calls sharing a scratch must
- * be ordered (one stream). */
-int sdp_group_norm_bwd_fused(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
-                             int channels, const int32_t* group_starts, int groups, int max_group_channels,
-                             const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
-                             void* dgamma_out, void* dbeta_out, float* scratch, unsigned int* counter,
-                             void* stream);
+                       void* dgamma, void* dbeta, float* scratch, long long scratch_floats, void* stream);
 
 /* Row LayerNorm on bf16 [rows, cols] activations, cols a multiple of 256 (up
  * to 2048 forward, 1024 backward): the GPT-2 blocks of the C4 training step

@@ -125,9 +125,9 @@ SIGNATURES = {
     "sdp_host_ptr_on_device": (C.c_int, [VP, C.POINTER(C.c_int)]),
     "sdp_ce_rows_fwd": (C.c_int, [VP, I64, I32, I64, VP, VP, VP, VP]),
     "sdp_group_norm_fwd": (C.c_int, [VP, I32, I32, I32, VP, I32, I32, VP, VP, C.c_float, I32, VP, VP, VP, VP]),
-    "sdp_group_norm_bwd": (C.c_int, [VP, VP, VP, I32, I32, I32, VP, I32, I32, VP, VP, VP, I32, VP, VP, VP, VP]),
-    "sdp_group_norm_bwd_fused": (C.c_int, [VP, VP, VP, I32, I32, I32, VP, I32, I32, VP, VP, VP, I32, VP, VP, VP, VP,
-                                           VP, VP]),
+    "sdp_group_norm_bwd_scratch": (C.c_int, [I32, I32, I32, I32, C.POINTER(C.c_longlong)]),
+    "sdp_group_norm_bwd": (C.c_int, [VP, VP, VP, I32, I32, I32, VP, I32, I32, VP, VP, VP, I32, VP, VP, VP, VP,
+                                     C.c_longlong, VP]),
     "sdp_layer_norm_fwd": (C.c_int, [VP, I64, I32, VP, VP, C.c_float, VP, VP, VP, VP]),
     "sdp_layer_norm_bwd_parts": (C.c_int, [I64, I32]),
     "sdp_layer_norm_bwd": (C.c_int, [VP, VP, I64, I32, VP, VP, VP, VP, VP, VP, VP, I32, VP]),

@@ -13,8 +13,8 @@
 //   k_gn_bwd  with dz = dy * [y > 0] (ReLU) and xhat recomputed:
 //             s1 = sum dz*gamma, s2 = sum dz*gamma*xhat over the group;
 //             dx = rstd * (dz*gamma - s1/n - xhat * s2/n);
-//             dgamma[c] += sum dz*xhat, dbeta[c] += sum dz (fp32 atomics from
-//             per-CTA shared-memory partials)
+//             dgamma[c] = sum dz*xhat, dbeta[c] = sum dz through per-CTA
+//             partial rows and an ordered fold (deterministic: no atomics)
 // Each CTA reads its part of the slab two or three times; the later reads
 // hit L1/L2.
 #include "sdp_common.cuh"
@@ -247,219 +247,162 @@ k_gn_fwd(const __nv_bfloat16* __restrict__ x, int hw, int c, const int32_t* __re
   }
 }
 
-// Optional fused epilogue of the backward: dgamma / dbeta accumulate in a
-// persistent fp32 scratch (zero between calls) and the LAST CTA to finish
-// (a global counter) writes them in the parameter's dtype, re-zeroes the
-// scratch and resets the counter -- no fill and no cast kernel per call.
-struct GnOut {
-  void* g;                 // dgamma output (bf16 or fp32), or null: plain fp32 accumulation
-  void* b;                 // dbeta output
-  bool bf16;
-  unsigned int* counter;   // CTAs finished (zero between calls)
-  int channels;
-};
-
-__device__ __forceinline__ void gn_finish(const GnOut& out, float* acc_g, float* acc_b) {
-  if (!out.g) return;
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(out.counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int k = threadIdx.x; k < out.channels; k += kGnThreads) {
-    const float a = __ldcg(acc_g + k), b = __ldcg(acc_b + k);
-    if (out.bf16) {
-      static_cast<__nv_bfloat16*>(out.g)[k] = __float2bfloat16_rn(a);
-      static_cast<__nv_bfloat16*>(out.b)[k] = __float2bfloat16_rn(b);
-    } else {
-      static_cast<float*>(out.g)[k] = a;
-      static_cast<float*>(out.b)[k] = b;
-    }
-    acc_g[k] = 0.f;
-    acc_b[k] = 0.f;
-  }
-  if (threadIdx.x == 0) *out.counter = 0u;
-}
-
-template <bool RELU, bool VEC>
+// Backward, deterministic end to end (no floating-point atomics):
+//   k_gn_bwd       one CTA per (sample, group, part) as in the forward.  The
+//                  thread -> (channel, pixel phase) map is fixed: cw = min(cg,
+//                  256) channels per pass, pstep = 256 / cw phases per
+//                  channel, so each thread keeps its channel's dgamma / dbeta
+//                  partial in registers; the CTA folds the phases of a channel
+//                  in ascending order and writes ONE partial row
+//                  part[(b * parts + part) * C + c] for its group's channels.
+//   k_gn_bwd_fold  sums the batch * parts partial rows of every channel in a
+//                  fixed order and writes dgamma / dbeta in the affine dtype.
+// Every partial-row entry is written by exactly one CTA, so the workspace
+// needs no zeroing and calls need no counters.
+template <bool RELU>
 __global__ void __launch_bounds__(kGnThreads, 4)
 k_gn_bwd(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
          const __nv_bfloat16* __restrict__ dy, int hw, int c, const int32_t* __restrict__ gs, int groups,
          const Affine gamma, const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-         __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, const GnOut out) {
+         __nv_bfloat16* __restrict__ dx, float* __restrict__ part_g, float* __restrict__ part_b) {
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ float s_dg[kGnMaxC], s_db[kGnMaxC];
+  __shared__ float s_pg[kGnMaxC], s_pb[kGnMaxC];
   __shared__ float2 s_part;
   const int parts = static_cast<int>(cl.num_blocks());
   const int bg = blockIdx.x / parts, part = static_cast<int>(cl.block_rank());
   const GnSlab t = gn_slab(bg, part, parts, hw, c, gs, groups);
   const float mean = mean_in[bg], rstd = rstd_in[bg];
-  constexpr bool vec = VEC;  // host-checked: every group start, C and the pointers 8-aligned
-  const int cv = vec ? t.cg / 8 : t.cg;
-  const int nv = (t.p1 - t.p0) * cv;
-  for (int k = threadIdx.x; k < t.cg; k += kGnThreads) {
-    s_dg[k] = 0.f;
-    s_db[k] = 0.f;
-  }
-  __syncthreads();
-  // the thread's channel (vector) is fixed when the vectors per pixel divide
-  // the CTA width: per-channel partials stay in registers
-  const bool fixed = (kGnThreads % cv) == 0;
-  if (!vec && fixed) {
-    // one channel per thread, kGnU pixels per round with all their loads in
-    // flight (the element-at-a-time loop kept ~6 KB per SM in flight: latency
-    // bound), gamma read once
-    const int kv = threadIdx.x % cv, pstep = kGnThreads / cv, npix = t.p1 - t.p0;
-    const float gch = gamma[t.c0 + kv];
-    const __nv_bfloat16* xb = x + t.base + kv;
-    const __nv_bfloat16* yb = y + t.base + kv;
-    const __nv_bfloat16* db = dy + t.base + kv;
-    float s1 = 0.f, s2 = 0.f, pgs = 0.f, pbs = 0.f;
-    for (int p0 = threadIdx.x / cv; p0 < npix; p0 += kGnU * pstep) {
-      float vx[kGnU], vd[kGnU], vy[kGnU];
+  const int npix = t.p1 - t.p0;
+  const int cw = min(t.cg, kGnThreads);       // channels per pass
+  const int pstep = kGnThreads / cw;          // pixel phases per channel
+  const int ph = threadIdx.x / cw;            // this thread's phase (>= pstep: idle)
+  const bool on = ph < pstep;
+  const int kv0 = threadIdx.x - ph * cw;
+  // pass 1: the group sums s1 = sum dz*gamma, s2 = sum dz*gamma*xhat and the
+  // per-channel partials, kGnU pixels per round with all their loads in flight
+  float s1 = 0.f, s2 = 0.f;
+  if (on) {
+    for (int kv = kv0; kv < t.cg; kv += cw) {
+      const float gch = gamma[t.c0 + kv];
+      const __nv_bfloat16* xb = x + t.base + kv;
+      const __nv_bfloat16* yb = y + t.base + kv;
+      const __nv_bfloat16* db = dy + t.base + kv;
+      float pgs = 0.f, pbs = 0.f;
+      for (int p0 = ph; p0 < npix; p0 += kGnU * pstep) {
+        float vx[kGnU], vd[kGnU], vy[kGnU];
 #pragma unroll
-      for (int u = 0; u < kGnU; ++u) {
-        const int pix = p0 + u * pstep;
-        const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
-        vx[u] = __bfloat162float(xb[o]);
-        vd[u] = pix < npix ? __bfloat162float(db[o]) : 0.f;
-        vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
-      }
+        for (int u = 0; u < kGnU; ++u) {
+          const int pix = p0 + u * pstep;
+          const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
+          vx[u] = __bfloat162float(xb[o]);
+          vd[u] = pix < npix ? __bfloat162float(db[o]) : 0.f;
+          vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
+        }
 #pragma unroll
-      for (int u = 0; u < kGnU; ++u) {
-        const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
-        const float xh = (vx[u] - mean) * rstd;
-        s1 += dz * gch;
-        s2 += dz * gch * xh;
-        pgs += dz * xh;
-        pbs += dz;
-      }
-    }
-    if (threadIdx.x < npix * cv) {
-      atomicAdd(&s_dg[kv], pgs);
-      atomicAdd(&s_db[kv], pbs);
-    }
-    block_sum2<kGnThreads>(s1, s2);
-    const float inv_n = 1.f / (static_cast<float>(hw) * t.cg);
-    cluster_sum2(cl, &s_part, s1, s2);
-    s1 *= inv_n;
-    s2 *= inv_n;
-    __nv_bfloat16* dxb = dx + t.base + kv;
-    for (int p0 = threadIdx.x / cv; p0 < npix; p0 += kGnU * pstep) {
-      float vx[kGnU], vd[kGnU], vy[kGnU];
-#pragma unroll
-      for (int u = 0; u < kGnU; ++u) {
-        const int pix = p0 + u * pstep;
-        const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
-        vx[u] = __bfloat162float(xb[o]);
-        vd[u] = __bfloat162float(db[o]);
-        vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
-      }
-#pragma unroll
-      for (int u = 0; u < kGnU; ++u) {
-        const int pix = p0 + u * pstep;
-        const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
-        const float xh = (vx[u] - mean) * rstd;
-        if (pix < npix) dxb[static_cast<int64_t>(pix) * c] = __float2bfloat16_rn(rstd * (dz * gch - s1 - xh * s2));
-      }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < t.cg; k += kGnThreads) {
-      atomicAdd(&dgamma[t.c0 + k], s_dg[k]);
-      atomicAdd(&dbeta[t.c0 + k], s_db[k]);
-    }
-    gn_finish(out, dgamma, dbeta);
-    return;
-  }
-  float s1 = 0.f, s2 = 0.f, pg[8], pb[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) pg[k] = pb[k] = 0.f;
-  for (int q = threadIdx.x; q < nv; q += kGnThreads) {
-    const int pix = q / cv, kv = q - pix * cv;
-    const int64_t i = t.base + static_cast<int64_t>(pix) * c + (vec ? kv * 8 : kv);
-    if (vec) {
-      const Bf8 rx = ld8(x + i), rd = ld8(dy + i);
-      Bf8 ry;
-      if (RELU) ry = ld8(y + i);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float dz = RELU && !(ry.v[k] > 0.f) ? 0.f : rd.v[k];
-        const float xh = (rx.v[k] - mean) * rstd;
-        const float dzg = dz * gamma[t.c0 + kv * 8 + k];
-        s1 += dzg;
-        s2 += dzg * xh;
-        if (fixed) {
-          pg[k] += dz * xh;
-          pb[k] += dz;
-        } else {
-          atomicAdd(&s_dg[kv * 8 + k], dz * xh);
-          atomicAdd(&s_db[kv * 8 + k], dz);
+        for (int u = 0; u < kGnU; ++u) {
+          const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
+          const float xh = (vx[u] - mean) * rstd;
+          s1 += dz * gch;
+          s2 += dz * gch * xh;
+          pgs += dz * xh;
+          pbs += dz;
         }
       }
-    } else {
-      float dz = __bfloat162float(dy[i]);
-      if (RELU && !(__bfloat162float(y[i]) > 0.f)) dz = 0.f;
-      const float xh = (__bfloat162float(x[i]) - mean) * rstd;
-      const float dzg = dz * gamma[t.c0 + kv];
-      s1 += dzg;
-      s2 += dzg * xh;
-      if (fixed) {
-        pg[0] += dz * xh;
-        pb[0] += dz;
-      } else {
-        atomicAdd(&s_dg[kv], dz * xh);
-        atomicAdd(&s_db[kv], dz);
-      }
+      s_pg[ph * t.cg + kv] = pgs;
+      s_pb[ph * t.cg + kv] = pbs;
     }
   }
-  if (fixed && threadIdx.x < nv) {
-    const int kv = threadIdx.x % cv;
-    if (vec) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        atomicAdd(&s_dg[kv * 8 + k], pg[k]);
-        atomicAdd(&s_db[kv * 8 + k], pb[k]);
-      }
-    } else {
-      atomicAdd(&s_dg[kv], pg[0]);
-      atomicAdd(&s_db[kv], pb[0]);
-    }
-  }
-  block_sum2<kGnThreads>(s1, s2);
+  block_sum2<kGnThreads>(s1, s2);  // (its barriers also publish s_pg / s_pb)
   const float inv_n = 1.f / (static_cast<float>(hw) * t.cg);
   cluster_sum2(cl, &s_part, s1, s2);
   s1 *= inv_n;
   s2 *= inv_n;
-  for (int q = threadIdx.x; q < nv; q += kGnThreads) {
-    const int pix = q / cv, kv = q - pix * cv;
-    const int64_t i = t.base + static_cast<int64_t>(pix) * c + (vec ? kv * 8 : kv);
-    if (vec) {
-      const Bf8 rx = ld8(x + i), rd = ld8(dy + i);
-      Bf8 ry;
-      if (RELU) ry = ld8(y + i);
-      float o[8];
+  // this CTA's partial row: channel k = phases 0, 1, ... in order
+  const int64_t row = static_cast<int64_t>(t.b * parts + part) * c + t.c0;
+  for (int k = threadIdx.x; k < t.cg; k += kGnThreads) {
+    float a = 0.f, b = 0.f;
+    for (int r = 0; r < pstep; ++r) {
+      a += s_pg[r * t.cg + k];
+      b += s_pb[r * t.cg + k];
+    }
+    part_g[row + k] = a;
+    part_b[row + k] = b;
+  }
+  // pass 2: dx (the slab re-read hits L1/L2)
+  if (on) {
+    for (int kv = kv0; kv < t.cg; kv += cw) {
+      const float gch = gamma[t.c0 + kv];
+      const __nv_bfloat16* xb = x + t.base + kv;
+      const __nv_bfloat16* yb = y + t.base + kv;
+      const __nv_bfloat16* db = dy + t.base + kv;
+      __nv_bfloat16* dxb = dx + t.base + kv;
+      for (int p0 = ph; p0 < npix; p0 += kGnU * pstep) {
+        float vx[kGnU], vd[kGnU], vy[kGnU];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float dz = RELU && !(ry.v[k] > 0.f) ? 0.f : rd.v[k];
-        const float xh = (rx.v[k] - mean) * rstd;
-        o[k] = rstd * (dz * gamma[t.c0 + kv * 8 + k] - s1 - xh * s2);
+        for (int u = 0; u < kGnU; ++u) {
+          const int pix = p0 + u * pstep;
+          const int64_t o = static_cast<int64_t>(pix < npix ? pix : 0) * c;
+          vx[u] = __bfloat162float(xb[o]);
+          vd[u] = __bfloat162float(db[o]);
+          vy[u] = RELU ? __bfloat162float(yb[o]) : 1.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kGnU; ++u) {
+          const int pix = p0 + u * pstep;
+          const float dz = RELU && !(vy[u] > 0.f) ? 0.f : vd[u];
+          const float xh = (vx[u] - mean) * rstd;
+          if (pix < npix) dxb[static_cast<int64_t>(pix) * c] = __float2bfloat16_rn(rstd * (dz * gch - s1 - xh * s2));
+        }
       }
-      st8(dx + i, o);
-    } else {
-      float dz = __bfloat162float(dy[i]);
-      if (RELU && !(__bfloat162float(y[i]) > 0.f)) dz = 0.f;
-      const float xh = (__bfloat162float(x[i]) - mean) * rstd;
-      dx[i] = __float2bfloat16_rn(rstd * (dz * gamma[t.c0 + kv] - s1 - xh * s2));
     }
   }
-  __syncthreads();
-  for (int k = threadIdx.x; k < t.cg; k += kGnThreads) {
-    atomicAdd(&dgamma[t.c0 + k], s_dg[k]);
-    atomicAdd(&dbeta[t.c0 + k], s_db[k]);
+}
+
+// 32 channels per CTA; warp w sums partial rows w, w + 8, ... in ascending
+// order (loads batched), then the 8 warp sums fold in warp order.
+constexpr int kGnFoldWarps = 8;
+__global__ void __launch_bounds__(32 * kGnFoldWarps)
+k_gn_bwd_fold(const float* __restrict__ part_g, const float* __restrict__ part_b, int rows, int c,
+              void* __restrict__ dgamma, void* __restrict__ dbeta, bool bf16) {
+  __shared__ float s_g[kGnFoldWarps][32], s_b[kGnFoldWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
+  float a = 0.f, b = 0.f;
+  if (col < c) {
+    constexpr int U = 4;
+    for (int r0 = warp; r0 < rows; r0 += U * kGnFoldWarps) {
+      float va[U], vb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u * kGnFoldWarps;
+        va[u] = r < rows ? part_g[static_cast<int64_t>(r) * c + col] : 0.f;
+        vb[u] = r < rows ? part_b[static_cast<int64_t>(r) * c + col] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a += va[u];
+        b += vb[u];
+      }
+    }
   }
-  gn_finish(out, dgamma, dbeta);
+  s_g[warp][lane] = a;
+  s_b[warp][lane] = b;
+  __syncthreads();
+  if (warp == 0 && col < c) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll
+    for (int w = 0; w < kGnFoldWarps; ++w) {
+      ta += s_g[w][lane];
+      tb += s_b[w][lane];
+    }
+    if (bf16) {
+      static_cast<__nv_bfloat16*>(dgamma)[col] = __float2bfloat16_rn(ta);
+      static_cast<__nv_bfloat16*>(dbeta)[col] = __float2bfloat16_rn(tb);
+    } else {
+      static_cast<float*>(dgamma)[col] = ta;
+      static_cast<float*>(dbeta)[col] = tb;
+    }
+  }
 }
 
 static int check_groups(int b, int hw, int c, int groups) {
@@ -501,61 +444,47 @@ int sdp_group_norm_fwd(const void* x_bf16, int batch, int hw, int channels, cons
   return SDP_OK;
 }
 
-static int gn_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw, int channels,
-                  const int32_t* group_starts, int groups, int max_group_channels, const void* gamma,
-                  const float* mean, const float* rstd, int flags, void* dx_bf16, float* dgamma, float* dbeta,
-                  const GnOut out, void* stream);
+int sdp_group_norm_bwd_scratch(int batch, int hw, int channels, int max_group_channels, long long* floats) {
+  if (!floats) return set_error(SDP_ERR_USAGE, "null output");
+  if (batch < 0 || hw < 1 || channels < 1 || max_group_channels < 1)
+    return set_error(SDP_ERR_USAGE, "bad group-norm shape");
+  *floats = 2ll * batch * gn_parts(hw, max_group_channels) * channels;
+  return SDP_OK;
+}
 
 int sdp_group_norm_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
                        int channels, const int32_t* group_starts, int groups, int max_group_channels,
                        const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
-                       float* dgamma, float* dbeta, void* stream) {
-  return gn_bwd(x_bf16, y_bf16, dy_bf16, batch, hw, channels, group_starts, groups, max_group_channels, gamma, mean,
-                rstd, flags, dx_bf16, dgamma, dbeta, GnOut{nullptr, nullptr, false, nullptr, 0}, stream);
-}
-
-int sdp_group_norm_bwd_fused(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw,
-                             int channels, const int32_t* group_starts, int groups, int max_group_channels,
-                             const void* gamma, const float* mean, const float* rstd, int flags, void* dx_bf16,
-                             void* dgamma_out, void* dbeta_out, float* scratch, unsigned int* counter,
-                             void* stream) {
-  if (!dgamma_out || !dbeta_out || !scratch || !counter) return set_error(SDP_ERR_USAGE, "null device pointer");
-  if (batch == 0) return set_error(SDP_ERR_USAGE, "fused group-norm backward needs batch > 0");
-  const GnOut out{dgamma_out, dbeta_out, (flags & SDP_GN_AFFINE_BF16) != 0, counter, channels};
-  return gn_bwd(x_bf16, y_bf16, dy_bf16, batch, hw, channels, group_starts, groups, max_group_channels, gamma, mean,
-                rstd, flags, dx_bf16, scratch, scratch + channels, out, stream);
-}
-
-static int gn_bwd(const void* x_bf16, const void* y_bf16, const void* dy_bf16, int batch, int hw, int channels,
-                  const int32_t* group_starts, int groups, int max_group_channels, const void* gamma,
-                  const float* mean, const float* rstd, int flags, void* dx_bf16, float* dgamma, float* dbeta,
-                  const GnOut out, void* stream) {
+                       void* dgamma, void* dbeta, float* scratch, long long scratch_floats, void* stream) {
   const bool relu = flags & SDP_GN_RELU;
-  const Affine ga{gamma, (flags & SDP_GN_AFFINE_BF16) != 0};
+  const bool bf16 = (flags & SDP_GN_AFFINE_BF16) != 0;
+  const Affine ga{gamma, bf16};
   if (int rc = check_groups(batch, hw, channels, groups)) return rc;
   if (max_group_channels > kGnMaxC) return set_error(SDP_ERR_USAGE, "a group of more than %d channels", kGnMaxC);
-  if (batch == 0) return SDP_OK;
+  if (batch == 0) return set_error(SDP_ERR_USAGE, "group-norm backward needs batch > 0");
+  if (!dgamma || !dbeta || !scratch) return set_error(SDP_ERR_USAGE, "null device pointer");
   const int parts = gn_parts(hw, max_group_channels);
+  const int64_t rows = static_cast<int64_t>(batch) * parts;
+  if (scratch_floats < 2 * rows * channels)
+    return set_error(SDP_ERR_USAGE, "group-norm backward scratch holds %lld floats, needs %lld", scratch_floats,
+                     static_cast<long long>(2 * rows * channels));
   const unsigned grid = static_cast<unsigned>(batch) * groups * parts;
   cudaStream_t s = as_stream(stream);
   auto xb = static_cast<const __nv_bfloat16*>(x_bf16);
   auto yb = static_cast<const __nv_bfloat16*>(y_bf16);
   auto db = static_cast<const __nv_bfloat16*>(dy_bf16);
   auto dxb = static_cast<__nv_bfloat16*>(dx_bf16);
-  // Measured on B200 (ResNet-18 DP step): the 16-B vector path speeds the
-  // forward up but slows this kernel down (3.2 -> 3.9 ms per step: 8x fewer
-  // work items per CTA idle most threads on the late-layer slabs), so the
-  // backward keeps one channel per element.
-  const bool vec = false;
-#define SDP_GN_BWD(R, V)                                                                                 \
-  SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<R, V>, grid, parts, s, xb, yb, db, hw, channels, group_starts,  \
-                                  groups, ga, mean, rstd, dxb, dgamma, dbeta, out))
-  if (relu) {
-    if (vec) SDP_GN_BWD(true, true); else SDP_GN_BWD(true, false);
-  } else {
-    if (vec) SDP_GN_BWD(false, true); else SDP_GN_BWD(false, false);
-  }
-#undef SDP_GN_BWD
+  float* pg = scratch;
+  float* pb = scratch + rows * channels;
+  if (relu)
+    SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<true>, grid, parts, s, xb, yb, db, hw, channels, group_starts, groups,
+                                    ga, mean, rstd, dxb, pg, pb));
+  else
+    SDP_CUDA_CHECK(launch_clustered(k_gn_bwd<false>, grid, parts, s, xb, yb, db, hw, channels, group_starts, groups,
+                                    ga, mean, rstd, dxb, pg, pb));
+  SDP_LAUNCH_CHECK();
+  k_gn_bwd_fold<<<(channels + 31) / 32, 32 * kGnFoldWarps, 0, s>>>(pg, pb, static_cast<int>(rows), channels, dgamma,
+                                                                  dbeta, bf16);
   SDP_LAUNCH_CHECK();
   return SDP_OK;
 }

@@ -83,7 +83,8 @@ def _group_starts(starts: tuple[int, ...], dev) -> torch.Tensor:
 class _GroupNormCL(torch.autograd.Function):
     """libsdp k_gn_fwd / k_gn_bwd: GroupNorm (+ReLU) on channels-last bf16
     activations over contiguous, possibly ragged channel groups; fp32
-    statistics and affine parameters, fp32 dgamma / dbeta."""
+    statistics; dgamma / dbeta in the affine dtype, deterministic (per-CTA
+    partial rows + an ordered fold, no atomics)."""
 
     @staticmethod
     def forward(ctx, x, gamma, beta, starts, eps, relu):
@@ -117,33 +118,19 @@ class _GroupNormCL(torch.autograd.Function):
         b, c, h, w = x.shape
         dy = dy.contiguous(memory_format=torch.channels_last)
         dx = torch.empty_like(x, memory_format=torch.channels_last)
-        if b > 0 and c <= _GN_SCRATCH_C:  # fused epilogue: dgamma | dbeta written in gamma's dtype
-            scratch, counter = _gn_scratch(x.device)
-            dgb = torch.empty(2 * c, dtype=gamma.dtype, device=x.device)
-            N.call("sdp_group_norm_bwd_fused", ptr(x), ptr(y), ptr(dy), b, h * w, c,
+        dgb = torch.empty(2 * c, dtype=gamma.dtype, device=x.device)  # dgamma | dbeta, written
+        if b > 0:
+            n = C.c_longlong(0)
+            N.call("sdp_group_norm_bwd_scratch", b, h * w, c, max_cg, C.byref(n))
+            # per call from the caching allocator: stream-ordered, so co-resident
+            # workers on different streams never share partial rows
+            scratch = torch.empty(n.value, dtype=torch.float32, device=x.device)
+            N.call("sdp_group_norm_bwd", ptr(x), ptr(y), ptr(dy), b, h * w, c,
                    ptr(_group_starts(starts, x.device)), len(starts) - 1, max_cg, ptr(gamma), ptr(mean), ptr(rstd),
-                   flags, ptr(dx), ptr(dgb[:c]), ptr(dgb[c:]), ptr(scratch), ptr(counter), stream_ptr(x.device))
-            return dx, dgb[:c], dgb[c:], None, None, None
-        dgb = torch.zeros(2 * c, dtype=torch.float32, device=x.device)  # dgamma | dbeta, one fill
-        N.call("sdp_group_norm_bwd", ptr(x), ptr(y), ptr(dy), b, h * w, c, ptr(_group_starts(starts, x.device)),
-               len(starts) - 1, max_cg, ptr(gamma), ptr(mean), ptr(rstd), flags, ptr(dx), ptr(dgb[:c]),
-               ptr(dgb[c:]), stream_ptr(x.device))
-        if gamma.dtype != torch.float32:
-            dgb = dgb.to(gamma.dtype)  # one cast for both
+                   flags, ptr(dx), ptr(dgb[:c]), ptr(dgb[c:]), ptr(scratch), n, stream_ptr(x.device))
+        else:
+            dgb.zero_()
         return dx, dgb[:c], dgb[c:], None, None, None
-
-
-_GN_SCRATCH_C = 4096
-_GN_SCRATCH: dict = {}
-
-
-def _gn_scratch(dev):
-    """Per-device fp32 accumulation scratch + CTA counter of the fused
-    GroupNorm backward (zeroed once; every call leaves them zero again)."""
-    if dev not in _GN_SCRATCH:
-        _GN_SCRATCH[dev] = (torch.zeros(2 * _GN_SCRATCH_C, dtype=torch.float32, device=dev),
-                            torch.zeros(1, dtype=torch.int32, device=dev))
-    return _GN_SCRATCH[dev]
 
 
 def _channels_last_bf16(x) -> bool:

@@ -175,7 +175,6 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, auto
     torch.backends.cudnn.deterministic = True
     try:
         model = train.build_resnet18(cuda, seed=5)
-        theta0 = model.theta.cpu().numpy()
         a = masking.build_assignment(model.topology, strategy, 4, 2, seed=1)
         tr = train.SubnetTrainer(model, a, lr=0.05, autocast=autocast, sync_layout=strategy == "neuron")
         for step in range(2):
@@ -194,16 +193,9 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, auto
         z = np.load(tmp_path / f"rank{r}.npz")
         for w in (0, 1) if r == 0 else (2, 3):
             got = z[f"w{w}"]
-            if not autocast:
-                assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
-            else:
-                # libsdp's GroupNorm backward sums dgamma / dbeta with fp32
-                # atomics (order varies run to run): same plumbing, not the
-                # same bits -- the copies agree to a small fraction of the
-                # two steps' update (a wrong slot or layout would be O(1))
-                upd = np.abs(canon - theta0)[masks[w]].max()
-                err = np.abs(got - canon)[masks[w]].max()
-                assert err <= 0.05 * upd, (r, w, err, upd)
+            # bit-identical in fp32 and under bf16 autocast (libsdp's GroupNorm
+            # backward folds dgamma / dbeta in a fixed order: no atomics)
+            assert np.array_equal(got[masks[w]].view(np.uint32), canon[masks[w]].view(np.uint32)), (r, w)
 
 
 LOCAL_CHILD = textwrap.dedent(r"""

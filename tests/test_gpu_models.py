@@ -214,6 +214,47 @@ def test_gather_scatter_all_paths_full_size(cuda, strategy, dtype):
         assert torch.equal(acc, torch.where(mask, base + theta, base))
 
 
+@pytest.mark.parametrize("shape", [(64, (32, 32), 32), (16, (29, 35), 12), (8, (300, 212), 4), (64, (256, 256), 4),
+                                   (4, (7, 1, 24), 16)])
+def test_group_norm_backward_is_deterministic(cuda, shape):
+    """k_gn_bwd + k_gn_bwd_fold: dx, dgamma and dbeta are bit-identical across
+    repeated calls (per-CTA partial rows folded in a fixed order -- no
+    floating-point atomics), for multi-CTA clusters, ragged groups and groups
+    wider than the CTA (> 256 channels); dgamma / dbeta agree with fp32
+    F.group_norm's to fold rounding."""
+    import torch.nn.functional as F
+    from paper_2507_09029_b200 import models
+    b, counts, hw = shape
+    c = sum(counts)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(c + b)
+    x = (torch.randn(b, c, hw, hw, generator=gen, device=cuda) * 2 + 0.5).to(torch.bfloat16)
+    x = x.contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    gamma = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
+    beta = torch.randn(c, generator=gen, device=cuda).requires_grad_(True)
+    dy = torch.randn(b, c, hw, hw, generator=gen, device=cuda).to(torch.bfloat16)
+    outs = []
+    for _ in range(3):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            y = models.ragged_group_norm(x, None, len(counts), gamma, beta, counts=counts, relu=True)
+        outs.append(torch.autograd.grad(y, (x, gamma, beta), dy))
+    for o in outs[1:]:
+        for a_, b_ in zip(outs[0], o):
+            assert torch.equal(a_.view(torch.int16) if a_.dtype == torch.bfloat16 else a_.view(torch.int32),
+                               b_.view(torch.int16) if b_.dtype == torch.bfloat16 else b_.view(torch.int32))
+    xr = x.detach().float().requires_grad_(True)
+    gr, br = gamma.detach().float().requires_grad_(True), beta.detach().float().requires_grad_(True)
+    parts, pos = [], 0
+    for k in counts:
+        parts.append(F.group_norm(xr[:, pos:pos + k], 1, gr[pos:pos + k], br[pos:pos + k]))
+        pos += k
+    rx, rg, rb = torch.autograd.grad(F.relu(torch.cat(parts, dim=1)), (xr, gr, br), dy.float())
+    gx, gg, gb = outs[0]
+    assert torch.allclose(gg, rg, rtol=1e-2, atol=1e-2 * rg.abs().max().item())
+    assert torch.allclose(gb, rb, rtol=1e-2, atol=1e-2 * rb.abs().max().item())
+    assert torch.allclose(gx.float(), rx, rtol=2e-2, atol=2e-2 * rx.abs().max().item())
+
+
 @pytest.mark.parametrize("affine", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("relu", [False, True])
 @pytest.mark.parametrize("counts", [(32, 32), (29, 35), (7, 1, 24)])

@@ -1,0 +1,91 @@
+"""Small-buffer sync probe (C5 1-16 MiB; run under gpurun; not part of bench).
+
+For each size / P: per-launch microseconds of k_owner_sync (cold L2 via a
+flush, warm L2 without), a same-traffic device copy for the practical floor,
+and an empty kernel for the event overhead.  One JSON line per row.
+
+    python tools/small_probe.py [--sizes 1,4,16] [--ps 2,4,8] [--tiles 1024,2048]
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2507_09029_b200 import engine, masking, zoo  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+FW = FR = None
+
+
+def flush():
+    FW.zero_()
+    FR.sum()
+
+
+def timed(fn, reps=30, cold=True):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    for i in range(reps):
+        if cold:
+            flush()
+        st[i].record()
+        fn()
+        en[i].record()
+    torch.cuda.synchronize()
+    ts = sorted(s.elapsed_time(e) * 1e3 for s, e in zip(st, en))
+    return ts[len(ts) // 2], ts[0]
+
+
+def main():
+    global FW, FR
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1,4,16")
+    ap.add_argument("--ps", default="2,4,8")
+    ap.add_argument("--tiles", default="auto")
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--strategy", default="block")
+    args = ap.parse_args()
+    FW = torch.empty(64 << 20, device=DEV)
+    FR = torch.zeros(64 << 20, device=DEV)
+    peak = json.load(open(Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json")).get("hbm_gbs", 6540.5)
+    tiny = torch.zeros(1, device=DEV)
+    med, mn = timed(lambda: tiny.add_(1))
+    print(json.dumps({"row": "empty kernel", "us": round(med, 2), "us_min": round(mn, 2)}), flush=True)
+    for mib in [int(x) for x in args.sizes.split(",")]:
+        d = mib * (1 << 20) // 4
+        topo = zoo.sweep_topology(d)
+        for p in [int(x) for x in args.ps.split(",")]:
+            a = masking.build_assignment(topo, args.strategy, args.n, p, seed=1)
+            reps = [torch.randn(d, device=DEV) * a.param_masks[w] for w in range(args.n)]
+            shadows = [torch.zeros(d, dtype=torch.bfloat16, device=DEV) for _ in reps]
+            own = int(a.owned_total())
+            nbytes = own * 10
+            src = torch.empty(nbytes // 8, device=DEV)
+            dst = torch.empty_like(src)
+            cm, cmn = timed(lambda: dst.copy_(src))
+            print(json.dumps({"row": "copy same traffic", "MiB": mib, "p": p, "bytes": nbytes,
+                              "us": round(cm, 2), "frac": round(nbytes / cm / 1e3 / peak, 3)}), flush=True)
+            tiles = [None] if args.tiles == "auto" else [int(t) for t in args.tiles.split(",")]
+            for t in tiles:
+                plan = a.sync_plan(tile=t)
+                prep = engine.PreparedSync(reps, a, writeback=True, shadows_bf16=shadows, plan=plan)
+                for cold in (True, False):
+                    m, mn = timed(prep.launch, cold=cold)
+                    print(json.dumps({"row": "sync", "MiB": mib, "p": p, "tile": plan.tile,
+                                      "grid": plan.grid, "tiles": plan.n_tiles,
+                                      "mixed": plan.n_tiles - plan.n_uniform, "cold": cold,
+                                      "bytes": nbytes, "us": round(m, 2), "us_min": round(mn, 2),
+                                      "frac": round(nbytes / m / 1e3 / peak, 3)}), flush=True)
+            del reps, shadows, src, dst
+
+
+if __name__ == "__main__":
+    main()
