@@ -191,9 +191,11 @@ def main():
         sync_case(r18, "C2 resnet18", "block", 8, 4)
         sync_case(r18, "C2 resnet18", "block", 8, 4, writeback=False, shadows=False)
         sync_case(r18, "C3 resnet18", "neuron", 8, 4)
+        sync_case(r18, "C3 resnet18", "neuron", 8, 4, writeback=False, shadows=False)
         sync_case(r18, "C3 resnet18 (sync layout)", "neuron", 8, 4, sync_layout=True)
         sync_case(gpt2, "C4 gpt2", "block", 8, 4)
         sync_case(gpt2, "C4 gpt2 width-wise (sync layout)", "neuron", 8, 4, sync_layout=True)
+        sync_case(gpt2, "C4 gpt2 width-wise", "neuron", 8, 4, writeback=False, shadows=False)
     if "sweep" in only:
         sizes = [1, 16, 256] if args.quick else [1, 4, 16, 64, 256, 1024]
         for mib in sizes:
