@@ -326,7 +326,8 @@ typedef struct {
   int32_t desc;
   int32_t row_begin, row_end;
   int32_t elem_begin, elem_end;
-  int32_t pad_[3];
+  int32_t seg;      /* segment (worker) of a *_multi launch; ignored (0) otherwise */
+  int32_t pad_[2];
 } sdp_slice_task;
 
 /* compact[...] = full[...] over every task (persistent CTAs walk the task list;
@@ -343,6 +344,20 @@ int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_ta
                       int n_tasks, const int32_t* fwd_maps, const void* full,
                       void* compact, int flags, void* stream);
 
+/* Several workers' slices in ONE launch: task `seg` selects the segment's
+ * (full, compact) base pointers from this host-side table (copied into the
+ * kernel's parameters).  The descriptor / task / map tables are the
+ * per-worker tables concatenated (models.SliceBatch).  A compact pointer may
+ * be NULL in a scatter segment only if that segment has no tasks. */
+typedef struct {
+  const void* full[SDP_MAX_WORKERS];
+  const void* compact[SDP_MAX_WORKERS];
+  int32_t n;
+} sdp_slice_segs;
+int sdp_gather_slices_multi(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                            int n_tasks, const int32_t* fwd_maps, const sdp_slice_segs* segs,
+                            int flags, void* stream);
+
 #define SDP_SCATTER_ZERO_FILL 0x1  /* full[j] = 0 where no compact element maps */
 #define SDP_SCATTER_ACCUMULATE 0x2 /* full[j] += compact[...] instead of = */
 
@@ -352,6 +367,9 @@ int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_ta
 int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
                        int n_tasks, const int32_t* inv_maps, const void* compact, void* full,
                        int flags, void* stream);
+int sdp_scatter_slices_multi(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                             int n_tasks, const int32_t* inv_maps, const sdp_slice_segs* segs,
+                             int flags, void* stream);
 
 /* out[j] = acc[j] / divisor[j] in dtype (the engine.py:74 divide after an
  * owner-ordered scatter-accumulate).  divisor is float64 [d]. */

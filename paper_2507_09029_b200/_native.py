@@ -75,7 +75,12 @@ class SliceDesc(C.Structure):
 
 class SliceTask(C.Structure):
     _fields_ = [("desc", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("elem_begin", C.c_int32), ("elem_end", C.c_int32), ("pad_", C.c_int32 * 3)]
+                ("elem_begin", C.c_int32), ("elem_end", C.c_int32), ("seg", C.c_int32),
+                ("pad_", C.c_int32 * 2)]
+
+
+class SliceSegs(C.Structure):
+    _fields_ = [("full", C.c_void_p * MAX_WORKERS), ("compact", C.c_void_p * MAX_WORKERS), ("n", C.c_int32)]
 
 
 
@@ -151,6 +156,8 @@ SIGNATURES = {
     "sdp_masked_extract": (C.c_int, [I32, VP, VP, I32, I64, I32, VP, VP]),
     "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
     "sdp_scatter_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),
+    "sdp_gather_slices_multi": (C.c_int, [I32, VP, VP, I32, VP, C.POINTER(SliceSegs), I32, VP]),
+    "sdp_scatter_slices_multi": (C.c_int, [I32, VP, VP, I32, VP, C.POINTER(SliceSegs), I32, VP]),
     "sdp_divide": (C.c_int, [I32, VP, VP, I64, VP, VP]),
     "sdp_restricted_dots": (C.c_int, [I32, VP, VP, VP, VP, I32, I32, VP, VP, VP]),
     "sdp_ipc_export": (C.c_int, [VP, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),

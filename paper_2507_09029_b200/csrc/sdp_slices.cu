@@ -48,10 +48,19 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t 
 // contiguous side (compact rows for gather, full rows for scatter) is
 // accessed at consecutive thread positions (coalesced).  Offsets inside one
 // tensor fit in 32 bits (rows * cols * inner < 2^31, checked on the host).
-constexpr int kSliceBatch = 8;
+constexpr int kSliceBatch = 6;
 template <typename T> constexpr int rows_per_iter() { return sizeof(T) == 8 ? 1 : 2; }
 constexpr int kStage = 32;
-constexpr int kSliceCtasPerSm = 3;  // <= 80 registers: 16 elements in flight per thread without spills
+constexpr int kSliceCtasPerSm = 4;  // <= 64 registers
+
+// Per-launch (full, compact) base pointers of up to SDP_MAX_WORKERS segments
+// (workers): a task's `seg` picks its pair, so ONE launch moves every
+// worker's slices.  Lives in the kernel parameter space.
+struct SegPtrs {
+  void* full[SDP_MAX_WORKERS];
+  void* compact[SDP_MAX_WORKERS];
+  int n;
+};
 
 struct SliceStage {
   sdp_slice_task task[kStage];
@@ -221,13 +230,16 @@ __device__ __forceinline__ void gather_flat(const sdp_slice_task& tk, const sdp_
 template <typename T, bool REVERSE>
 __global__ void __launch_bounds__(kSliceThreads, kSliceCtasPerSm)
 k_gather(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks, int n_tasks,
-         const int32_t* __restrict__ fwd, T* __restrict__ full, T* __restrict__ compact) {
+         const int32_t* __restrict__ fwd, const __grid_constant__ SegPtrs segs) {
   __shared__ SliceStage st;
   for (int first = blockIdx.x; first < n_tasks; first += kStage * gridDim.x) {
     const int n = stage_tasks(st, descs, tasks, n_tasks, first);
     for (int i = 0; i < n; ++i) {
       const sdp_slice_task& tk = st.task[i];
       const sdp_slice_desc& d = st.desc[i];
+      const int sg = segs.n == 1 ? 0 : tk.seg;
+      T* const full = static_cast<T*>(segs.full[sg]);
+      T* const compact = static_cast<T*>(segs.compact[sg]);
       const uint32_t row_len = static_cast<uint32_t>(d.ccols) * d.inner;
       if (row_len >= kSliceThreads) {
         if (rows_vectorizable<T>(tk, d, full, compact, row_len))
@@ -415,8 +427,7 @@ __device__ __forceinline__ void scatter_flat(const sdp_slice_task& tk, const sdp
 template <typename T>
 __global__ void __launch_bounds__(kSliceThreads, kSliceCtasPerSm)
 k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __restrict__ tasks, int n_tasks,
-          const int32_t* __restrict__ inv, const T* __restrict__ compact, T* __restrict__ full,
-          int flags) {
+          const int32_t* __restrict__ inv, const __grid_constant__ SegPtrs segs, int flags) {
   __shared__ SliceStage st;
   const bool zero_fill = (flags & SDP_SCATTER_ZERO_FILL) && !(flags & SDP_SCATTER_ACCUMULATE);
   const bool accumulate = (flags & SDP_SCATTER_ACCUMULATE) != 0;
@@ -425,6 +436,9 @@ k_scatter(const sdp_slice_desc* __restrict__ descs, const sdp_slice_task* __rest
     for (int i = 0; i < n; ++i) {
       const sdp_slice_task& tk = st.task[i];
       const sdp_slice_desc& d = st.desc[i];
+      const int sg = segs.n == 1 ? 0 : tk.seg;
+      T* const full = static_cast<T*>(segs.full[sg]);
+      const T* const compact = static_cast<const T*>(segs.compact[sg]);
       const uint32_t row_len = static_cast<uint32_t>(d.cols) * d.inner;
       if (row_len >= kSliceThreads) {
         if (rows_vectorizable<T>(tk, d, full, compact, row_len))
@@ -489,24 +503,15 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask, int
   return SDP_OK;
 }
 
-int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
-                      int n_tasks, const int32_t* fwd_maps, const void* full, void* compact,
-                      int flags, void* stream) {
-  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
-  if (n_tasks == 0) return SDP_OK;
-  if (!descs || !tasks || !full || !compact) return set_error(SDP_ERR_USAGE, "null device pointer");
+static int gather_launch(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks, int n_tasks,
+                         const int32_t* fwd_maps, const SegPtrs& sp, int flags, void* stream) {
   cudaStream_t s = as_stream(stream);
   const bool rev = (flags & SDP_GATHER_REVERSE) != 0;
   const int grid = slice_grid(n_tasks);
-  void* fu = const_cast<void*>(full);
-#define SDP_GATHER(TT)                                                                          \
-  do {                                                                                          \
-    if (rev)                                                                                    \
-      k_gather<TT, true><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps,        \
-                                                           static_cast<TT*>(fu), static_cast<TT*>(compact)); \
-    else                                                                                        \
-      k_gather<TT, false><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps,       \
-                                                            static_cast<TT*>(fu), static_cast<TT*>(compact)); \
+#define SDP_GATHER(TT)                                                                              \
+  do {                                                                                              \
+    if (rev) k_gather<TT, true><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps, sp);  \
+    else k_gather<TT, false><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, fwd_maps, sp);     \
   } while (0)
   if (dtype == SDP_DTYPE_F32) SDP_GATHER(float);
   else if (dtype == SDP_DTYPE_F64) SDP_GATHER(double);
@@ -518,24 +523,81 @@ int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_ta
   return SDP_OK;
 }
 
+static int scatter_launch(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks, int n_tasks,
+                          const int32_t* inv_maps, const SegPtrs& sp, int flags, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const int grid = slice_grid(n_tasks);
+  if (dtype == SDP_DTYPE_F32)
+    k_scatter<float><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, sp, flags);
+  else if (dtype == SDP_DTYPE_F64)
+    k_scatter<double><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, sp, flags);
+  else
+    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+static int segs_from(const sdp_slice_segs* in, SegPtrs& sp, bool need_compact) {
+  if (!in) return set_error(SDP_ERR_USAGE, "null segment table");
+  if (in->n < 1 || in->n > SDP_MAX_WORKERS)
+    return set_error(SDP_ERR_CONFIG, "segment count %d outside [1, %d]", in->n, SDP_MAX_WORKERS);
+  sp = SegPtrs{};
+  sp.n = in->n;
+  for (int k = 0; k < in->n; ++k) {
+    if (!in->full[k] || (need_compact && !in->compact[k]))
+      return set_error(SDP_ERR_USAGE, "segment %d has a null buffer", k);
+    sp.full[k] = const_cast<void*>(in->full[k]);
+    sp.compact[k] = const_cast<void*>(in->compact[k]);
+  }
+  return SDP_OK;
+}
+
+int sdp_gather_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                      int n_tasks, const int32_t* fwd_maps, const void* full, void* compact,
+                      int flags, void* stream) {
+  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
+  if (n_tasks == 0) return SDP_OK;
+  if (!descs || !tasks || !full || !compact) return set_error(SDP_ERR_USAGE, "null device pointer");
+  SegPtrs sp{};
+  sp.n = 1;
+  sp.full[0] = const_cast<void*>(full);
+  sp.compact[0] = compact;
+  return gather_launch(dtype, descs, tasks, n_tasks, fwd_maps, sp, flags, stream);
+}
+
+int sdp_gather_slices_multi(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                            int n_tasks, const int32_t* fwd_maps, const sdp_slice_segs* segs, int flags,
+                            void* stream) {
+  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
+  SegPtrs sp;
+  if (int rc = segs_from(segs, sp, true)) return rc;
+  if (n_tasks == 0) return SDP_OK;
+  if (!descs || !tasks) return set_error(SDP_ERR_USAGE, "null device pointer");
+  return gather_launch(dtype, descs, tasks, n_tasks, fwd_maps, sp, flags, stream);
+}
+
 int sdp_scatter_slices(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
                        int n_tasks, const int32_t* inv_maps, const void* compact, void* full,
                        int flags, void* stream) {
   if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
   if (n_tasks == 0) return SDP_OK;
   if (!descs || !tasks || !full) return set_error(SDP_ERR_USAGE, "null device pointer");
-  cudaStream_t s = as_stream(stream);
-  const int grid = slice_grid(n_tasks);
-  if (dtype == SDP_DTYPE_F32)
-    k_scatter<float><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, static_cast<const float*>(compact),
-                                                       static_cast<float*>(full), flags);
-  else if (dtype == SDP_DTYPE_F64)
-    k_scatter<double><<<grid, kSliceThreads, 0, s>>>(descs, tasks, n_tasks, inv_maps, static_cast<const double*>(compact),
-                                                        static_cast<double*>(full), flags);
-  else
-    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
-  SDP_LAUNCH_CHECK();
-  return SDP_OK;
+  SegPtrs sp{};
+  sp.n = 1;
+  sp.full[0] = full;
+  sp.compact[0] = const_cast<void*>(compact);
+  return scatter_launch(dtype, descs, tasks, n_tasks, inv_maps, sp, flags, stream);
+}
+
+int sdp_scatter_slices_multi(int dtype, const sdp_slice_desc* descs, const sdp_slice_task* tasks,
+                             int n_tasks, const int32_t* inv_maps, const sdp_slice_segs* segs, int flags,
+                             void* stream) {
+  if (n_tasks < 0) return set_error(SDP_ERR_USAGE, "negative task count");
+  SegPtrs sp;
+  if (int rc = segs_from(segs, sp, false)) return rc;
+  if (n_tasks == 0) return SDP_OK;
+  if (!descs || !tasks) return set_error(SDP_ERR_USAGE, "null device pointer");
+  return scatter_launch(dtype, descs, tasks, n_tasks, inv_maps, sp, flags, stream);
 }
 
 int sdp_divide(int dtype, const void* acc, const double* divisor, int64_t total, void* out,

@@ -78,6 +78,7 @@ class _DescBuilder:
         tasks = slice_tasks(descs, compact=True)
         maps = np.concatenate(self.maps) if self.maps else np.zeros(1, np.int32)
         maps = add_col_tables(descs, maps, inverse=False)
+        self.host = (descs, tasks, maps.astype(np.int32))  # for models.SliceBatch
         return (upload_struct(descs, dev), upload_struct(tasks, dev), len(tasks),
                 torch.from_numpy(maps.astype(np.int32)).to(dev))
 
@@ -200,6 +201,7 @@ class WorkerTransfer:
                 builder.add(sub.offsets[p.name], off, crows, ccols, inner,
                             None if len(rpos) == crows else rpos, None if len(cpos) == ccols else cpos)
         self.d_desc, self.d_tasks, self.n_tasks, self.maps = builder.upload(a.device)
+        self.host = builder.host
         self.compact_total = sub.compact_total
 
     def to_compact(self, theta_sync: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

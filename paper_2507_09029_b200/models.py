@@ -32,7 +32,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from ._device import device, ptr, sdp_dtype, slice_dtype, stream_ptr
-from .errors import ConfigError, InputError
+from .errors import ConfigError, InputError, UsageError
 from .topology import GlobalModel, fast_divisor
 from . import zoo
 
@@ -358,7 +358,7 @@ SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("row
                         ("inner_shr", "<u4"), ("rowlen_mul", "<u4"), ("rowlen_shr", "<u4"),
                         ("col_tab", "<i4")])
 TASK_DTYPE = np.dtype([("desc", "<i4"), ("row_begin", "<i4"), ("row_end", "<i4"),
-                       ("elem_begin", "<i4"), ("elem_end", "<i4"), ("pad_", "<i4", 3)])
+                       ("elem_begin", "<i4"), ("elem_end", "<i4"), ("seg", "<i4"), ("pad_", "<i4", 2)])
 TASK_ELEMS = 4096   # elements per gather/scatter task
 TILE_ELEMS = 2048   # max row elements a tiled task walks (256 threads x 8)
 TILED_MIN = 256     # walked rows at least this long are tiled (sdp_slices.cu)
@@ -382,11 +382,11 @@ def slice_tasks(descs: np.ndarray, compact: bool, per_task: int = TASK_ELEMS) ->
             k = max(1, per_task // chunk)
             for e in range(0, row_len, chunk):
                 for r in range(0, rows, k):
-                    out.append((i, r, min(rows, r + k), e, min(row_len, e + chunk), (0, 0, 0)))
+                    out.append((i, r, min(rows, r + k), e, min(row_len, e + chunk), 0, (0, 0)))
         else:
             k = max(1, per_task // row_len)
             for r in range(0, rows, k):
-                out.append((i, r, min(rows, r + k), 0, row_len, (0, 0, 0)))
+                out.append((i, r, min(rows, r + k), 0, row_len, 0, (0, 0)))
     return np.array(out, dtype=TASK_DTYPE)
 
 
@@ -416,6 +416,72 @@ def add_col_tables(descs: np.ndarray, maps: np.ndarray, inverse: bool) -> np.nda
         tabs[i] = seen[key]
     descs["col_tab"] = tabs
     return np.concatenate(parts)
+
+
+class SliceBatch:
+    """Several workers' slice tables concatenated so ONE sdp_*_slices_multi
+    launch moves all of them (task `seg` = the part's position): the
+    co-resident trainer's N gathers / scatters per step become one launch
+    each, large enough to be bandwidth- rather than launch-latency-bound.
+
+    parts: [(descs, tasks, maps)] host tables (SubnetLayout.host_gather /
+    host_scatter, layout.WorkerTransfer.host) -- descriptor map offsets and
+    task descriptor indices are rebased onto the concatenation."""
+
+    def __init__(self, parts, dev):
+        from ._device import upload_struct
+        if not 1 <= len(parts) <= N.MAX_WORKERS:
+            raise ConfigError(f"a slice batch holds 1..{N.MAX_WORKERS} parts, got {len(parts)}")
+        ds, ts, ms = [], [], []
+        nd = nm = 0
+        for k, (descs, tasks, maps) in enumerate(parts):
+            d = descs.copy()
+            for f in ("row_map", "col_map", "col_tab"):
+                d[f] = np.where(d[f] >= 0, d[f] + nm, d[f])
+            t = tasks.copy()
+            t["desc"] += nd
+            t["seg"] = k
+            ds.append(d)
+            ts.append(t)
+            ms.append(maps)
+            nd += len(descs)
+            nm += len(maps)
+        descs = np.concatenate(ds)
+        tasks = np.concatenate(ts)
+        # interleave the parts' tasks (round-robin) so every wave of the
+        # persistent CTAs streams several workers' tensors at once
+        order = np.argsort(np.concatenate([np.arange(len(t)) for t in ts]), kind="stable")
+        tasks = tasks[order]
+        self.n_parts = len(parts)
+        self.d_descs = upload_struct(descs, dev)
+        self.d_tasks = upload_struct(tasks, dev)
+        self.n_tasks = len(tasks)
+        self.maps = torch.from_numpy(np.concatenate(ms).astype(np.int32)).to(dev)
+        self.device = dev
+
+    def _segs(self, fulls, compacts) -> N.SliceSegs:
+        if len(fulls) != self.n_parts or len(compacts) != self.n_parts:
+            raise UsageError(f"slice batch of {self.n_parts} parts got {len(fulls)} / {len(compacts)} buffers")
+        sg = N.SliceSegs()
+        sg.n = self.n_parts
+        for k, (f, c) in enumerate(zip(fulls, compacts)):
+            sg.full[k] = ptr(f)
+            sg.compact[k] = ptr(c)
+        return sg
+
+    def gather(self, fulls, compacts, reverse: bool = False) -> None:
+        """compacts[k][...] = fulls[k][...] for every part (REVERSE: the other way)."""
+        dt = slice_dtype(fulls[0].dtype)
+        sg = self._segs(fulls, compacts)
+        N.call("sdp_gather_slices_multi", dt, ptr(self.d_descs), ptr(self.d_tasks), self.n_tasks, ptr(self.maps),
+               C.byref(sg), N.GATHER_REVERSE if reverse else 0, stream_ptr(self.device))
+
+    def scatter(self, compacts, fulls, accumulate: bool = False) -> None:
+        """fulls[k] = scatter(compacts[k]) (zero fill) or += for every part."""
+        sg = self._segs(fulls, compacts)
+        flags = N.SCATTER_ACCUMULATE if accumulate else N.SCATTER_ZERO_FILL
+        N.call("sdp_scatter_slices_multi", sdp_dtype(compacts[0].dtype), ptr(self.d_descs), ptr(self.d_tasks),
+               self.n_tasks, ptr(self.maps), C.byref(sg), flags, stream_ptr(self.device))
 
 
 class SubnetLayout:
@@ -519,6 +585,9 @@ class SubnetLayout:
         self.d_inv = upload_struct(descs_inv, dev)
         g_tasks = slice_tasks(descs, compact=True)
         s_tasks = slice_tasks(descs, compact=False)
+        # host copies: SliceBatch concatenates several workers' tables
+        self.host_gather = (descs, g_tasks, fw.astype(np.int32))
+        self.host_scatter = (descs_inv, s_tasks, iv.astype(np.int32))
         self.t_gather, self.n_gather = upload_struct(g_tasks, dev), len(g_tasks)
         self.t_scatter, self.n_scatter = upload_struct(s_tasks, dev), len(s_tasks)
         self.fwd_maps = torch.from_numpy(fw.astype(np.int32)).to(dev)

@@ -587,7 +587,8 @@ class _GradStore:
             self._slots[w] = param_views(self.model.topology, self.grads[w])
         return self._slots[w]
 
-    def _compact_step_bf16(self, w: int, x, y, cache: bool, src: torch.Tensor | None = None) -> torch.Tensor:
+    def _compact_step_bf16(self, w: int, x, y, cache: bool, src: torch.Tensor | None = None,
+                           cvec: torch.Tensor | None = None, g_out: torch.Tensor | None = None) -> torch.Tensor:
         """Width-wise worker step under bf16 autocast: the compact parameters
         are per-parameter leaves (conv weights made channels-last once, as
         cuDNN's NHWC kernels want them), so the backward returns per-parameter
@@ -597,7 +598,8 @@ class _GradStore:
         weights back in OIHW order, and the sync-space transfer."""
         sub = self.subs[w]
         src = self.theta_bf16 if src is None else src
-        cvec = self.transfers[w].to_compact(src) if self.slayout else sub.gather(src)
+        if cvec is None:  # else: the step's batched gather already extracted it
+            cvec = self.transfers[w].to_compact(src) if self.slayout else sub.gather(src)
         views = sub.views(cvec)
         if getattr(self, "_cg_max", None) is None:
             self._cg_max = N.lib().sdp_conv_grad_max_block()
@@ -648,16 +650,17 @@ class _GradStore:
             dst.append(slot)
             src.append(g)
         torch._foreach_copy_(dst, src)
-        g32 = self._cbuf32[:max(1, n)]
+        g32 = self._cbuf32[:max(1, n)] if g_out is None else g_out
         g32.copy_(self._cbuf[:max(1, n)])  # conv slots are OHWI here; rewritten below
         if conv:
             descs, max_o = self._conv_table(("g", w, tuple(conv)), [slots[k] for k in conv])
             N.call("sdp_conv_grads_to_oihw", ptr(descs), len(conv), max_o, ptr(self._cbuf), ptr(g32),
                    stream_ptr(cvec.device))
-        if self.slayout:
-            self.transfers[w].from_compact(g32, self.grads[w])
-        else:
-            sub.scatter(g32, self.grads[w])
+        if g_out is None:  # else: the step's batched scatter writes every worker's replica
+            if self.slayout:
+                self.transfers[w].from_compact(g32, self.grads[w])
+            else:
+                sub.scatter(g32, self.grads[w])
         return loss.detach()
 
     def _conv_table(self, key, views: list):
@@ -907,32 +910,62 @@ class SubnetTrainer(_GradStore):
             out["__wte_padded"] = _LinearCrossEntropy._padded(views["wte"], torch.bfloat16)
         return out
 
+    def _batches(self):
+        """The step's two slice launches over ALL workers (models.SliceBatch):
+        extraction of every worker's compact parameters before the first
+        forward, write-back of every compact gradient after the last backward."""
+        if getattr(self, "_xfer", None) is None:
+            from .models import SliceBatch
+            dev = self.master.device
+            if self.slayout:
+                parts = [t.host for t in self.transfers]
+                self._xfer = (SliceBatch(parts, dev), SliceBatch(parts, dev))
+            else:
+                self._xfer = (SliceBatch([s_.host_gather for s_ in self.subs], dev),
+                              SliceBatch([s_.host_scatter for s_ in self.subs], dev))
+        return self._xfer
+
+    def _extract_all(self, src: torch.Tensor) -> list:
+        """Every worker's compact parameters from `src` in ONE launch."""
+        gather_b, _ = self._batches()
+        outs = [torch.empty(max(1, s_.compact_total), dtype=src.dtype, device=src.device) for s_ in self.subs]
+        if self.slayout:  # transfer tables: "full" = the compact tensor, "compact" = the sync block
+            gather_b.gather(outs, [src] * len(outs), reverse=True)
+        else:
+            gather_b.gather([src] * len(outs), outs)
+        return outs
+
+    def _write_back_all(self, gs: list) -> None:
+        """Every worker's compact gradient into its fp32 replica in ONE launch."""
+        _, scatter_b = self._batches()
+        if self.slayout:
+            scatter_b.gather(gs, self.grads)
+        else:
+            scatter_b.scatter(gs, self.grads)
+
     def _step_eager(self, batches, cache: bool = True) -> torch.Tensor:
         topo = self.model.topology
         step_params = None
         losses = []
+        if self.compact:
+            # the workers train on the bf16 copy the previous sync wrote
+            src = self.theta_bf16 if self.autocast else self.master
+            cvecs = self._extract_all(src)
+            g32s = [torch.empty(max(1, s_.compact_total), dtype=torch.float32, device=src.device)
+                    for s_ in self.subs]
         for w, (x, y) in enumerate(batches):
             if self.compact and self.autocast:
-                losses.append(self._compact_step_bf16(w, x, y, cache))
+                losses.append(self._compact_step_bf16(w, x, y, cache, cvec=cvecs[w], g_out=g32s[w]))
                 continue
             if self.compact:
                 sub = self.subs[w]
-                # the worker trains on the bf16 copy the previous sync wrote
-                src = self.theta_bf16 if self.autocast else self.master
-                if self.slayout:  # the worker's blocks of the permuted theta
-                    leaf = self.transfers[w].to_compact(src).requires_grad_(True)
-                else:
-                    leaf = sub.gather(src).requires_grad_(True)  # sdp_gather_slices
+                leaf = cvecs[w][:sub.compact_total].requires_grad_(True)
                 with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
                     logits = self.model.arch.forward_compact(sub.views(leaf), x, sub)
                     loss = self.loss_fn(logits, y)
                 del logits
                 (g,) = torch.autograd.grad(loss, leaf)
-                g = g.float()  # fp32 gradient replica (the sync accumulates in fp32)
-                if self.slayout:
-                    self.transfers[w].from_compact(g, self.grads[w])
-                else:
-                    sub.scatter(g, self.grads[w])  # sdp_scatter_slices, zero fill
+                g32s[w][:sub.compact_total].copy_(g)  # fp32 gradient replica (the sync accumulates in fp32)
                 losses.append(loss.detach())
                 continue
             # the worker trains on the bf16 weights the previous sync wrote;
@@ -950,6 +983,8 @@ class SubnetTrainer(_GradStore):
             gs = torch.autograd.grad(loss, [params[k] for k in names])
             self._store_grads(w, names, gs)
             losses.append(loss.detach())
+        if self.compact:
+            self._write_back_all(g32s)
         self._sync()
         return torch.stack(losses).mean()
 

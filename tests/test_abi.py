@@ -80,6 +80,7 @@ int main(void) {
   printf("sdp_update_desc %zu\n", sizeof(sdp_update_desc));
   F(sdp_slice_desc, rows) F(sdp_slice_desc, col_map) F(sdp_slice_desc, inner_shr)
   printf("sdp_slice_task %zu\n", sizeof(sdp_slice_task));
+  printf("sdp_slice_segs %zu\n", sizeof(sdp_slice_segs));
   return 0;
 }
 """
@@ -100,6 +101,7 @@ def test_struct_layouts_match_c(tmp_path):
     assert int(out["sdp_rule_desc"]) == C.sizeof(N.RuleDesc)
     assert int(out["sdp_group_desc"]) == C.sizeof(N.GroupDesc)
     assert int(out["sdp_slice_task"]) == C.sizeof(N.SliceTask) == 32
+    assert int(out["sdp_slice_segs"]) == C.sizeof(N.SliceSegs)
     assert int(out["sdp_worker_state"]) == C.sizeof(N.WorkerState) == 40
     assert int(out["sdp_update_desc"]) == C.sizeof(N.UpdateDesc) == 16
     from paper_2507_09029_b200.models import SLICE_DTYPE, TASK_DTYPE

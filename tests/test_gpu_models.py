@@ -214,6 +214,52 @@ def test_gather_scatter_all_paths_full_size(cuda, strategy, dtype):
         assert torch.equal(acc, torch.where(mask, base + theta, base))
 
 
+@pytest.mark.parametrize("strategy,dtype", [("neuron", torch.float32), ("block", torch.float32),
+                                            ("neuron", torch.float64), ("neuron", torch.bfloat16)])
+def test_slice_batch_one_launch_equals_per_worker(cuda, strategy, dtype):
+    """models.SliceBatch: all 8 workers' gathers (and zero-fill / accumulate
+    scatters) in ONE sdp_*_slices_multi launch == the per-worker launches,
+    bit for bit, for the flat layout and for the sync-layout transfers."""
+    from paper_2507_09029_b200 import masking, models, zoo
+    from paper_2507_09029_b200.layout import SyncLayout, WorkerTransfer
+    topo = zoo.resnet18_cifar_topology()
+    a = masking.build_assignment(topo, strategy, 8, 4, seed=1)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(11)
+    theta = torch.randn(topo.total, generator=gen, device=cuda).to(dtype)
+    subs = [models.SubnetLayout(a, w) for w in range(8)]
+    gb = models.SliceBatch([s.host_gather for s in subs], cuda)
+    outs = [torch.empty(max(1, s.compact_total), dtype=dtype, device=cuda) for s in subs]
+    gb.gather([theta] * 8, outs)
+    for s, o in zip(subs, outs):
+        ref = s.gather(theta)
+        assert torch.equal(o[:s.compact_total].view(torch.uint8), ref[:s.compact_total].view(torch.uint8))
+    if dtype == torch.bfloat16:
+        return  # scatters are fp32 / fp64 only
+    sb = models.SliceBatch([s.host_scatter for s in subs], cuda)
+    fulls = [torch.full((topo.total,), 7.0, dtype=dtype, device=cuda) for _ in subs]
+    sb.scatter(outs, fulls)
+    base = torch.randn(topo.total, generator=gen, device=cuda).to(dtype)
+    accs = [base.clone() for _ in subs]
+    sb.scatter(outs, accs, accumulate=True)
+    for s, o, f, acc in zip(subs, outs, fulls, accs):
+        assert torch.equal(f, s.scatter(o))
+        assert torch.equal(acc, s.scatter(o, base.clone(), accumulate=True))
+    if strategy != "neuron" or dtype != torch.float32:
+        return
+    lay = SyncLayout(a)
+    trs = [WorkerTransfer(lay, s) for s in subs]
+    tb = models.SliceBatch([t.host for t in trs], cuda)
+    ts = lay.to_sync(theta)
+    comps = [torch.empty(max(1, s.compact_total), device=cuda) for s in subs]
+    tb.gather(comps, [ts] * 8, reverse=True)
+    grads = [torch.zeros(topo.total, device=cuda) for _ in subs]
+    tb.gather(comps, grads)
+    for t, c, g in zip(trs, comps, grads):
+        assert torch.equal(c[:t.compact_total], t.to_compact(ts)[:t.compact_total])
+        assert torch.equal(g, t.from_compact(c, torch.zeros(topo.total, device=cuda)))
+
+
 @pytest.mark.parametrize("shape", [(64, (32, 32), 32), (16, (29, 35), 12), (8, (300, 212), 4), (64, (256, 256), 4),
                                    (4, (7, 1, 24), 16)])
 def test_group_norm_backward_is_deterministic(cuda, shape):

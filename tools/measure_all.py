@@ -128,6 +128,21 @@ def slices_case(topo, tag, strategy, n, p):
     us, us_min = timed(lambda: sub.scatter(comp, full, accumulate=True))
     emit("k_scatter(accumulate)", tag, us, us_min, sub.compact_total * 12, compact=sub.compact_total,
          d=topo.total)
+    # all N workers in ONE launch (models.SliceBatch): what the co-resident trainer runs
+    subs = [models.SubnetLayout(a, w) for w in range(n)]
+    tot = sum(s_.compact_total for s_ in subs)
+    gb = models.SliceBatch([s_.host_gather for s_ in subs], DEV)
+    sb = models.SliceBatch([s_.host_scatter for s_ in subs], DEV)
+    comps = [torch.empty(max(1, s_.compact_total), device=DEV) for s_ in subs]
+    fulls = [torch.empty(topo.total, device=DEV) for _ in subs]
+    us, us_min = timed(lambda: gb.gather([theta] * n, comps))
+    emit("k_gather(all workers)", tag, us, us_min, tot * 8, compact=tot, d=topo.total, n=n)
+    us, us_min = timed(lambda: sb.scatter(comps, fulls))
+    emit("k_scatter(zero-fill, all workers)", tag, us, us_min, tot * 4 + n * topo.total * 4, compact=tot,
+         d=topo.total, n=n)
+    us, us_min = timed(lambda: sb.scatter(comps, fulls, accumulate=True))
+    emit("k_scatter(accumulate, all workers)", tag, us, us_min, tot * 12, compact=tot, d=topo.total, n=n)
+    del fulls
     view = a.worker_view(0)
     out = torch.empty_like(theta)
     us, us_min = timed(lambda: N.call("sdp_masked_extract", 0, ptr(theta), ptr(view.param_mask_bool), 1,
@@ -142,6 +157,14 @@ def slices_case(topo, tag, strategy, n, p):
         emit("k_gather(to_sync)", tag, us, us_min, topo.total * 8, d=topo.total)
         us, us_min = timed(lambda: lay.from_sync(ts, theta))
         emit("k_gather(from_sync, reverse)", tag, us, us_min, topo.total * 8, d=topo.total)
+        trs = [WorkerTransfer(lay, s_) for s_ in subs]
+        tb = models.SliceBatch([t.host for t in trs], DEV)
+        grads = [torch.zeros(topo.total, device=DEV) for _ in subs]
+        us, us_min = timed(lambda: tb.gather(comps, [ts] * n, reverse=True))
+        emit("k_gather(to_compact, reverse, all workers)", tag, us, us_min, tot * 8, compact=tot, d=topo.total, n=n)
+        us, us_min = timed(lambda: tb.gather(comps, grads))
+        emit("k_gather(from_compact, all workers)", tag, us, us_min, tot * 8, compact=tot, d=topo.total, n=n)
+        del grads
         tr = WorkerTransfer(lay, sub)
         us, us_min = timed(lambda: tr.to_compact(ts, comp))
         emit("k_gather(to_compact, reverse)", tag, us, us_min, sub.compact_total * 8,

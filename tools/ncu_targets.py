@@ -33,6 +33,19 @@ def main():
         for _ in range(3):
             sub.gather(theta, comp)
             sub.scatter(comp, full)
+    if "slices_all_r18" in which:  # all 8 workers per launch (models.SliceBatch)
+        topo = zoo.resnet18_cifar_topology()
+        a = masking.build_assignment(topo, "neuron", 8, 4, seed=1)
+        subs = [models.SubnetLayout(a, w) for w in range(8)]
+        gb = models.SliceBatch([s.host_gather for s in subs], dev)
+        sb = models.SliceBatch([s.host_scatter for s in subs], dev)
+        theta = torch.randn(topo.total, device=dev)
+        comps = [torch.empty(max(1, s.compact_total), device=dev) for s in subs]
+        fulls = [torch.empty(topo.total, device=dev) for _ in subs]
+        for _ in range(4):
+            gb.gather([theta] * 8, comps)
+            sb.scatter(comps, fulls)
+            sb.scatter(comps, fulls, accumulate=True)
     if "sync_r18" in which:
         from paper_2507_09029_b200 import engine
         topo = zoo.resnet18_cifar_topology()
