@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10)
     ap.add_argument("--no-memory-ranks", action="store_true")
+    ap.add_argument("--equal-loss-steps", type=int, default=1500,
+                    help="steps of the equal-compute subnet-vs-DP loss run (0: skip)")
     ap.add_argument("--memory-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -385,6 +387,8 @@ def run_ours(args):
             train = {"c4_gpt2": run_train_gpt2(args, dev), "c2_c3_resnet18": run_train(args, dev)}
             if not args.no_memory_ranks and args.n_logical == 8:
                 train["memory_n8_ranks"] = run_memory_ranks(args)
+            if args.equal_loss_steps > 0 and args.n_logical == 8 and args.p == 4:
+                train["equal_loss"] = run_equal_loss(args, dev, train.get("memory_n8_ranks"))
             if args.n_logical == 8 and args.p == 4:
                 c1 = argparse.Namespace(**{**vars(args), "n_logical": 4, "p": 2})
                 train["c1_mini_resnet"] = run_train_c1(c1, dev)
@@ -518,6 +522,23 @@ def run_train(args, dev):
                       "channel-slice compact subnetworks (gather/scatter kernels) P=4",
                       "dp": "full-replica DP comparator (P=N)"}
     out["memory"] = "peak memory per GPU: train.memory_n8_ranks (measured in 8 real rank processes)"
+    return out
+
+
+def run_equal_loss(args, dev, memory: dict | None) -> dict:
+    """North-star memory target "at equal loss": the C2 / C3 subnetwork runs
+    and the P = N DP comparator trained for the same steps on the same
+    learnable synthetic task (tools/equal_loss.py), next to the peak memory
+    per GPU the 8-rank run measured for the same configurations."""
+    sys.path.insert(0, str(ROOT / "tools"))
+    from equal_loss import equal_loss
+    out = equal_loss(dev, steps=args.equal_loss_steps)
+    if memory and "resnet18_subnet" in memory and "resnet18_dp" in memory:
+        sub, dp = memory["resnet18_subnet"], memory["resnet18_dp"]
+        out["peak_memory_vs_dp"] = {
+            "subnet_largest_rank": sub["peak_bytes_max"] / dp["peak_bytes_max"] - 1.0,
+            "subnet_mean_rank": sub["peak_bytes_mean"] / dp["peak_bytes_mean"] - 1.0,
+            "source": "train.memory_n8_ranks (ResNet-18 C2, 8 PeerTrainer rank processes, compact storage)"}
     return out
 
 
