@@ -18,6 +18,7 @@ optionally fused with the SGD-Nesterov update (optim.py:78-84).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import sys
 import threading
 from dataclasses import dataclass
@@ -422,12 +423,8 @@ def aggregate(grads, assignment) -> AggregatedGradient:
         hosts = [torch.from_numpy(np.ascontiguousarray(g, dtype=dt_np(dt))) for g in grads]
         if all(h.numel() == d and _aligned(h) and _device_readable(h) for h in hosts):
             return _aggregate_host_zero_copy(hosts, assignment, check)
-    if host and not check:
-        return _aggregate_host_pipelined(grads, assignment)
     if host:
-        # pageable inputs + the uncovered-leak check (it reads every worker at
-        # zero-coverage entries): plain copies
-        reps = [h.to(dev, non_blocking=True) for h in hosts]
+        return _aggregate_host_staged([h.numpy() for h in hosts], assignment, check)
     else:
         reps = _as_replica_list(grads, n, d)
         dt = reps[0].dtype
@@ -442,9 +439,6 @@ def aggregate(grads, assignment) -> AggregatedGradient:
         torch.cuda.current_stream(dev).synchronize()
         return AggregatedGradient(gbar=out_np, divisor=assignment.host_divisor())
     return AggregatedGradient(gbar=gbar, divisor=assignment.divisor)
-
-
-HOST_CHUNKS = 4  # tuned on B200 (tools/e2e_probe.py): 4 chunks 5.36 ms, 8 5.46, 1 5.76
 
 
 class _PinnedResults:
@@ -514,46 +508,111 @@ def _aggregate_host_zero_copy(hosts, assignment, check: bool) -> AggregatedGradi
     return AggregatedGradient(gbar=out_np, divisor=assignment.host_divisor())
 
 
-def _aggregate_host_pipelined(grads, assignment) -> AggregatedGradient:
-    """Host-buffer aggregate: the vector is cut into HOST_CHUNKS tile ranges and
-    pipelined over three streams -- H2D of chunk c (only the tiles each worker
-    owns an element of: the kernel never reads the rest), the owner sync of
-    chunk c, and the D2H of chunk c's mean into pinned memory overlap with the
-    neighbouring chunks (PCIe is full duplex)."""
+STAGE_CHUNK_BYTES = 64 << 20  # bytes staged per pipeline chunk (all workers together)
+STAGE_SLOTS = 3               # pinned staging slots in flight
+STAGE_PIECE = 4 << 20         # bytes per host-thread memcpy piece
+_STAGING: dict = {}
+_COPY_POOL = None
+
+
+def _copy_pool():
+    """Host threads for the pageable -> pinned staging copies (numpy copies
+    release the GIL)."""
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        import concurrent.futures
+        _COPY_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+    return _COPY_POOL
+
+
+def _staging(dev, dt: torch.dtype, elems: int):
+    """Pinned staging slots (cached per device and dtype, grown on demand)."""
+    key = (dev, dt)
+    st = _STAGING.get(key)
+    if st is None or st[0].numel() < STAGE_SLOTS * elems:
+        buf = torch.empty(STAGE_SLOTS * elems, dtype=dt, pin_memory=True)
+        st = (buf, buf.numpy(), [torch.cuda.Event() for _ in range(STAGE_SLOTS)], [False] * STAGE_SLOTS)
+        _STAGING[key] = st
+    return st
+
+
+_STAGE_LOCK = threading.Lock()
+
+
+def _aggregate_host_staged(grads, assignment, check: bool) -> AggregatedGradient:
+    with _STAGE_LOCK:  # one caller at a time owns the staging slots
+        return _host_staged(grads, assignment, check)
+
+
+def _host_staged(grads, assignment, check: bool) -> AggregatedGradient:
+    """Host-buffer aggregate over ordinary (pageable) numpy arrays -- what a
+    reference caller passes (engine.run hands over flat_gradient outputs).
+    The vector is cut into tile-range chunks of ~STAGE_CHUNK_BYTES of input;
+    per chunk, a pool of host threads copies every worker's owned ranges into
+    a pinned staging slot (a single-threaded driver staging copy ran ~4x
+    slower), the copy engine moves the slot to the device replicas, the owner
+    sync runs on the chunk, and the mean's D2H goes into a pinned result --
+    host copies of chunk c+1 overlap the H2D / sync / D2H of chunk c.  With
+    the uncovered-leak check every worker's full range is staged (the kernel
+    reads all workers at zero-coverage entries)."""
     n, d = assignment.n_workers, assignment.topology.total
     dev = assignment.device
     dt = torch.float64 if grads[0].dtype == np.float64 else torch.float32
+    esz = 8 if dt == torch.float64 else 4
     full = assignment.sync_plan()
     tile = full.tile
     n_tiles = len(full.all_tiles)
-    k = max(1, min(HOST_CHUNKS, n_tiles))
+    ranges = [[(0, d)] if check else full.worker_ranges(w) for w in range(n)]
+    staged = sum(ln for rs in ranges for _, ln in rs)
+    k = max(1, min(n_tiles, -(-staged * esz // STAGE_CHUNK_BYTES)))
     bounds = [n_tiles * c // k for c in range(k + 1)]
-    hosts = [torch.from_numpy(np.ascontiguousarray(g, dtype=dt_np(dt))) for g in grads]
+    chunks = []
+    for c in range(k):
+        lo_e, hi_e = bounds[c] * tile, min(d, bounds[c + 1] * tile)
+        pieces, off = [], 0
+        for w in range(n):
+            for s, ln in ranges[w]:
+                a, b = max(s, lo_e), min(s + ln, hi_e)
+                if a < b:
+                    pieces.append((w, a, b, off))
+                    off += b - a
+        chunks.append((lo_e, hi_e, pieces, off))
+    slot_elems = max(1, max(ch[3] for ch in chunks))
+    buf, buf_np, evs, used = _staging(dev, dt, slot_elems)
     reps = [torch.empty(d, dtype=dt, device=dev) for _ in range(n)]
     gbar = torch.empty(d, dtype=dt, device=dev)
     out_np, out = _RESULTS.get(d, dt)
     cur = torch.cuda.current_stream(dev)
     s_in, s_out = _copy_streams(dev)
     s_in.wait_stream(cur)
-    for c in range(k):
-        lo_e, hi_e = bounds[c] * tile, min(d, bounds[c + 1] * tile)
+    pool = _copy_pool()
+    piece = max(1, STAGE_PIECE // esz)
+    status = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
+    for c, (lo_e, hi_e, pieces, _) in enumerate(chunks):
+        slot = c % STAGE_SLOTS
+        if used[slot]:
+            evs[slot].synchronize()  # the slot's previous H2D has drained
+        base = slot * slot_elems
+        jobs = [(w, a0, min(a0 + piece, b), off + (a0 - a))
+                for w, a, b, off in pieces for a0 in range(a, b, piece)]
+        list(pool.map(lambda j: np.copyto(buf_np[base + j[3]:base + j[3] + j[2] - j[1]], grads[j[0]][j[1]:j[2]]),
+                      jobs))
         with torch.cuda.stream(s_in):
-            for w in range(n):
-                for s, ln in full.worker_ranges(w):
-                    a, b = max(s, lo_e), min(s + ln, hi_e)
-                    if a < b:
-                        reps[w][a:b].copy_(hosts[w][a:b], non_blocking=True)
-        ev_in = torch.cuda.Event()
-        ev_in.record(s_in)
-        cur.wait_event(ev_in)
+            for w, a, b, off in pieces:
+                reps[w][a:b].copy_(buf[base + off:base + off + b - a], non_blocking=True)
+            evs[slot].record(s_in)
+            used[slot] = True
+        cur.wait_event(evs[slot])
         plan = assignment.sync_plan(tile=tile, tile_lo=bounds[c], tile_hi=bounds[c + 1])
-        owner_sync(reps, assignment, out=gbar, writeback=False, plan=plan)
+        owner_sync(reps, assignment, out=gbar, writeback=False, plan=plan, check_uncovered=check, status=status)
         ev_c = torch.cuda.Event()
         ev_c.record(cur)
         s_out.wait_event(ev_c)
         with torch.cuda.stream(s_out):
             out[lo_e:hi_e].copy_(gbar[lo_e:hi_e], non_blocking=True)
     s_out.synchronize()
+    if check and int(status.item()) & N.STATUS_UNCOVERED_LEAK:
+        raise ProtocolError("a gradient reached a parameter with zero mask coverage")
     for r in reps + [gbar]:
         r.record_stream(s_in)
     return AggregatedGradient(gbar=out_np, divisor=assignment.host_divisor())

@@ -66,11 +66,11 @@ print(f'8 full H2D: {ms:.3f} ms  {8 * d * 4 / ms / 1e6:.1f} GB/s')
 ms = tm(lambda: [dst[w][s:s + ln].copy_(torch.from_numpy(host[w])[s:s + ln], non_blocking=True)
                  for w in range(8) for s, ln in rng[w]])
 print(f'owned-range H2D: {ms:.3f} ms  {owned / ms / 1e6:.1f} GB/s')
-for k in (1, 2, 4, 8, 16):
-    engine.HOST_CHUNKS = k
-    ms = tm(lambda: engine.aggregate(host, a))
-    print(f'aggregate {k:2d} chunks: {ms:.3f} ms  e2e {plan.owned_elems * 4 / ms / 1e6:.1f} GB/s')
-engine.HOST_CHUNKS = 8
+for mb in (16, 32, 64, 128):
+    engine.STAGE_CHUNK_BYTES = mb << 20
+    ms = tm(lambda: engine.aggregate([np.array(h) for h in host], a))
+    print(f'pageable aggregate, {mb} MB chunks: {ms:.3f} ms  e2e {plan.owned_elems * 4 / ms / 1e6:.1f} GB/s')
+engine.STAGE_CHUNK_BYTES = 64 << 20
 t0 = time.perf_counter()
 for _ in range(10):
     engine.aggregate(host, a)
