@@ -16,6 +16,10 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
+from paper_2507_09029_b200 import _native as N  # noqa: E402
+
+if "--lib" in sys.argv:  # an A/B variant (tools/variant_build.py) instead of the in-tree build
+    N.load(sys.argv[sys.argv.index("--lib") + 1])
 from paper_2507_09029_b200 import engine, masking, zoo  # noqa: E402
 
 DEV = torch.device("cuda", 0)
@@ -52,6 +56,8 @@ def main():
     ap.add_argument("--tiles", default="auto")
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--strategy", default="block")
+    ap.add_argument("--lib", default=None)
+    ap.add_argument("--graph-only", action="store_true")
     args = ap.parse_args()
     FW = torch.empty(64 << 20, device=DEV)
     FR = torch.zeros(64 << 20, device=DEV)
@@ -74,7 +80,7 @@ def main():
             print(json.dumps({"row": "copy same traffic", "MiB": mib, "p": p, "bytes": nbytes,
                               "us": round(cm, 2), "frac": round(nbytes / cm / 1e3 / peak, 3)}), flush=True)
             tiles = [None] if args.tiles == "auto" else [int(t) for t in args.tiles.split(",")]
-            for t in tiles:
+            for t in ([] if args.graph_only else tiles):
                 plan = a.sync_plan(tile=t)
                 prep = engine.PreparedSync(reps, a, writeback=True, shadows_bf16=shadows, plan=plan)
                 for cold in (True, False):
