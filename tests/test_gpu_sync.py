@@ -133,6 +133,41 @@ def test_uncovered_leak_pinned_host(cuda):
         engine.aggregate([_pinned(x) for x in grads], a)
 
 
+def test_uncovered_leak_pageable_host(cuda):
+    """The staged pageable path (what engine.run passes) keeps the
+    engine.py:75-78 leak check: every worker's full range is staged."""
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import ProtocolError
+    case = next(c for c in G.cases(with_grads=True) if c["uncovered_params"] > 0)
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    unc = np.nonzero(~masks.any(0))[0]
+    grads[1, unc[-1]] = np.nan
+    with pytest.raises(ProtocolError, match="zero mask coverage"):
+        engine.aggregate([np.array(x) for x in grads], a)
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_pageable_staged_many_chunks_bitexact(cuda, strategy, monkeypatch):
+    """engine.aggregate on pageable numpy inputs with tiny staging chunks
+    (many chunks, every staging slot reused several times): the same bits as
+    the device-input path and the ordered restatement."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    monkeypatch.setattr(engine, "STAGE_CHUNK_BYTES", 1 << 16)
+    monkeypatch.setattr(engine, "STAGE_PIECE", 1 << 12)
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (8, 8))
+    a = masking.build_assignment(topo, strategy, 8, 3, seed=4)
+    masks = a.param_masks.cpu().numpy()
+    rng = np.random.default_rng(3)
+    g32 = (rng.standard_normal((8, topo.total)) * masks).astype(np.float32)
+    host = engine.aggregate([np.array(g) for g in g32], a).gbar
+    dev = engine.aggregate([torch.from_numpy(g).to(cuda) for g in g32], a).gbar.cpu().numpy()
+    assert np.array_equal(host.view(np.uint32), dev.view(np.uint32))
+    assert np.array_equal(host.view(np.uint32), O.aggregate_f32_ordered(list(g32), masks).view(np.uint32))
+
+
 def test_disjoint_known_answer(cuda):
     """SPEC.md:298: m1=[1,0], m2=[0,1], g1=[2,0], g2=[0,4] -> [2,4]."""
     engine, masking = _pkg()
