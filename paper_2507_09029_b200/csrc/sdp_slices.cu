@@ -16,13 +16,49 @@ namespace sdp {
 
 constexpr int kSliceThreads = 256;
 
-template <typename T, int MB>
+// theta * mask_w, 16 B of theta per thread per iteration (VE elements, their
+// VE mask words read as one aligned word when they fit 8 bytes), scalar tail;
+// VEC = false: the scalar loop (unaligned buffers).
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+
+template <typename T, int MB, bool VEC>
 __global__ void k_masked_extract(const T* __restrict__ theta, const typename MaskT<MB>::T* __restrict__ mask,
                                  int64_t total, int worker, T* __restrict__ out) {
-  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  using M = typename MaskT<MB>::T;
+  constexpr int VE = 16 / static_cast<int>(sizeof(T));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t done = 0;
+  if constexpr (VEC) {
+    using VT = typename Vec16<T>::type;
+    const int64_t nvec = total / VE;
+    for (int64_t v = tid; v < nvec; v += stride) {
+      const VT x = __ldg(reinterpret_cast<const VT*>(theta) + v);
+      const T* xe = reinterpret_cast<const T*>(&x);
+      uint64_t mw = 0;  // the VE mask words, packed
+      if constexpr (MB * VE <= 8) {
+        if constexpr (MB * VE == 2) mw = __ldg(reinterpret_cast<const uint16_t*>(mask) + v);
+        else if constexpr (MB * VE == 4) mw = __ldg(reinterpret_cast<const uint32_t*>(mask) + v);
+        else mw = __ldg(reinterpret_cast<const unsigned long long*>(mask) + v);
+      }
+      VT y;
+      T* ye = reinterpret_cast<T*>(&y);
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        uint64_t m;
+        if constexpr (MB * VE <= 8) m = (mw >> (8 * MB * e)) & (MB == 8 ? ~0ull : ((1ull << (8 * MB)) - 1));
+        else m = static_cast<uint64_t>(__ldg(mask + v * VE + e));
+        ye[e] = xe[e] * static_cast<T>((m >> worker) & 1ull);  // a plain multiply: keeps -0.0 / NaN like numpy
+      }
+      reinterpret_cast<VT*>(out)[v] = y;
+    }
+    done = nvec * VE;
+  }
+  for (int64_t j = done + tid; j < total; j += stride) {
     const T m = static_cast<T>((static_cast<uint64_t>(__ldg(mask + j)) >> worker) & 1ull);
-    out[j] = theta[j] * m;  // a plain multiply: keeps -0.0 / NaN like numpy
+    out[j] = theta[j] * m;
   }
 }
 
@@ -484,9 +520,21 @@ int sdp_masked_extract(int dtype, const void* theta, const void* owner_mask, int
   if (total <= 0) return SDP_OK;
   const int grid = grid_for(total);
   cudaStream_t s = as_stream(stream);
-#define SDP_EXTRACT(TT, MB)                                                                  \
-  k_masked_extract<TT, MB><<<grid, kSliceThreads, 0, s>>>(static_cast<const TT*>(theta),    \
-      static_cast<const MaskT<MB>::T*>(owner_mask), total, worker, static_cast<TT*>(out))
+  // 16-B vectors when theta / out are 16-B aligned and the mask words of a
+  // vector are aligned to their packed size
+  const int esz = dtype == SDP_DTYPE_F64 ? 8 : 4;
+  const uintptr_t mal = static_cast<uintptr_t>(mask_bytes) * (16 / esz);
+  const bool vec = ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(out)) % 16) == 0 &&
+                   reinterpret_cast<uintptr_t>(owner_mask) % (mal < 8 ? mal : 8) == 0;
+#define SDP_EXTRACT(TT, MB)                                                                        \
+  do {                                                                                             \
+    if (vec)                                                                                       \
+      k_masked_extract<TT, MB, true><<<grid, kSliceThreads, 0, s>>>(static_cast<const TT*>(theta), \
+          static_cast<const MaskT<MB>::T*>(owner_mask), total, worker, static_cast<TT*>(out));     \
+    else                                                                                           \
+      k_masked_extract<TT, MB, false><<<grid, kSliceThreads, 0, s>>>(static_cast<const TT*>(theta),\
+          static_cast<const MaskT<MB>::T*>(owner_mask), total, worker, static_cast<TT*>(out));     \
+  } while (0)
 #define SDP_EXTRACT_T(TT)                  \
   switch (mask_bytes) {                    \
     case 1: SDP_EXTRACT(TT, 1); break;     \
