@@ -901,11 +901,14 @@ def run_memory_child(args):
     res = {}
     steps = max(2, args.train_steps // 2)
     for wl in ("gpt2", "resnet18"):
-        for tag, p in (("subnet", args.p), ("dp", world)):
+        runs = (("subnet", args.p, "block"), ("dp", world, "block"))
+        if wl == "resnet18":  # configs[2]: width-wise compact subnetworks, owned-tile storage too
+            runs += (("widthwise", args.p, "neuron"),)
+        for tag, p, strategy in runs:
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
             model = train.build_gpt2(dev) if wl == "gpt2" else train.build_resnet18(dev)
-            a = masking.build_assignment(model.topology, "block", world, p, seed=1)
+            a = masking.build_assignment(model.topology, strategy, world, p, seed=1)
             kw = {"loss_fn": train.lm_loss, "lr": 1e-4} if wl == "gpt2" else {"lr": 0.02}
             tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, graphed=False,
                                    timeout_cycles=60_000_000_000, **kw)
@@ -973,10 +976,11 @@ def run_memory_ranks(args, world: int = 8) -> dict:
                     "state_bytes_max": max(rk[key]["state_bytes"] for rk in ranks),
                     "loss_per_step_rank_mean": [float(np.mean([rk[key]["losses"][i] for rk in ranks]))
                                                 for i in range(len(ranks[0][key]["losses"]))]}
-    for wl in ("gpt2", "resnet18"):
-        sub, dp = out[f"{wl}_subnet"], out[f"{wl}_dp"]
-        out[f"{wl}_mem_reduction_vs_dp"] = 1 - sub["peak_bytes_max"] / dp["peak_bytes_max"]
-        out[f"{wl}_mem_reduction_vs_dp_mean"] = 1 - sub["peak_bytes_mean"] / dp["peak_bytes_mean"]
+    for wl, tag in (("gpt2", "subnet"), ("resnet18", "subnet"), ("resnet18", "widthwise")):
+        sub, dp = out[f"{wl}_{tag}"], out[f"{wl}_dp"]
+        name = wl if tag == "subnet" else f"{wl}_{tag}"
+        out[f"{name}_mem_reduction_vs_dp"] = 1 - sub["peak_bytes_max"] / dp["peak_bytes_max"]
+        out[f"{name}_mem_reduction_vs_dp_mean"] = 1 - sub["peak_bytes_mean"] / dp["peak_bytes_mean"]
     return out
 
 

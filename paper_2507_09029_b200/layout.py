@@ -178,7 +178,12 @@ class WorkerTransfer:
     space.  Entries of blocks w does not own are never touched (and never read
     by the sync kernel)."""
 
-    def __init__(self, layout: SyncLayout, sub):
+    def __init__(self, layout: SyncLayout, sub, compact=None):
+        """compact: a storage.CompactLayout of the sync-space plan -- the
+        worker's sync-space buffers (theta, bf16 copy, gradient replica) then
+        hold only the tiles it owns, and every sync block is addressed at its
+        slot-mapped offset (a block the worker owns spans stored tiles only,
+        in consecutive slots)."""
         a = layout.assignment
         w = sub.worker
         topo = a.topology
@@ -198,6 +203,13 @@ class WorkerTransfer:
                 cpos = np.searchsorted(live_c, cidx).astype(np.int32)
                 # "full" = the worker's compact tensor [crows, ccols, inner] (same memory
                 # order as SubnetLayout's), "compact" = the contiguous sync block
+                size = len(ridx) * len(cidx) * inner
+                if compact is not None and size:
+                    c0 = compact.compact_offset(w, off)
+                    if compact.compact_offset(w, off + size - 1) != c0 + size - 1:
+                        raise ConfigError(f"{p.name}: sync block at {off} is not contiguous in worker {w}'s "
+                                          "owned-tile storage")
+                    off = c0
                 builder.add(sub.offsets[p.name], off, crows, ccols, inner,
                             None if len(rpos) == crows else rpos, None if len(cpos) == ccols else cpos)
         self.d_desc, self.d_tasks, self.n_tasks, self.maps = builder.upload(a.device)

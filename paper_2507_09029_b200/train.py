@@ -1031,10 +1031,7 @@ class PeerTrainer(_GradStore):
         self.device = torch.device(device)
         self.compact = assignment.strategy == "neuron"
         if compact_storage is None:
-            compact_storage = not self.compact
-        if compact_storage and self.compact:
-            raise UsageError("compact owned-tile storage covers block assignments; width-wise workers "
-                             "keep window-class-major replicas")
+            compact_storage = True
         self.compact_storage = bool(compact_storage)
         self.slayout = None
         theta0 = model.theta.to(self.device)
@@ -1051,7 +1048,10 @@ class PeerTrainer(_GradStore):
         self.views = {w: assignment.worker_view(w) for w in self.local}
         if self.compact:
             self.subs = {w: SubnetLayout(assignment, w) for w in self.local}
-            self.transfers = {w: WorkerTransfer(self.slayout, self.subs[w]) for w in self.local}
+            # compact storage: the sync-space buffers hold only the worker's
+            # owned tiles and the transfers address them through the slot table
+            cl = self.group.compact if self.compact_storage else None
+            self.transfers = {w: WorkerTransfer(self.slayout, self.subs[w], compact=cl) for w in self.local}
         if self.compact_storage:
             lay = self.group.compact
             self.theta = {w: lay.gather(w, theta0) for w in self.local}
@@ -1070,7 +1070,8 @@ class PeerTrainer(_GradStore):
         if self.compact_storage:
             from .storage import worker_states
             topo = model.topology
-            self._specs = {w: [topo.index[k] for k in self._live[w]] for w in self.local}
+            if not self.compact:
+                self._specs = {w: [topo.index[k] for k in self._live[w]] for w in self.local}
             self._states = worker_states([(self.theta[w], self.velocity[w], None, self.theta_bf16[w],
                                            self.grads[w]) for w in self.local], self.device)
             self._updates, per_cta = lay.update_table(self.local, self.group.plan.leader_cta(), self.group.grid)
@@ -1117,15 +1118,21 @@ class PeerTrainer(_GradStore):
         self._graph_lr = self.lr
 
     def _step_compact_storage(self, batches: dict, cache: bool) -> torch.Tensor:
-        """Block workers on owned-tile storage: the live parameters are views
-        of the worker's compact bf16 copy (one contiguous range each), their
-        gradients go straight into the worker's compact fp32 replica, and ONE
-        sync launch per rank averages, applies Nesterov to every local owner's
-        compact theta / velocity and writes its bf16 copy."""
+        """Workers on owned-tile storage.  Block workers: the live parameters
+        are views of the worker's compact bf16 copy (one contiguous range
+        each) and their gradients go straight into the worker's compact fp32
+        replica.  Width-wise workers: their compact subnetwork is extracted
+        from / written back into the owned-tile buffers by the slot-mapped
+        sync-layout transfers.  Then ONE sync launch per rank averages,
+        applies Nesterov to every local owner's compact theta / velocity and
+        writes its bf16 copy."""
         lay = self.group.compact
         losses = []
         for w in self.local:
             x, y = batches[w]
+            if self.compact:
+                losses.append(self._widthwise_step(w, x, y, cache))
+                continue
             src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
             params = {}
             for k, v in lay.views(w, src, self._specs[w]).items():
@@ -1161,6 +1168,18 @@ class PeerTrainer(_GradStore):
         return sum(t.numel() * t.element_size() for w in self.local
                    for t in (self.theta[w], self.velocity[w], self.theta_bf16[w], self.grads[w]))
 
+    def _widthwise_step(self, w: int, x, y, cache: bool) -> torch.Tensor:
+        """One width-wise worker's fwd/bwd: compact subnetwork out of the
+        worker's sync-space copy, its gradient into the worker's replica."""
+        if self.autocast:
+            return self._compact_step_bf16(w, x, y, cache, src=self.theta_bf16[w])
+        sub = self.subs[w]
+        leaf = self.transfers[w].to_compact(self.theta[w]).requires_grad_(True)
+        loss = self.loss_fn(self.model.arch.forward_compact(sub.views(leaf), x, sub), y)
+        (g,) = torch.autograd.grad(loss, leaf)
+        self.transfers[w].from_compact(g.float(), self.group.replicas[w])
+        return loss.detach()
+
     def _step_eager(self, batches: dict, cache: bool = True) -> torch.Tensor:
         if self.compact_storage:
             return self._step_compact_storage(batches, cache)
@@ -1168,29 +1187,20 @@ class PeerTrainer(_GradStore):
         losses = []
         for w in self.local:
             x, y = batches[w]
-            if self.compact and self.autocast:
-                losses.append(self._compact_step_bf16(w, x, y, cache, src=self.theta_bf16[w]))
-                continue
             if self.compact:
-                sub = self.subs[w]
-                src = self.theta_bf16[w] if self.autocast else self.theta[w]
-                leaf = self.transfers[w].to_compact(src).requires_grad_(True)
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
-                    loss = self.loss_fn(self.model.arch.forward_compact(sub.views(leaf), x, sub), y)
-                (g,) = torch.autograd.grad(loss, leaf)
-                self.transfers[w].from_compact(g.float(), self.group.replicas[w])
-            else:
-                src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
-                params = {}
-                for k, v in param_views(topo, src).items():
-                    if self.autocast and v.dim() == 4:  # channels-last conv weights (cuDNN NHWC)
-                        v = v.contiguous(memory_format=torch.channels_last)
-                    params[k] = v.requires_grad_(True)
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
-                    loss = self.loss_fn(self.model.arch.forward(params, x, self.views[w]), y)
-                names = self._live[w]
-                gs = torch.autograd.grad(loss, [params[k] for k in names])
-                self._store_grads(w, names, gs)
+                losses.append(self._widthwise_step(w, x, y, cache))
+                continue
+            src = (self.theta_bf16[w] if self.autocast else self.theta[w]).detach()
+            params = {}
+            for k, v in param_views(topo, src).items():
+                if self.autocast and v.dim() == 4:  # channels-last conv weights (cuDNN NHWC)
+                    v = v.contiguous(memory_format=torch.channels_last)
+                params[k] = v.requires_grad_(True)
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.autocast, cache_enabled=cache):
+                loss = self.loss_fn(self.model.arch.forward(params, x, self.views[w]), y)
+            names = self._live[w]
+            gs = torch.autograd.grad(loss, [params[k] for k in names])
+            self._store_grads(w, names, gs)
             losses.append(loss.detach())
         self.group.launch()  # peer-mapped owner sync: replicas[w] <- mean on w's elements
         for w in self.local:  # width-wise: replicas in the sync layout, update per worker
@@ -1202,10 +1212,11 @@ class PeerTrainer(_GradStore):
     def theta_of(self, w: int) -> torch.Tensor:
         """Worker w's parameter copy in the reference's flat layout (compact
         storage: elements of tiles w does not store read 0)."""
+        flat = self.theta[w]
         if self.compact_storage:
             d = self.model.topology.total
-            return self.group.compact.scatter(w, self.theta[w], torch.zeros(d, device=self.device))
-        return self.slayout.from_sync(self.theta[w]) if self.slayout else self.theta[w]
+            flat = self.group.compact.scatter(w, self.theta[w], torch.zeros(d, device=self.device))
+        return self.slayout.from_sync(flat) if self.slayout else flat
 
     def close(self) -> None:
         self.group.close()

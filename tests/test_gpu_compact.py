@@ -115,11 +115,15 @@ def test_local_update_phase_is_reference_nesterov(cuda, name, strategy, n, p):
     assert int(status.item()) & 0x2
 
 
-@pytest.mark.parametrize("arch", ["resnet18", "mini"])
-def test_peer_trainer_compact_storage_matches_coresident(cuda, arch):
+@pytest.mark.parametrize("arch,strategy,autocast", [("resnet18", "block", False), ("mini", "block", False),
+                                                    ("resnet18", "neuron", False), ("mini", "neuron", False),
+                                                    ("resnet18", "neuron", True), ("resnet18", "block", True)])
+def test_peer_trainer_compact_storage_matches_coresident(cuda, arch, strategy, autocast):
     """PeerTrainer at world 1 (every worker local, owned-tile storage, one
     sync+Nesterov launch per step) == SubnetTrainer's canonical theta on every
-    worker's owned elements, bit for bit (fp32, deterministic cuDNN)."""
+    worker's owned elements, bit for bit (deterministic cuDNN; fp32 and bf16
+    autocast), for block workers and for width-wise workers (sync-layout
+    blocks addressed through the slot table)."""
     from paper_2507_09029_b200 import masking, models, train
     prev = torch.backends.cudnn.deterministic
     torch.backends.cudnn.deterministic = True
@@ -134,13 +138,13 @@ def test_peer_trainer_compact_storage_matches_coresident(cuda, arch):
         steps = [[(torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
                    torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(n)] for _ in range(3)]
         m1 = model()
-        a = masking.build_assignment(m1.topology, "block", n, p, seed=1)
-        ref = train.SubnetTrainer(m1, a, lr=0.05, autocast=False)
+        a = masking.build_assignment(m1.topology, strategy, n, p, seed=1)
+        ref = train.SubnetTrainer(m1, a, lr=0.05, autocast=autocast, sync_layout=strategy == "neuron")
         for b in steps:
             ref.step(b)
         canon = ref.theta().cpu().numpy()
         m2 = model()
-        tr = train.PeerTrainer(m2, a, 0, 1, cuda, lambda o: [o], lr=0.05, autocast=False)
+        tr = train.PeerTrainer(m2, a, 0, 1, cuda, lambda o: [o], lr=0.05, autocast=autocast)
         assert tr.compact_storage
         for b in steps:
             tr.step({w: b[w] for w in range(n)})
