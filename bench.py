@@ -552,11 +552,14 @@ def run_equal_loss(args, dev, memory: dict | None) -> dict:
     from equal_loss import equal_loss
     out = equal_loss(dev, steps=args.equal_loss_steps)
     if memory and "resnet18_subnet" in memory and "resnet18_dp" in memory:
-        sub, dp = memory["resnet18_subnet"], memory["resnet18_dp"]
-        out["peak_memory_vs_dp"] = {
-            "subnet_largest_rank": sub["peak_bytes_max"] / dp["peak_bytes_max"] - 1.0,
-            "subnet_mean_rank": sub["peak_bytes_mean"] / dp["peak_bytes_mean"] - 1.0,
-            "source": "train.memory_n8_ranks (ResNet-18 C2, 8 PeerTrainer rank processes, compact storage)"}
+        dp = memory["resnet18_dp"]
+        out["peak_memory_vs_dp"] = {"source": "train.memory_n8_ranks (ResNet-18, 8 PeerTrainer rank processes, "
+                                              "owned-tile storage)"}
+        for tag in ("subnet", "widthwise"):
+            if f"resnet18_{tag}" in memory:
+                m = memory[f"resnet18_{tag}"]
+                out["peak_memory_vs_dp"][f"{tag}_largest_rank"] = m["peak_bytes_max"] / dp["peak_bytes_max"] - 1.0
+                out["peak_memory_vs_dp"][f"{tag}_mean_rank"] = m["peak_bytes_mean"] / dp["peak_bytes_mean"] - 1.0
     return out
 
 
