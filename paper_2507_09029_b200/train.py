@@ -994,17 +994,21 @@ class PeerTrainer(_GradStore):
     A step is: every local worker's forward/backward writes its fp32 gradient
     into its peer-mapped replica; ONE owner-sync launch per rank (the leader
     of each tile reads every owner's gradient -- local or over NVLink -- in
-    ascending worker order and writes the mean into every owner's replica);
-    then each local worker applies SGD-Nesterov to its copy with the bf16
-    cast fused (sdp_nesterov_update).  Remote traffic is 4 B per remote owner
-    per element; updating remote theta / velocity copies from the leader
-    instead would cost 10 B.  Every owner applies the same update to the same
-    mean, so the owners' copies of an owned parameter stay bit-identical to
-    the co-resident trainer's canonical theta (engine.py:222-223).
+    ascending worker order and writes the mean into every owner's replica)
+    whose last phase applies SGD-Nesterov + the bf16 cast to every local
+    worker's own copy (SDP_SYNC_LOCAL_UPDATE; without owned-tile storage, a
+    separate sdp_nesterov_update per worker).  Remote traffic is 4 B per
+    remote owner per element; updating remote theta / velocity copies from
+    the leader instead would cost 10 B.  Every owner applies the same update
+    to the same mean, so the owners' copies of an owned parameter stay
+    bit-identical to the co-resident trainer's canonical theta
+    (engine.py:222-223).
 
     Width-wise (neuron) assignments keep replicas and parameter copies in the
     window-class-major sync layout (layout.SyncLayout) and train compact
-    subnetworks through layout.WorkerTransfer, like SubnetTrainer."""
+    subnetworks through layout.WorkerTransfer, like SubnetTrainer; on
+    owned-tile storage the transfers address the worker's blocks through the
+    slot table."""
 
     def __init__(self, model: GlobalModel, assignment, rank: int, world: int, device, all_gather,
                  lr: float = 0.1, momentum: float = 0.9, autocast: bool = True, loss_fn=None,
@@ -1016,9 +1020,9 @@ class PeerTrainer(_GradStore):
         epochs on the device (comm.PeerGroup.epochs), so replays stay in step
         as long as every rank calls step() the same number of times.
 
-        compact_storage (default: on for block assignments): each local
-        worker keeps theta, velocity, the bf16 copy and its gradient replica
-        ONLY for the tiles it owns (storage.CompactLayout; dropped blocks have
+        compact_storage (default: on): each local worker keeps theta,
+        velocity, the bf16 copy and its gradient replica ONLY for the tiles it
+        owns (storage.CompactLayout; dropped blocks / unowned sync blocks have
         no storage), and the step's optimizer runs inside the sync launch as
         its local-update phase (SDP_SYNC_LOCAL_UPDATE): one libsdp launch per
         rank per step for sync + Nesterov + bf16 cast."""
