@@ -938,10 +938,73 @@ def run_memory_child(args):
             tr.close()
             del tr, model, a, batches
             dist.barrier()
+        res[f"{wl}_torch_ddp"] = torch_ddp_memory(wl, dev, rank, steps)
+        dist.barrier()
     allr = all_gather(res)
     if rank == 0:
         print("MEMORY_RANKS " + json.dumps(allr), flush=True)
     dist.destroy_process_group()
+
+
+def torch_ddp_memory(wl: str, dev, rank: int, steps: int) -> dict:
+    """The stock comparator the north star names: torch DistributedDataParallel
+    over the same model (one flat fp32 nn.Parameter holding every weight, cast
+    to bf16 once per forward, the same forward kernels), bf16 autocast,
+    torch.optim.SGD(momentum 0.9, nesterov), DDP's default 25 MB gradient
+    buckets, on this rank's batch.
+    Peak = torch.cuda.max_memory_allocated over the training steps."""
+    import torch
+    from torch.nn.parallel import DistributedDataParallel
+
+    from paper_2507_09029_b200 import train
+
+    class Flat(torch.nn.Module):
+        def __init__(self, m):
+            super().__init__()
+            self.arch, self.topo = m.arch, m.topology
+            self.theta = torch.nn.Parameter(m.theta.detach().clone())
+
+        def forward(self, x):
+            # AMP's weight cast, once for the whole flat vector (as the
+            # trainers' bf16 copy): bf16 activations on the same kernels
+            params = train.param_views(self.topo, self.theta.to(torch.bfloat16))
+            if wl == "gpt2":
+                params["__wte_padded"] = train._LinearCrossEntropy._padded(params["wte"].detach(), torch.bfloat16)
+            return self.arch.forward(params, x)
+
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    m = train.build_gpt2(dev) if wl == "gpt2" else train.build_resnet18(dev)
+    net = Flat(m)
+    m.theta = None
+    ddp = DistributedDataParallel(net, device_ids=[dev.index])
+    opt = torch.optim.SGD(ddp.parameters(), lr=1e-4 if wl == "gpt2" else 0.02, momentum=0.9, nesterov=True)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(rank)
+    if wl == "gpt2":
+        x = torch.randint(0, 50257, (8, 1024), generator=gen, device=dev)
+        y = x
+        loss_fn = train.lm_loss
+    else:
+        x = torch.randn(64, 3, 32, 32, generator=gen, device=dev)
+        y = torch.randint(0, 10, (64,), generator=gen, device=dev)
+        loss_fn = lambda out, t: torch.nn.functional.cross_entropy(out.float(), t)  # noqa: E731
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    losses = []
+    for _ in range(steps):
+        opt.zero_grad(set_to_none=False)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = loss_fn(ddp(x), y)
+        loss.backward()
+        opt.step()
+        losses.append(float(loss.item()))
+    torch.cuda.synchronize()
+    out = {"peak_bytes": int(torch.cuda.max_memory_allocated(dev)),
+           "state_bytes": int(3 * net.theta.numel() * 4), "stored_params": int(net.theta.numel()),
+           "losses": losses}
+    del ddp, net, opt, m
+    return out
 
 
 def run_memory_ranks(args, world: int = 8) -> dict:
@@ -984,6 +1047,10 @@ def run_memory_ranks(args, world: int = 8) -> dict:
         name = wl if tag == "subnet" else f"{wl}_{tag}"
         out[f"{name}_mem_reduction_vs_dp"] = 1 - sub["peak_bytes_max"] / dp["peak_bytes_max"]
         out[f"{name}_mem_reduction_vs_dp_mean"] = 1 - sub["peak_bytes_mean"] / dp["peak_bytes_mean"]
+        ddp = out.get(f"{wl}_torch_ddp")
+        if ddp:
+            out[f"{name}_mem_reduction_vs_torch_ddp"] = 1 - sub["peak_bytes_max"] / ddp["peak_bytes_max"]
+            out[f"{name}_mem_reduction_vs_torch_ddp_mean"] = 1 - sub["peak_bytes_mean"] / ddp["peak_bytes_mean"]
     return out
 
 
