@@ -275,6 +275,15 @@ int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity,
                         const void* grad, double lr, double momentum,
                         void* theta_bf16, uint32_t* status, void* stream);
 
+/* Standalone optim.Adam.update (optim.py:101-109) on a flat vector, after the
+ * caller's step counter was incremented to `step` (>= 1):
+ *   m = b1 m + (1-b1) g;  v = b2 v + ((1-b2) g) g;
+ *   th -= (lr (m / (1 - b1^step))) / (sqrt(v / (1 - b2^step)) + eps)
+ * in numpy's evaluation order (f64: bit-identical); theta_bf16 optional. */
+int sdp_adam_update(int dtype, int64_t total, void* theta, void* m, void* v, const void* grad,
+                    double lr, double beta1, double beta2, double eps, int step,
+                    void* theta_bf16, void* stream);
+
 /* Finite check that runs BEFORE an optimizer update (optim.py:78-80 raises
  * NumericalError before touching theta): ORs SDP_STATUS_NONFINITE into
  * *status if any of x[0..total) is Inf or NaN. */

@@ -152,6 +152,7 @@ SIGNATURES = {
     "sdp_plan_tiles": (C.c_int, [VP, I32, I64, I32, VP, VP, VP]),
     "sdp_owner_sync": (C.c_int, [C.POINTER(SyncArgs), VP]),
     "sdp_nesterov_update": (C.c_int, [I32, I64, VP, VP, VP, DBL, DBL, VP, VP, VP]),
+    "sdp_adam_update": (C.c_int, [I32, I64, VP, VP, VP, VP, DBL, DBL, DBL, DBL, I32, VP, VP]),
     "sdp_check_finite": (C.c_int, [I32, I64, VP, VP, VP]),
     "sdp_masked_extract": (C.c_int, [I32, VP, VP, I32, I64, I32, VP, VP]),
     "sdp_gather_slices": (C.c_int, [I32, VP, VP, I32, VP, VP, VP, I32, VP]),

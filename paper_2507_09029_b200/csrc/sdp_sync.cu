@@ -17,6 +17,8 @@
 // runs only the tiles it leads, bracketed by release/acquire flag barriers.
 #include "sdp_common.cuh"
 
+#include <cmath>
+
 namespace sdp {
 
 constexpr int kSyncThreads = 256;
@@ -565,6 +567,31 @@ __global__ void k_nesterov(int64_t total, T* __restrict__ theta, T* __restrict__
     atomicOr(status, SDP_STATUS_NONFINITE);
 }
 
+// optim.Adam.update (optim.py:101-109) on a flat vector, numpy's evaluation
+// order and rounding (no FMA contraction):
+//   m = b1*m + (1-b1)*g;  v = b2*v + ((1-b2)*g)*g;
+//   th = th - (lr*(m/c1)) / (sqrt(v/c2) + eps),   c_k = 1 - b_k**t (host)
+template <typename T>
+__global__ void k_adam(int64_t total, T* __restrict__ theta, T* __restrict__ m, T* __restrict__ v,
+                       const T* __restrict__ grad, double lr, double beta1, double beta2, double eps,
+                       double bias1, double bias2, __nv_bfloat16* __restrict__ theta_bf16) {
+  const T b1 = static_cast<T>(beta1), b2 = static_cast<T>(beta2);
+  const T omb1 = static_cast<T>(1.0 - beta1), omb2 = static_cast<T>(1.0 - beta2);
+  const T c1 = static_cast<T>(bias1), c2 = static_cast<T>(bias2), lrt = static_cast<T>(lr);
+  const T ep = static_cast<T>(eps);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T g = grad[j];
+    const T mm = add_rn(mul_rn(b1, m[j]), mul_rn(omb1, g));
+    const T vv = add_rn(mul_rn(b2, v[j]), mul_rn(mul_rn(omb2, g), g));
+    const T t = sub_rn(theta[j], div_rn(mul_rn(lrt, div_rn(mm, c1)), add_rn(sqrt_rn(div_rn(vv, c2)), ep)));
+    m[j] = mm;
+    v[j] = vv;
+    theta[j] = t;
+    if (theta_bf16) theta_bf16[j] = to_bf16(t);
+  }
+}
+
 template <typename T>
 __global__ void k_check_finite(int64_t total, const T* __restrict__ x, uint32_t* status) {
   bool bad = false;
@@ -735,6 +762,31 @@ int sdp_nesterov_update(int dtype, int64_t total, void* theta, void* velocity, c
     k_nesterov<double><<<grid, 256, 0, s>>>(total, static_cast<double*>(theta), static_cast<double*>(velocity),
                                             static_cast<const double*>(grad), lr, momentum,
                                             static_cast<__nv_bfloat16*>(theta_bf16), status);
+  else
+    return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
+  SDP_LAUNCH_CHECK();
+  return SDP_OK;
+}
+
+int sdp_adam_update(int dtype, int64_t total, void* theta, void* m, void* v, const void* grad, double lr,
+                    double beta1, double beta2, double eps, int step, void* theta_bf16, void* stream) {
+  if (total <= 0) return SDP_OK;
+  if (!theta || !m || !v || !grad) return set_error(SDP_ERR_USAGE, "null buffer");
+  if (step < 1) return set_error(SDP_ERR_CONFIG, "Adam step must be >= 1 (the reference increments t first)");
+  // bias corrections as the reference computes them: 1 - beta**t in double
+  const double bias1 = 1.0 - std::pow(beta1, static_cast<double>(step));
+  const double bias2 = 1.0 - std::pow(beta2, static_cast<double>(step));
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sm_count() * 8));
+  cudaStream_t s = as_stream(stream);
+  auto* tb = static_cast<__nv_bfloat16*>(theta_bf16);
+  if (dtype == SDP_DTYPE_F32)
+    k_adam<float><<<grid, 256, 0, s>>>(total, static_cast<float*>(theta), static_cast<float*>(m),
+                                       static_cast<float*>(v), static_cast<const float*>(grad), lr, beta1, beta2,
+                                       eps, bias1, bias2, tb);
+  else if (dtype == SDP_DTYPE_F64)
+    k_adam<double><<<grid, 256, 0, s>>>(total, static_cast<double*>(theta), static_cast<double*>(m),
+                                        static_cast<double*>(v), static_cast<const double*>(grad), lr, beta1,
+                                        beta2, eps, bias1, bias2, tb);
   else
     return set_error(SDP_ERR_CONFIG, "dtype must be SDP_DTYPE_F32 or SDP_DTYPE_F64");
   SDP_LAUNCH_CHECK();

@@ -28,7 +28,7 @@ import torch
 
 from . import _native as N
 from ._device import device, ptr, sdp_dtype, stream_ptr, upload_struct
-from .errors import NumericalError, ProtocolError, UsageError
+from .errors import ConfigError, NumericalError, ProtocolError, UsageError
 from .storage import dispatch_order, leader_cta
 
 TILE = 2048              # elements per sync tile (8 KB of fp32 per replica); measured
@@ -644,29 +644,85 @@ class SgdNesterov:
     def _check(self, theta: torch.Tensor, grad: torch.Tensor, theta_bf16) -> None:
         if self.velocity is None:
             self.velocity = torch.zeros(self.dim, dtype=theta.dtype, device=theta.device)
-        for nm, t in (("theta", theta), ("velocity", self.velocity), ("grad", grad)):
-            if not torch.is_tensor(t) or t.dtype != theta.dtype or t.numel() != self.dim \
-                    or t.device != theta.device or not t.is_contiguous():
-                raise UsageError(f"SgdNesterov: {nm} must be a contiguous [{self.dim}] {theta.dtype} tensor on "
-                                 f"{theta.device} (got {getattr(t, 'dtype', type(t))}, "
-                                 f"{getattr(t, 'numel', lambda: '?')()} elements, {getattr(t, 'device', '?')})")
-        if theta.dtype not in (torch.float32, torch.float64) or theta.device.type != "cuda":
-            raise UsageError("SgdNesterov: theta must be a float32 / float64 CUDA tensor")
-        if theta_bf16 is not None and (theta_bf16.dtype != torch.bfloat16 or theta_bf16.numel() != self.dim
-                                       or theta_bf16.device != theta.device or not theta_bf16.is_contiguous()):
-            raise UsageError(f"SgdNesterov: theta_bf16 must be a contiguous [{self.dim}] bfloat16 tensor")
+        _check_update_args("SgdNesterov", self.dim, theta, grad, {"velocity": self.velocity}, theta_bf16)
 
     def update(self, theta: torch.Tensor, grad: torch.Tensor, lr: float,
                theta_bf16: torch.Tensor | None = None) -> None:
         self._check(theta, grad, theta_bf16)
-        status = torch.zeros(1, dtype=torch.int32, device=theta.device)
         s = stream_ptr(theta.device)
-        N.call("sdp_check_finite", sdp_dtype(grad.dtype), grad.numel(), ptr(grad), ptr(status), s)
-        if int(status.item()) & N.STATUS_NONFINITE:
-            raise NumericalError("aggregated gradient contains non-finite values")
+        _raise_if_nonfinite(grad, s)
         N.call("sdp_nesterov_update", sdp_dtype(theta.dtype), theta.numel(), ptr(theta),
                ptr(self.velocity), ptr(grad), float(lr), float(self.momentum), ptr(theta_bf16),
                None, s)
 
     def state_elements(self) -> int:
         return self.dim
+
+
+class Adam:
+    """optim.Adam (optim.py:90-112) over a device theta, on libsdp's k_adam:
+    numpy's evaluation order, float64 bit-identical to the reference.  Like
+    the reference a non-finite gradient raises NumericalError before the step
+    counter, the moments or theta change.  The moments take theta's dtype and
+    device on the first update unless `dtype` is given."""
+
+    kind = "adam"
+
+    def __init__(self, dim: int, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 dtype=None, device_=None):
+        self.dim = int(dim)
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.t = 0
+        self.m = self.v = None
+        if dtype is not None:
+            self.m = torch.zeros(dim, dtype=dtype, device=device(device_))
+            self.v = torch.zeros_like(self.m)
+
+    def update(self, theta: torch.Tensor, grad: torch.Tensor, lr: float,
+               theta_bf16: torch.Tensor | None = None) -> None:
+        if self.m is None:
+            self.m = torch.zeros(self.dim, dtype=theta.dtype, device=theta.device)
+            self.v = torch.zeros_like(self.m)
+        _check_update_args("Adam", self.dim, theta, grad, {"m": self.m, "v": self.v}, theta_bf16)
+        s = stream_ptr(theta.device)
+        _raise_if_nonfinite(grad, s)
+        self.t += 1
+        N.call("sdp_adam_update", sdp_dtype(theta.dtype), theta.numel(), ptr(theta), ptr(self.m), ptr(self.v),
+               ptr(grad), float(lr), float(self.beta1), float(self.beta2), float(self.eps), self.t,
+               ptr(theta_bf16), s)
+
+    def state_elements(self) -> int:
+        return 2 * self.dim
+
+
+def make_optimizer(kind: str, dim: int, momentum: float = 0.9):
+    """optim.make_optimizer (optim.py:115-120) for device thetas."""
+    if kind == "sgd-nesterov":
+        return SgdNesterov(dim, momentum=momentum)
+    if kind == "adam":
+        return Adam(dim)
+    raise ConfigError(f"unknown optimizer kind {kind!r}")
+
+
+def _check_update_args(name: str, dim: int, theta, grad, states: dict, theta_bf16) -> None:
+    """Every buffer of an optimizer update: contiguous [dim], theta's dtype and
+    device (the kernels cast every pointer to theta's element type)."""
+    for nm, t in (("theta", theta), *states.items(), ("grad", grad)):
+        if not torch.is_tensor(t) or t.dtype != theta.dtype or t.numel() != dim \
+                or t.device != theta.device or not t.is_contiguous():
+            raise UsageError(f"{name}: {nm} must be a contiguous [{dim}] {theta.dtype} tensor on "
+                             f"{theta.device} (got {getattr(t, 'dtype', type(t))}, "
+                             f"{getattr(t, 'numel', lambda: '?')()} elements, {getattr(t, 'device', '?')})")
+    if theta.dtype not in (torch.float32, torch.float64) or theta.device.type != "cuda":
+        raise UsageError(f"{name}: theta must be a float32 / float64 CUDA tensor")
+    if theta_bf16 is not None and (theta_bf16.dtype != torch.bfloat16 or theta_bf16.numel() != dim
+                                   or theta_bf16.device != theta.device or not theta_bf16.is_contiguous()):
+        raise UsageError(f"{name}: theta_bf16 must be a contiguous [{dim}] bfloat16 tensor")
+
+
+def _raise_if_nonfinite(grad: torch.Tensor, stream) -> None:
+    """optim.py:78-80 / :102-103: NumericalError before anything is updated."""
+    status = torch.zeros(1, dtype=torch.int32, device=grad.device)
+    N.call("sdp_check_finite", sdp_dtype(grad.dtype), grad.numel(), ptr(grad), ptr(status), stream)
+    if int(status.item()) & N.STATUS_NONFINITE:
+        raise NumericalError("aggregated gradient contains non-finite values")

@@ -330,6 +330,43 @@ def test_standalone_nesterov_and_nonfinite(cuda):
         opt.update(th, torch.from_numpy(g).to(cuda), 0.1)
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_standalone_adam_and_make_optimizer(cuda, dtype):
+    """engine.Adam / engine.make_optimizer: three optim.Adam.update steps
+    (optim.py:101-109) bit-identical to the restatement (f64: the reference's
+    own arithmetic); a non-finite gradient raises before t, m, v or theta move."""
+    engine, _ = _pkg()
+    from paper_2507_09029_b200.errors import ConfigError, NumericalError
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    d = 20011
+    rng = np.random.default_rng(9)
+    th0 = rng.standard_normal(d).astype(npdt)
+    opt = engine.make_optimizer("adam", d)
+    assert opt.kind == "adam" and engine.make_optimizer("sgd-nesterov", d).kind == "sgd-nesterov"
+    with pytest.raises(ConfigError):
+        engine.make_optimizer("lamb", d)
+    th = torch.from_numpy(th0.copy()).to(cuda)
+    tb = torch.empty(d, dtype=torch.bfloat16, device=cuda)
+    want, m, v = th0.copy(), np.zeros(d, npdt), np.zeros(d, npdt)
+    for t in (1, 2, 3):
+        g = rng.standard_normal(d).astype(npdt)
+        opt.update(th, torch.from_numpy(g).to(cuda), 0.01, theta_bf16=tb)
+        want, m, v = O.adam_update(want, m, v, g, 0.01, t)
+    bits = np.uint64 if dtype == torch.float64 else np.uint32
+    assert opt.t == 3
+    assert np.array_equal(th.cpu().numpy().view(bits), want.view(bits))
+    assert np.array_equal(opt.m.cpu().numpy().view(bits), m.view(bits))
+    assert np.array_equal(opt.v.cpu().numpy().view(bits), v.view(bits))
+    if dtype == torch.float32:  # (a float64 theta rounds to bf16 directly)
+        assert np.array_equal(tb.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(want))
+    g = rng.standard_normal(d).astype(npdt)
+    g[7] = np.inf
+    before = th.clone()
+    with pytest.raises(NumericalError):
+        opt.update(th, torch.from_numpy(g).to(cuda), 0.01)
+    assert opt.t == 3 and torch.equal(th, before)
+
+
 @pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (8, 3), (8, 8), (16, 5), (33, 7), (64, 20)])
 def test_mask_widths_and_partial_tiles(cuda, n, p):
     """uint8/16/32/64 owner masks; d not a multiple of the tile or of 4."""
