@@ -243,6 +243,16 @@ typedef struct {
   int32_t updates_per_cta;
   int32_t pad2_;
   const struct sdp_worker_state* states;  /* device array indexed by sdp_update_desc.state */
+  /* fused Adam, optional: device-resident step (graph replay).  When
+   * adam_step is set, the kernel reads t = *adam_step and takes the bias
+   * corrections from adam_bias_table[2 * min(t, adam_table_len - 1) + {0, 1}]
+   * (the host fills the table with 1 - beta^t exactly as the reference
+   * computes it; past the last entry both are exactly 1.0), ignoring
+   * bias1 / bias2 above. */
+  const int32_t* adam_step;
+  const double* adam_bias_table;
+  int32_t adam_table_len;
+  int32_t pad3_;
 } sdp_sync_args;
 
 /* One local worker's optimizer state, all in its compact storage layout. */

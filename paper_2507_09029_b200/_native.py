@@ -108,6 +108,8 @@ class SyncArgs(C.Structure):
         ("slots", C.c_void_p), ("slot_stride", C.c_int64),
         ("updates", C.c_void_p), ("updates_per_cta", C.c_int32), ("pad2_", C.c_int32),
         ("states", C.c_void_p),
+        ("adam_step", C.c_void_p), ("adam_bias_table", C.c_void_p), ("adam_table_len", C.c_int32),
+        ("pad3_", C.c_int32),
     ]
 
 

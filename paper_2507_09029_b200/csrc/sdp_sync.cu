@@ -110,7 +110,17 @@ struct SyncParams {
   uint32_t epoch;
   bool has_shadow;
   uint32_t* epoch_ctr;  // device-resident barrier epochs (graph replay), or null
+  const int32_t* adam_step;       // device-resident Adam step, or null (then bias1 / bias2)
+  const double* adam_bias_table;  // [2 * adam_table_len]: 1 - beta1^t, 1 - beta2^t
+  int32_t adam_table_len;
 };
+
+// Adam bias corrections: the host scalars, or the device step's table entry.
+__device__ __forceinline__ double adam_bias(const SyncParams& p, int k) {
+  if (!p.adam_step) return k == 0 ? p.bias1 : p.bias2;
+  const int t = min(max(__ldg(p.adam_step), 0), p.adam_table_len - 1);
+  return __ldg(p.adam_bias_table + 2 * t + k);
+}
 
 // Pairwise per-CTA barrier: CTA b of every rank meets CTA b of every other rank.
 // Completion of a launch therefore implies every peer CTA has finished too.
@@ -152,8 +162,8 @@ __device__ __forceinline__ void optim_step(const SyncParams& p, T g, T& th, T& s
   } else {
     s1 = add_rn(mul_rn(static_cast<T>(p.beta1), s1), mul_rn(static_cast<T>(p.omb1), g));
     s2 = add_rn(mul_rn(static_cast<T>(p.beta2), s2), mul_rn(mul_rn(static_cast<T>(p.omb2), g), g));
-    const T mh = div_rn(s1, static_cast<T>(p.bias1));
-    const T vh = div_rn(s2, static_cast<T>(p.bias2));
+    const T mh = div_rn(s1, static_cast<T>(adam_bias(p, 0)));
+    const T vh = div_rn(s2, static_cast<T>(adam_bias(p, 1)));
     th = sub_rn(th, div_rn(mul_rn(lr, mh), add_rn(sqrt_rn(vh), static_cast<T>(p.eps))));
   }
 }
@@ -651,8 +661,12 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
       return set_error(SDP_ERR_USAGE, "fused Adam needs a 16-byte aligned second-moment buffer");
   }
   if (a->flags & SDP_SYNC_ADAM) {
-    if (!(a->bias1 > 0.0) || !(a->bias2 > 0.0))
+    if (a->adam_step) {
+      if (!a->adam_bias_table || a->adam_table_len < 2)
+        return set_error(SDP_ERR_USAGE, "a device Adam step needs its bias table (>= 2 entries)");
+    } else if (!(a->bias1 > 0.0) || !(a->bias2 > 0.0)) {
       return set_error(SDP_ERR_CONFIG, "Adam bias corrections must be positive (step >= 1)");
+    }
   }
   if (a->world > 1) {
     for (int r = 0; r < a->world; ++r)
@@ -684,6 +698,9 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   p.omb2 = a->one_minus_beta2;
   p.bias1 = a->bias1;
   p.bias2 = a->bias2;
+  p.adam_step = (a->flags & SDP_SYNC_ADAM) ? a->adam_step : nullptr;
+  p.adam_bias_table = a->adam_bias_table;
+  p.adam_table_len = a->adam_table_len;
   p.eps = a->eps;
   p.total = a->total;
   p.timeout_cycles = a->timeout_cycles > 0 ? a->timeout_cycles : (int64_t)20000000000ll;

@@ -366,10 +366,20 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
         a.lr = float(nesterov["lr"])
         a.momentum = float(nesterov.get("momentum", 0.9))
     if adam is not None:
-        # optim.Adam (optim.py:90-109): t is the step count after increment
+        # optim.Adam (optim.py:90-109): t is the step count after increment --
+        # a host int ("t"), or a device int32 ("step") the kernel reads at run
+        # time together with adam_bias_table(...) ("bias_table"): graph replay
         flags |= N.SYNC_ADAM
         b1, b2 = float(adam.get("beta1", 0.9)), float(adam.get("beta2", 0.999))
-        t = int(adam["t"])
+        step = adam.get("step")
+        if step is not None:
+            tab = adam["bias_table"]
+            a.adam_step = step.data_ptr()
+            a.adam_bias_table = tab.data_ptr()
+            a.adam_table_len = tab.numel() // 2
+            t = 1  # host scalars unused
+        else:
+            t = int(adam["t"])
         if flat_opt:
             a.theta = adam["theta"].data_ptr()
             a.velocity = adam["m"].data_ptr()
@@ -392,6 +402,22 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     a.status = None if status is None else status.data_ptr()
     a.flags = flags
     return a
+
+
+def adam_bias_table(beta1: float = 0.9, beta2: float = 0.999, dev=None, max_len: int = 1 << 20) -> torch.Tensor:
+    """Float64 [2 * L] device table of the Adam bias corrections
+    (1 - beta1**t, 1 - beta2**t) for t = 0 .. L-1, computed exactly as the
+    reference does (Python float pow, optim.py:107-108), up to the first t
+    where both are exactly 1.0 -- the kernel clamps larger steps to it."""
+    rows = []
+    t = 0
+    while True:
+        c1, c2 = 1 - beta1 ** t, 1 - beta2 ** t
+        rows.append((c1, c2))
+        if (c1 == 1.0 and c2 == 1.0) or len(rows) >= max_len:
+            break
+        t += 1
+    return torch.tensor(rows, dtype=torch.float64, device=device(dev)).reshape(-1)
 
 
 def aggregate(grads, assignment) -> AggregatedGradient:

@@ -25,7 +25,7 @@ import torch.nn.functional as F
 from . import _native as N
 from . import engine, masking, zoo
 from ._device import ptr, stream_ptr
-from .errors import NumericalError, UsageError
+from .errors import ConfigError, NumericalError, UsageError
 from .models import _channels_last_bf16, group_norm
 from .topology import GlobalModel
 
@@ -750,6 +750,28 @@ class _GradStore:
         return self._runs[w]
 
 
+OPTIMIZERS = ("sgd-nesterov", "adam")
+
+
+def _check_optimizer(kind: str) -> str:
+    if kind not in OPTIMIZERS:
+        raise ConfigError(f"unknown optimizer kind {kind!r}")  # optim.py:120
+    return kind
+
+
+def _fused_optimizer(tr, theta, m, v, theta_bf16) -> dict:
+    """owner_sync keyword of a trainer's fused optimizer: Nesterov scalars, or
+    Adam with the trainer's device step counter and bias-correction table."""
+    if tr.optimizer == "sgd-nesterov":
+        return {"nesterov": {"theta": theta, "velocity": m, "lr": tr.lr, "momentum": tr.momentum,
+                             "theta_bf16": theta_bf16}}
+    if getattr(tr, "_bias_table", None) is None:
+        tr._bias_table = engine.adam_bias_table(tr.betas[0], tr.betas[1], tr.adam_step.device)
+    return {"adam": {"theta": theta, "m": m, "v": v, "lr": tr.lr, "beta1": tr.betas[0], "beta2": tr.betas[1],
+                     "eps": tr.eps, "theta_bf16": theta_bf16, "step": tr.adam_step,
+                     "bias_table": tr._bias_table}}
+
+
 class SubnetTrainer(_GradStore):
     """N logical workers co-resident on one GPU (the reference's in-process
     structure, engine.py:180-245) with the owner-subset sync fused into the
@@ -761,8 +783,14 @@ class SubnetTrainer(_GradStore):
 
     def __init__(self, model: GlobalModel, assignment, lr: float = 0.1, momentum: float = 0.9,
                  autocast: bool = True, compact: bool | None = None, loss_fn=None,
-                 sync_layout: bool = False, graphed: bool = False):
-        """graphed: capture the whole protocol step (N worker fwd/bwd, gather /
+                 sync_layout: bool = False, graphed: bool = False, optimizer: str = "sgd-nesterov",
+                 betas: tuple = (0.9, 0.999), eps: float = 1e-8):
+        """optimizer: the reference's kinds (optim.py:115-120), fused into the
+        sync launch -- "sgd-nesterov" (momentum) or "adam" (betas, eps; the
+        step count lives on the device with a table of the reference's bias
+        corrections, so graph replays advance it).
+
+        graphed: capture the whole protocol step (N worker fwd/bwd, gather /
         scatter, the fused sync) in one CUDA graph and replay it -- the eager
         step is host-bound (thousands of small launches), see step()."""
         self.model = model
@@ -793,7 +821,11 @@ class SubnetTrainer(_GradStore):
             self.slayout = SyncLayout(assignment)
             self.transfers = [WorkerTransfer(self.slayout, s) for s in self.subs]
             self.master = self.slayout.to_sync(model.theta)
-        self.velocity = torch.zeros(d, device=dev)
+        self.velocity = torch.zeros(d, device=dev)  # Nesterov v / Adam m
+        self.optimizer = _check_optimizer(optimizer)
+        self.betas, self.eps = (float(betas[0]), float(betas[1])), float(eps)
+        self.second = torch.zeros(d, device=dev) if optimizer == "adam" else None  # Adam v
+        self.adam_step = torch.zeros(1, dtype=torch.int32, device=dev)  # steps taken (device)
         self.theta_bf16 = self.master.to(torch.bfloat16)
         self.grads = [torch.zeros(d, device=dev) for _ in range(assignment.n_workers)]
         self.lr, self.momentum, self.autocast = lr, momentum, autocast
@@ -830,12 +862,13 @@ class SubnetTrainer(_GradStore):
 
     def _sync(self):
         if self._prep is None:
+            opt = _fused_optimizer(self, self.master, self.velocity, self.second, self.theta_bf16)
             self._prep = engine.PreparedSync(
                 self.grads, self.assignment, writeback=False, plan=self.plan, check_finite=True,
-                status=self.status,
-                nesterov={"theta": self.master, "velocity": self.velocity, "lr": self.lr,
-                          "momentum": self.momentum, "theta_bf16": self.theta_bf16})
+                status=self.status, **opt)
         self._prep.args.lr = float(self.lr)
+        if self.optimizer == "adam":
+            self.adam_step.add_(1)  # optim.py:104: t += 1 before the update
         self._prep.launch()
 
     def step(self, batches) -> torch.Tensor:
@@ -860,7 +893,8 @@ class SubnetTrainer(_GradStore):
 
     def _capture(self, batches, warmup: int = 2) -> None:
         self._static = [(x.clone(), y.clone()) for x, y in batches]
-        state = [self.master, self.velocity, self.theta_bf16]
+        state = [self.master, self.velocity, self.theta_bf16, self.adam_step] + \
+            ([self.second] if self.second is not None else [])
         saved = [t.clone() for t in state]
         side = torch.cuda.Stream(self.master.device)
         side.wait_stream(torch.cuda.current_stream())
@@ -1013,7 +1047,8 @@ class PeerTrainer(_GradStore):
     def __init__(self, model: GlobalModel, assignment, rank: int, world: int, device, all_gather,
                  lr: float = 0.1, momentum: float = 0.9, autocast: bool = True, loss_fn=None,
                  timeout_cycles: int = 20_000_000_000, graphed: bool = False,
-                 compact_storage: bool | None = None):
+                 compact_storage: bool | None = None, optimizer: str = "sgd-nesterov",
+                 betas: tuple = (0.9, 0.999), eps: float = 1e-8):
         """graphed: capture the rank's whole step (local workers' fwd/bwd, the
         peer-mapped sync, the Nesterov updates) in one CUDA graph, as
         SubnetTrainer does.  The sync kernel keeps its cross-rank barrier
@@ -1037,6 +1072,11 @@ class PeerTrainer(_GradStore):
         if compact_storage is None:
             compact_storage = True
         self.compact_storage = bool(compact_storage)
+        self.optimizer = _check_optimizer(optimizer)
+        self.betas, self.eps = (float(betas[0]), float(betas[1])), float(eps)
+        if optimizer == "adam" and not self.compact_storage:
+            raise UsageError("the fused Adam update runs in the sync's local-update phase: "
+                             "use compact_storage=True")
         self.slayout = None
         theta0 = model.theta.to(self.device)
         if self.compact:
@@ -1062,7 +1102,10 @@ class PeerTrainer(_GradStore):
         else:
             self.theta = {w: theta0.clone() for w in self.local}
         del theta0
-        self.velocity = {w: torch.zeros_like(self.theta[w]) for w in self.local}
+        self.velocity = {w: torch.zeros_like(self.theta[w]) for w in self.local}  # Nesterov v / Adam m
+        self.second = ({w: torch.zeros_like(self.theta[w]) for w in self.local}
+                       if optimizer == "adam" else None)  # Adam v
+        self.adam_step = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.theta_bf16 = {w: self.theta[w].to(torch.bfloat16) for w in self.local}
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         # the gradient replicas are the peer-mapped ones; parameters of a
@@ -1076,11 +1119,22 @@ class PeerTrainer(_GradStore):
             topo = model.topology
             if not self.compact:
                 self._specs = {w: [topo.index[k] for k in self._live[w]] for w in self.local}
-            self._states = worker_states([(self.theta[w], self.velocity[w], None, self.theta_bf16[w],
-                                           self.grads[w]) for w in self.local], self.device)
+            self._states = worker_states([(self.theta[w], self.velocity[w],
+                                           None if self.second is None else self.second[w],
+                                           self.theta_bf16[w], self.grads[w]) for w in self.local], self.device)
             self._updates, per_cta = lay.update_table(self.local, self.group.plan.leader_cta(), self.group.grid)
             a = self.group.args
-            a.flags |= N.SYNC_NESTEROV | N.SYNC_LOCAL_UPDATE | N.SYNC_CHECK_FINITE
+            if optimizer == "adam":
+                self._bias_table = engine.adam_bias_table(self.betas[0], self.betas[1], self.device)
+                a.flags |= N.SYNC_ADAM | N.SYNC_LOCAL_UPDATE | N.SYNC_CHECK_FINITE
+                a.beta1, a.beta2 = self.betas
+                a.one_minus_beta1, a.one_minus_beta2 = 1 - self.betas[0], 1 - self.betas[1]
+                a.eps = self.eps
+                a.adam_step = self.adam_step.data_ptr()
+                a.adam_bias_table = self._bias_table.data_ptr()
+                a.adam_table_len = self._bias_table.numel() // 2
+            else:
+                a.flags |= N.SYNC_NESTEROV | N.SYNC_LOCAL_UPDATE | N.SYNC_CHECK_FINITE
             a.momentum = float(momentum)
             a.updates = self._updates.data_ptr()
             a.updates_per_cta = per_cta
@@ -1106,6 +1160,7 @@ class PeerTrainer(_GradStore):
         every rank does the same number), rolled back, then one captured step."""
         self._static = {w: (x.clone(), y.clone()) for w, (x, y) in batches.items()}
         state = [t for w in self.local for t in (self.theta[w], self.velocity[w], self.theta_bf16[w])]
+        state += [self.adam_step] + ([self.second[w] for w in self.local] if self.second is not None else [])
         saved = [t.clone() for t in state]
         side = torch.cuda.Stream(self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
@@ -1153,7 +1208,9 @@ class PeerTrainer(_GradStore):
             torch._foreach_copy_([slots[k] for k in names], list(gs))
             losses.append(loss.detach())
         self.group.args.lr = float(self.lr)
-        self.group.launch()  # sync + local Nesterov + bf16 cast, one launch
+        if self.optimizer == "adam":
+            self.adam_step.add_(1)  # optim.py:104: t += 1 before the update
+        self.group.launch()  # sync + local Nesterov / Adam + bf16 cast, one launch
         return torch.stack(losses).mean()
 
     def check(self) -> None:
@@ -1167,10 +1224,12 @@ class PeerTrainer(_GradStore):
             raise NumericalError("training aborted: the aggregated gradient contains non-finite values")
 
     def state_bytes(self) -> int:
-        """Bytes of this rank's per-worker training state (theta, velocity,
+        """Bytes of this rank's per-worker training state (theta, moments,
         bf16 copy, gradient replica)."""
+        extra = list(self.second.values()) if self.second is not None else []
         return sum(t.numel() * t.element_size() for w in self.local
-                   for t in (self.theta[w], self.velocity[w], self.theta_bf16[w], self.grads[w]))
+                   for t in (self.theta[w], self.velocity[w], self.theta_bf16[w], self.grads[w])) + \
+            sum(t.numel() * t.element_size() for t in extra)
 
     def _widthwise_step(self, w: int, x, y, cache: bool) -> torch.Tensor:
         """One width-wise worker's fwd/bwd: compact subnetwork out of the

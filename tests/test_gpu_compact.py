@@ -115,10 +115,12 @@ def test_local_update_phase_is_reference_nesterov(cuda, name, strategy, n, p):
     assert int(status.item()) & 0x2
 
 
-@pytest.mark.parametrize("arch,strategy,autocast", [("resnet18", "block", False), ("mini", "block", False),
-                                                    ("resnet18", "neuron", False), ("mini", "neuron", False),
-                                                    ("resnet18", "neuron", True), ("resnet18", "block", True)])
-def test_peer_trainer_compact_storage_matches_coresident(cuda, arch, strategy, autocast):
+@pytest.mark.parametrize("arch,strategy,autocast,opt", [
+    ("resnet18", "block", False, "sgd-nesterov"), ("mini", "block", False, "sgd-nesterov"),
+    ("resnet18", "neuron", False, "sgd-nesterov"), ("mini", "neuron", False, "sgd-nesterov"),
+    ("resnet18", "neuron", True, "sgd-nesterov"), ("resnet18", "block", True, "sgd-nesterov"),
+    ("resnet18", "block", False, "adam"), ("resnet18", "neuron", True, "adam")])
+def test_peer_trainer_compact_storage_matches_coresident(cuda, arch, strategy, autocast, opt):
     """PeerTrainer at world 1 (every worker local, owned-tile storage, one
     sync+Nesterov launch per step) == SubnetTrainer's canonical theta on every
     worker's owned elements, bit for bit (deterministic cuDNN; fp32 and bf16
@@ -139,12 +141,13 @@ def test_peer_trainer_compact_storage_matches_coresident(cuda, arch, strategy, a
                    torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(n)] for _ in range(3)]
         m1 = model()
         a = masking.build_assignment(m1.topology, strategy, n, p, seed=1)
-        ref = train.SubnetTrainer(m1, a, lr=0.05, autocast=autocast, sync_layout=strategy == "neuron")
+        lr = 0.05 if opt == "sgd-nesterov" else 0.002
+        ref = train.SubnetTrainer(m1, a, lr=lr, autocast=autocast, sync_layout=strategy == "neuron", optimizer=opt)
         for b in steps:
             ref.step(b)
         canon = ref.theta().cpu().numpy()
         m2 = model()
-        tr = train.PeerTrainer(m2, a, 0, 1, cuda, lambda o: [o], lr=0.05, autocast=autocast)
+        tr = train.PeerTrainer(m2, a, 0, 1, cuda, lambda o: [o], lr=lr, autocast=autocast, optimizer=opt)
         assert tr.compact_storage
         for b in steps:
             tr.step({w: b[w] for w in range(n)})

@@ -314,6 +314,40 @@ def test_fused_adam_matches_reference_steps(cuda, dtype):
             assert np.array_equal(thb.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(t0))
 
 
+def test_fused_adam_device_step_equals_host_step(cuda):
+    """The graph-replayable form of the fused Adam (a device int32 step and
+    engine.adam_bias_table) == the host-t form, which the golden test pins to
+    the reference's optim.Adam; the table holds 1 - beta**t exactly as
+    optim.py:107-108 computes it and ends where both corrections are 1.0."""
+    engine, _ = _pkg()
+    tab = engine.adam_bias_table(0.9, 0.999, cuda).cpu().numpy().reshape(-1, 2)
+    for t in (1, 2, 17, 300, len(tab) - 1):
+        assert tab[t, 0] == 1 - 0.9 ** t and tab[t, 1] == 1 - 0.999 ** t
+    assert tab[-1, 0] == 1.0 and tab[-1, 1] == 1.0 and tab[-2, 1] != 1.0
+    case = G.cases(with_grads=True)[1]
+    a = _build(case)
+    masks = G.case_masks(case)
+    grads, _, _ = G.case_inputs(case, masks)
+    th0 = torch.from_numpy(G.arrays()[f"c{case['id']}_theta1"]).to(cuda)
+    outs = []
+    for mode in ("host", "device"):
+        th, m, v = th0.clone(), torch.zeros_like(th0), torch.zeros_like(th0)
+        step = torch.zeros(1, dtype=torch.int32, device=cuda)
+        dtab = engine.adam_bias_table(0.9, 0.999, cuda)
+        for t in (1, 2, 3):
+            reps = [torch.from_numpy(g * (0.5 ** t)).to(cuda) for g in grads]
+            opt = {"theta": th, "m": m, "v": v, "lr": 0.01}
+            if mode == "host":
+                opt["t"] = t
+            else:
+                step.add_(1)
+                opt.update(step=step, bias_table=dtab)
+            engine.owner_sync(reps, a, writeback=False, adam=opt)
+        outs.append((th, m, v))
+    for x, y in zip(*outs):
+        assert torch.equal(x, y)
+
+
 def test_standalone_nesterov_and_nonfinite(cuda):
     engine, _ = _pkg()
     from paper_2507_09029_b200.errors import NumericalError

@@ -30,6 +30,47 @@ def test_resnet18_subnet_step_matches_oracle(cuda):
     assert np.array_equal(tr.theta_bf16.view(torch.int16).cpu().numpy().view(np.uint16), O.bf16_rne(th1))
 
 
+def test_resnet18_adam_steps_match_oracle_and_graph_replay(cuda):
+    """optimizer="adam" (optim.py:101-109 fused into the sync, device step
+    counter + bias table): three steps == aggregate + the Adam restatement
+    (fp32, the reference's bias corrections), and the graphed trainer
+    replays the same three steps bit for bit (the step advances inside the
+    graph)."""
+    from paper_2507_09029_b200 import masking, train
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(0)
+    steps = [[(torch.randn(4, 3, 32, 32, generator=gen, device=cuda),
+               torch.randint(0, 10, (4,), generator=gen, device=cuda)) for _ in range(8)] for _ in range(3)]
+    model = train.build_resnet18(cuda, seed=3)
+    a = masking.build_assignment(model.topology, "block", 8, 4, seed=1)
+    tr = train.SubnetTrainer(model, a, lr=0.01, autocast=False, optimizer="adam")
+    th = model.theta.cpu().numpy().copy()
+    m, v = np.zeros_like(th), np.zeros_like(th)
+    masks = a.param_masks.cpu().numpy()
+    for t, b in enumerate(steps, start=1):
+        tr.step(b)
+        gbar = O.aggregate_f32_ordered([g.cpu().numpy() for g in tr.grads], masks)
+        th, m, v = O.adam_update(th, m, v, gbar, 0.01, t)
+    tr.check()
+    assert int(tr.adam_step.item()) == 3
+    assert np.array_equal(model.theta.cpu().numpy().view(np.uint32), th.view(np.uint32))
+    assert np.array_equal(tr.second.cpu().numpy().view(np.uint32), v.view(np.uint32))
+    prev = torch.backends.cudnn.deterministic
+    torch.backends.cudnn.deterministic = True  # eager vs graphed: same conv algorithms
+    try:
+        out = []
+        for graphed in (False, True):
+            mm = train.build_resnet18(cuda, seed=3)
+            gtr = train.SubnetTrainer(mm, a, lr=0.01, autocast=False, optimizer="adam", graphed=graphed)
+            for b in steps:
+                gtr.step(b)
+            assert int(gtr.adam_step.item()) == 3
+            out.append(mm.theta)
+        assert torch.equal(out[0], out[1])
+    finally:
+        torch.backends.cudnn.deterministic = prev
+
+
 def test_resnet18_width_wise_compact_equals_masked_full(cuda):
     """C3: gather -> compact ResNet-18 fwd/bwd (ragged GN) -> scatter equals the
     reference semantics (theta*mask through the full model, active-channel GN)."""
