@@ -78,7 +78,7 @@ class _DescBuilder:
         tasks = slice_tasks(descs, compact=True)
         maps = np.concatenate(self.maps) if self.maps else np.zeros(1, np.int32)
         maps = add_col_tables(descs, maps, inverse=False)
-        self.host = (descs, tasks, maps.astype(np.int32))  # for models.SliceBatch
+        self.host = (descs, tasks, maps.astype(np.int32), True)  # for models.SliceBatch
         return (upload_struct(descs, dev), upload_struct(tasks, dev), len(tasks),
                 torch.from_numpy(maps.astype(np.int32)).to(dev))
 

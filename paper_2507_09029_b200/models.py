@@ -359,7 +359,9 @@ SLICE_DTYPE = np.dtype([("full_offset", "<i8"), ("compact_offset", "<i8"), ("row
                         ("col_tab", "<i4")])
 TASK_DTYPE = np.dtype([("desc", "<i4"), ("row_begin", "<i4"), ("row_end", "<i4"),
                        ("elem_begin", "<i4"), ("elem_end", "<i4"), ("seg", "<i4"), ("pad_", "<i4", 2)])
-TASK_ELEMS = 4096   # elements per gather/scatter task
+TASK_ELEMS = 4096   # elements per gather/scatter task (one worker per launch)
+BATCH_TASK_ELEMS = 8192  # ... with all workers in one launch (tools/task_size_probe.py: C3 scatter
+                         # 0.57 -> 0.61 of HBM, C4 gather 0.95 -> 1.03; one worker prefers 4096)
 TILE_ELEMS = 2048   # max row elements a tiled task walks (256 threads x 8)
 TILED_MIN = 256     # walked rows at least this long are tiled (sdp_slices.cu)
 
@@ -424,17 +426,22 @@ class SliceBatch:
     co-resident trainer's N gathers / scatters per step become one launch
     each, large enough to be bandwidth- rather than launch-latency-bound.
 
-    parts: [(descs, tasks, maps)] host tables (SubnetLayout.host_gather /
-    host_scatter, layout.WorkerTransfer.host) -- descriptor map offsets and
-    task descriptor indices are rebased onto the concatenation."""
+    parts: [(descs, tasks, maps, compact_rows)] host tables
+    (SubnetLayout.host_gather / host_scatter, layout.WorkerTransfer.host) --
+    descriptor map offsets and task descriptor indices are rebased onto the
+    concatenation; the tasks are re-cut at `per_task` elements (a batch
+    launch has work to spare: larger tasks amortise the per-task column
+    tables)."""
 
-    def __init__(self, parts, dev):
+    def __init__(self, parts, dev, per_task: int = BATCH_TASK_ELEMS):
         from ._device import upload_struct
         if not 1 <= len(parts) <= N.MAX_WORKERS:
             raise ConfigError(f"a slice batch holds 1..{N.MAX_WORKERS} parts, got {len(parts)}")
         ds, ts, ms = [], [], []
         nd = nm = 0
-        for k, (descs, tasks, maps) in enumerate(parts):
+        for k, (descs, tasks, maps, compact_rows) in enumerate(parts):
+            if per_task:
+                tasks = slice_tasks(descs, compact=compact_rows, per_task=per_task)
             d = descs.copy()
             for f in ("row_map", "col_map", "col_tab"):
                 d[f] = np.where(d[f] >= 0, d[f] + nm, d[f])
@@ -586,8 +593,9 @@ class SubnetLayout:
         g_tasks = slice_tasks(descs, compact=True)
         s_tasks = slice_tasks(descs, compact=False)
         # host copies: SliceBatch concatenates several workers' tables
-        self.host_gather = (descs, g_tasks, fw.astype(np.int32))
-        self.host_scatter = (descs_inv, s_tasks, iv.astype(np.int32))
+        # (descriptors, tasks, maps, whether tasks walk compact rows)
+        self.host_gather = (descs, g_tasks, fw.astype(np.int32), True)
+        self.host_scatter = (descs_inv, s_tasks, iv.astype(np.int32), False)
         self.t_gather, self.n_gather = upload_struct(g_tasks, dev), len(g_tasks)
         self.t_scatter, self.n_scatter = upload_struct(s_tasks, dev), len(s_tasks)
         self.fwd_maps = torch.from_numpy(fw.astype(np.int32)).to(dev)
