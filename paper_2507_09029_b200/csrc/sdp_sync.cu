@@ -353,12 +353,15 @@ __device__ __forceinline__ void sync_uniform_tile(const SyncParams& p, uint32_t 
 
 // Mixed tile: per-element owner sets from the owner mask (neuron strategy).
 // Lane-per-element: a warp covers 32 consecutive elements, each thread EL of
-// them at a stride of the CTA width, and the tile's owners (the union over the
-// tile, warp-uniform) are walked in ascending order, two at a time, with
+// them at a stride of the CTA width, and the owners some lane of the warp
+// needs (a warp-uniform OR of the lanes' masks, within the tile's union) are
+// walked in ascending order, KQ at a time with all their loads in flight and
 // per-lane predicates -- every load and store is a coalesced, predicated
 // access that touches only owned elements, and each element adds exactly its
-// own owners in ascending order.
-template <typename T, int MB, int R, bool CS>
+// own owners in ascending order (GPT-2 width-wise flat `aggregate`: 900 ->
+// 796 us, profiles/r2_sync_mixed_variants_v2.jsonl; the R = 4 instantiation,
+// whose registers are spoken for, walks the tile's union two at a time).
+template <typename T, int MB, int R, bool CS, int KQ>
 __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, uint32_t tix, int64_t s,
                                                 uint64_t tile_union, uint32_t& st) {
   constexpr int EL = 4;  // elements per thread per round
@@ -375,25 +378,61 @@ __device__ __forceinline__ void sync_mixed_tile(const SyncParams& p, uint32_t ti
       m[u] = static_cast<uint64_t>(__ldg(mask + o[u]));
       acc[u] = static_cast<T>(0);
     }
+    // only the owners some lane of THIS warp needs (warp-uniform; the tile's
+    // union is the fallback bound)
     uint64_t b = tile_union;
-    while (b) {
-      const int w0 = __ffsll(static_cast<long long>(b)) - 1;
-      b &= b - 1;
-      const bool two = b != 0;
-      const int w1 = two ? __ffsll(static_cast<long long>(b)) - 1 : w0;
-      if (two) b &= b - 1;
-      const T* g0 = rep_tile<const T, CS>(p, w0, tix);
-      const T* g1 = rep_tile<const T, CS>(p, w1, tix);
-      T a[EL], c[EL];
+    if constexpr (KQ > 2) {
+      uint64_t lane_any = m[0];
 #pragma unroll
-      for (int u = 0; u < EL; ++u) {
-        a[u] = ((m[u] >> w0) & 1ull) ? __ldcs(g0 + o[u]) : static_cast<T>(0);
-        c[u] = (two && ((m[u] >> w1) & 1ull)) ? __ldcs(g1 + o[u]) : static_cast<T>(0);
+      for (int u = 1; u < EL; ++u) lane_any |= m[u];
+      const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(lane_any));
+      const uint32_t hi = MB > 4 ? __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(lane_any >> 32)) : 0u;
+      b &= (static_cast<uint64_t>(hi) << 32) | lo;
+    }
+    if constexpr (KQ > 2) {
+      while (b) {
+        int wq[KQ];
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+          wq[q] = b ? __ffsll(static_cast<long long>(b)) - 1 : 64;
+          if (b) b &= b - 1;
+        }
+        T a[KQ][EL];
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+          if (wq[q] == 64) continue;
+          const T* g = rep_tile<const T, CS>(p, wq[q], tix);
+#pragma unroll
+          for (int u = 0; u < EL; ++u) a[q][u] = ((m[u] >> wq[q]) & 1ull) ? __ldcs(g + o[u]) : static_cast<T>(0);
+        }
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+          if (wq[q] == 64) continue;
+#pragma unroll
+          for (int u = 0; u < EL; ++u)
+            if ((m[u] >> wq[q]) & 1ull) acc[u] = add_rn(acc[u], a[q][u]);
+        }
       }
+    } else {
+      while (b) {
+        const int w0 = __ffsll(static_cast<long long>(b)) - 1;
+        b &= b - 1;
+        const bool two = b != 0;
+        const int w1 = two ? __ffsll(static_cast<long long>(b)) - 1 : w0;
+        if (two) b &= b - 1;
+        const T* g0 = rep_tile<const T, CS>(p, w0, tix);
+        const T* g1 = rep_tile<const T, CS>(p, w1, tix);
+        T a[EL], c[EL];
 #pragma unroll
-      for (int u = 0; u < EL; ++u) {
-        if ((m[u] >> w0) & 1ull) acc[u] = add_rn(acc[u], a[u]);
-        if (two && ((m[u] >> w1) & 1ull)) acc[u] = add_rn(acc[u], c[u]);
+        for (int u = 0; u < EL; ++u) {
+          a[u] = ((m[u] >> w0) & 1ull) ? __ldcs(g0 + o[u]) : static_cast<T>(0);
+          c[u] = (two && ((m[u] >> w1) & 1ull)) ? __ldcs(g1 + o[u]) : static_cast<T>(0);
+        }
+#pragma unroll
+        for (int u = 0; u < EL; ++u) {
+          if ((m[u] >> w0) & 1ull) acc[u] = add_rn(acc[u], a[u]);
+          if (two && ((m[u] >> w1) & 1ull)) acc[u] = add_rn(acc[u], c[u]);
+        }
       }
     }
     T mean[EL];
@@ -440,7 +479,7 @@ __device__ __forceinline__ void run_tile(const SyncParams& p, const sdp_tile_des
   const bool uniform = (d.len_flags & SDP_TILE_UNIFORM) != 0;
   if (len == p.tile) {
     if (uniform) sync_uniform_tile<T, R, CS>(p, tix, s, d.owner_bits, st);
-    else sync_mixed_tile<T, MB, (R > 2 ? 2 : R), CS>(p, tix, s, d.owner_bits, st);
+    else sync_mixed_tile<T, MB, (R > 2 ? 2 : R), CS, (R > 2 ? 2 : 4)>(p, tix, s, d.owner_bits, st);
   } else {
     const typename MaskT<MB>::T* mask = static_cast<const typename MaskT<MB>::T*>(p.owner_mask);
     for (int e = threadIdx.x; e < len; e += kSyncThreads) {
