@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 # the headline kernel, full set (DRAM bytes -> profiles/traffic.json)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_owner_sync -s 3 -c 1 \
     -o gpurun_out/sync_gpt2 python bench.py --steps 4 --warmup 3 --no-train --no-cpu-baseline > /dev/null 2>&1
-timeout 900 python tools/measure_all.py --only sync,slices > gpurun_out/measure.jsonl 2> gpurun_out/measure.err
+timeout 1500 python tools/measure_all.py --only build,sync,sweep,slices --no-cpu > gpurun_out/measure.jsonl 2> gpurun_out/measure.err
 timeout 700 python tools/small_probe.py --sizes 1,4,16,64 --ps 2,4,8 > gpurun_out/small.jsonl 2> gpurun_out/small.err
 timeout 900 python tools/equal_loss.py --steps 1500 --out gpurun_out/equal_loss.json > /dev/null 2>&1
 timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_multirank.py -q -x -p no:cacheprovider \
