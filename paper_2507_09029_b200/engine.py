@@ -534,8 +534,11 @@ def _aggregate_host_zero_copy(hosts, assignment, check: bool) -> AggregatedGradi
     return AggregatedGradient(gbar=out_np, divisor=assignment.host_divisor())
 
 
-STAGE_CHUNK_BYTES = 64 << 20  # bytes staged per pipeline chunk (all workers together)
-STAGE_SLOTS = 3               # pinned staging slots in flight
+# pageable host path (tools/pageable_probe.py, profiles/r2_pageable_staging_ab.jsonl:
+# C4, 16 threads: 128 MB x 2 slots 67 ms, 64 MB x 3 slots 82 ms, 32 MB 120 ms;
+# a 16-thread pageable -> pinned memcpy alone peaks at 56 GB/s on the box)
+STAGE_CHUNK_BYTES = 128 << 20  # bytes staged per pipeline chunk (all workers together)
+STAGE_SLOTS = 2                # pinned staging slots in flight
 STAGE_PIECE = 4 << 20         # bytes per host-thread memcpy piece
 _STAGING: dict = {}
 _COPY_POOL = None
