@@ -122,8 +122,10 @@ TRAIN_CHILD = textwrap.dedent(r"""
     dev = torch.device("cuda", torch.cuda.current_device())
     model = train.build_resnet18(dev, seed=5)
     a = masking.build_assignment(model.topology, os.environ["STRATEGY"], 4, 2, seed=1)
-    tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05, autocast=os.environ["AUTOCAST"] == "1",
-                           timeout_cycles=10_000_000_000, graphed=os.environ["GRAPHED"] == "1")
+    opt = os.environ.get("OPT", "sgd-nesterov")
+    tr = train.PeerTrainer(model, a, rank, world, dev, all_gather, lr=0.05 if opt == "sgd-nesterov" else 0.002,
+                           autocast=os.environ["AUTOCAST"] == "1", timeout_cycles=10_000_000_000,
+                           graphed=os.environ["GRAPHED"] == "1", optimizer=opt)
     for step in range(2):
         batches = {}
         for w in tr.local:
@@ -142,9 +144,10 @@ TRAIN_CHILD = textwrap.dedent(r"""
 """)
 
 
-@pytest.mark.parametrize("graphed,autocast", [(False, False), (True, False), (True, True)])
+@pytest.mark.parametrize("graphed,autocast,opt", [(False, False, "sgd-nesterov"), (True, False, "sgd-nesterov"),
+                                                  (True, True, "sgd-nesterov"), (True, True, "adam")])
 @pytest.mark.parametrize("strategy", ["block", "neuron"])
-def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, autocast):
+def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, autocast, opt):
     """train.PeerTrainer over 2 processes (CUDA-IPC replicas, cross-rank sync,
     local Nesterov) leaves every worker's copy of its parameters bit-identical
     to the co-resident trainer's canonical theta (deterministic cuDNN; fp32,
@@ -159,7 +162,7 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, auto
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), REPO=repo, OUT=str(tmp_path), STRATEGY=strategy,
-                   GRAPHED=str(int(graphed)), AUTOCAST=str(int(autocast)))
+                   GRAPHED=str(int(graphed)), AUTOCAST=str(int(autocast)), OPT=opt)
         procs.append(subprocess.Popen([sys.executable, "-c", TRAIN_CHILD], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
@@ -176,7 +179,8 @@ def test_peer_trainer_matches_coresident(cuda, tmp_path, strategy, graphed, auto
     try:
         model = train.build_resnet18(cuda, seed=5)
         a = masking.build_assignment(model.topology, strategy, 4, 2, seed=1)
-        tr = train.SubnetTrainer(model, a, lr=0.05, autocast=autocast, sync_layout=strategy == "neuron")
+        tr = train.SubnetTrainer(model, a, lr=0.05 if opt == "sgd-nesterov" else 0.002, autocast=autocast,
+                                 sync_layout=strategy == "neuron", optimizer=opt)
         for step in range(2):
             batches = []
             for w in range(4):
