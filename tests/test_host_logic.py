@@ -80,3 +80,50 @@ def test_busbw_and_link_bytes_accounting():
     plan2 = _fake_plan([(0, 1, 2, 3), (0, 4)], 1000, [0, 1])
     assert comm.busbw_bytes(plan2, lay2) == int(2 * 1 / 2 * 1000 * 4)
     assert comm.link_bytes(plan2, lay2, shadows=False) == {"rx": 1000 * 4, "tx": 1000 * 4}
+
+
+def test_slice_batch_concatenation_rebases_tables():
+    """models.SliceBatch (one launch for all workers): descriptor map offsets
+    and col tables are rebased onto the concatenated map array, every task
+    points at its part's descriptor and carries the part as its segment, and
+    the parts' tasks are interleaved round-robin."""
+    from paper_2507_09029_b200 import models
+    from paper_2507_09029_b200.models import SLICE_DTYPE, TASK_DTYPE
+
+    def part(n_desc, maps_len, map_base):
+        d = np.zeros(n_desc, dtype=SLICE_DTYPE)
+        d["rows"], d["cols"], d["inner"], d["crows"], d["ccols"] = 4, 300, 1, 2, 300
+        d["row_map"] = [map_base, -1][:n_desc] + [-1] * max(0, n_desc - 2)
+        d["col_map"] = -1
+        d["col_tab"] = -1
+        t = models.slice_tasks(d, compact=True, per_task=600)
+        return d, t, np.arange(maps_len, dtype=np.int32), True
+
+    parts = [part(2, 5, 1), part(1, 7, 3), part(2, 3, 0)]
+    sb = models.SliceBatch(parts, torch.device("cpu"), per_task=600)
+    descs = sb.d_descs.numpy().view(SLICE_DTYPE)[: 5]
+    tasks = sb.d_tasks.numpy().view(TASK_DTYPE)[: sb.n_tasks]
+    assert sb.maps.numel() == 5 + 7 + 3
+    assert list(descs["row_map"]) == [1, -1, 5 + 3, 5 + 7 + 0, -1]
+    assert sb.n_tasks == sum(len(p[1]) for p in parts)
+    d_of_seg = {0: {0, 1}, 1: {2}, 2: {3, 4}}
+    for t in tasks:
+        assert int(t["desc"]) in d_of_seg[int(t["seg"])]
+    # round-robin: the first len(parts) tasks come from different parts
+    assert sorted(int(s) for s in tasks["seg"][:3]) == [0, 1, 2]
+    with pytest.raises(Exception):
+        models.SliceBatch([parts[0]] * 65, torch.device("cpu"))
+
+
+def test_adam_bias_table_is_the_reference_arithmetic():
+    """engine.adam_bias_table: row t = (1 - beta1**t, 1 - beta2**t) computed as
+    optim.py:107-108 does (Python float pow), ending at the first t where
+    both are exactly 1.0 (the kernel clamps later steps there)."""
+    from paper_2507_09029_b200 import engine, train
+    tab = engine.adam_bias_table(0.9, 0.999, "cpu").numpy().reshape(-1, 2)
+    for t in range(0, len(tab), 997):
+        assert tab[t, 0] == 1 - 0.9 ** t and tab[t, 1] == 1 - 0.999 ** t
+    assert (tab[-1] == 1.0).all() and not (tab[-2] == 1.0).all()
+    assert 30000 < len(tab) < 60000
+    with pytest.raises(Exception, match="unknown optimizer"):
+        train._check_optimizer("lamb")
