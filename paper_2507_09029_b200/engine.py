@@ -404,11 +404,11 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     return a
 
 
-def adam_bias_table(beta1: float = 0.9, beta2: float = 0.999, dev=None, max_len: int = 1 << 20) -> torch.Tensor:
-    """Float64 [2 * L] device table of the Adam bias corrections
-    (1 - beta1**t, 1 - beta2**t) for t = 0 .. L-1, computed exactly as the
-    reference does (Python float pow, optim.py:107-108), up to the first t
-    where both are exactly 1.0 -- the kernel clamps larger steps to it."""
+def adam_bias_rows(beta1: float = 0.9, beta2: float = 0.999, max_len: int = 1 << 20) -> np.ndarray:
+    """[L, 2] float64: the Adam bias corrections (1 - beta1**t, 1 - beta2**t)
+    for t = 0 .. L-1, computed exactly as the reference does (Python float
+    pow, optim.py:107-108), up to the first t where both are exactly 1.0 --
+    the kernel clamps larger steps to that row."""
     rows = []
     t = 0
     while True:
@@ -417,7 +417,12 @@ def adam_bias_table(beta1: float = 0.9, beta2: float = 0.999, dev=None, max_len:
         if (c1 == 1.0 and c2 == 1.0) or len(rows) >= max_len:
             break
         t += 1
-    return torch.tensor(rows, dtype=torch.float64, device=device(dev)).reshape(-1)
+    return np.array(rows, dtype=np.float64)
+
+
+def adam_bias_table(beta1: float = 0.9, beta2: float = 0.999, dev=None) -> torch.Tensor:
+    """adam_bias_rows on the device, flattened (sdp_sync_args.adam_bias_table)."""
+    return torch.from_numpy(adam_bias_rows(beta1, beta2).reshape(-1)).to(device(dev))
 
 
 def aggregate(grads, assignment) -> AggregatedGradient:

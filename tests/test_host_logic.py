@@ -116,11 +116,11 @@ def test_slice_batch_concatenation_rebases_tables():
 
 
 def test_adam_bias_table_is_the_reference_arithmetic():
-    """engine.adam_bias_table: row t = (1 - beta1**t, 1 - beta2**t) computed as
+    """engine.adam_bias_rows: row t = (1 - beta1**t, 1 - beta2**t) computed as
     optim.py:107-108 does (Python float pow), ending at the first t where
     both are exactly 1.0 (the kernel clamps later steps there)."""
     from paper_2507_09029_b200 import engine, train
-    tab = engine.adam_bias_table(0.9, 0.999, "cpu").numpy().reshape(-1, 2)
+    tab = engine.adam_bias_rows(0.9, 0.999)
     for t in range(0, len(tab), 997):
         assert tab[t, 0] == 1 - 0.9 ** t and tab[t, 1] == 1 - 0.999 ** t
     assert (tab[-1] == 1.0).all() and not (tab[-2] == 1.0).all()
