@@ -181,6 +181,12 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
                                         rank's local workers' (compact) state, after
                                         the exit barrier, instead of in the leader's
                                         epilogue on one flat theta */
+#define SDP_SYNC_DIRECT 0x40         /* small buffers (world 1, flat replicas, N <= 8):
+                                        no tile table -- every thread loads its
+                                        elements' owner masks and ALL N replicas at
+                                        once (one DRAM round trip instead of the
+                                        descriptor -> mask -> owners chain) and adds
+                                        exactly each element's owners, ascending */
 
 /* status word bits written (atomicOr) by the kernel */
 #define SDP_STATUS_UNCOVERED_LEAK 0x1

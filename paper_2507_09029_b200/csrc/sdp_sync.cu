@@ -596,6 +596,69 @@ k_owner_sync(const __grid_constant__ SyncParams p) {
   if (p.epoch_ctr && threadIdx.x == 0) p.epoch_ctr[blockIdx.x] = ep;
 }
 
+// SDP_SYNC_DIRECT: the latency-bound small-buffer form.  Thread t of CTA b
+// owns the VN elements at (b * 256 + t) * VN; it loads their owner masks and
+// the same VN elements of ALL N replicas before the first add -- one DRAM
+// round trip, where the tiled kernel chains descriptor -> mask -> owners --
+// then sums exactly each element's owners in ascending order (non-owners'
+// values are loaded but never used) and runs the usual epilogue.  Flat
+// replicas only (every worker's buffer spans [0, d)).
+template <typename T, int MB, int NW>
+__global__ void __launch_bounds__(kSyncThreads)
+k_owner_sync_direct(const __grid_constant__ SyncParams p) {
+  constexpr int VN = V<T>::N;
+  using Vt = typename V<T>::type;
+  using M = typename MaskT<MB>::T;
+  uint32_t st = 0;
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * kSyncThreads + threadIdx.x) * VN;
+  if (j < p.total) {
+    const M* mask = static_cast<const M*>(p.owner_mask);
+    const int tile = p.tile;
+    const uint32_t tix = static_cast<uint32_t>(j / tile);
+    const int64_t s = static_cast<int64_t>(tix) * tile;
+    const int o = static_cast<int>(j - s);
+    if (j + VN <= p.total) {
+      uint64_t m[VN];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) m[e] = static_cast<uint64_t>(__ldg(mask + j + e));
+      Vt g[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        if (w < p.n_workers) g[w] = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
+      Vt mean;
+      bool same = true;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        T acc = static_cast<T>(0);
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+          if (w < p.n_workers && ((m[e] >> w) & 1ull)) acc = add_rn(acc, g[w].x[e]);
+        const int c = __popcll(m[e]);
+        mean.x[e] = div_rn(acc, static_cast<T>(c > 0 ? c : 1));
+        if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+        if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w)
+            if (w < p.n_workers && !finite(g[w].x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
+        }
+        same &= m[e] == m[0];
+      }
+      if (same) {
+        emit_vec<T, false>(p, tix, s, o, m[0], mean);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) emit_scalar<T, false>(p, tix, s, o + e, m[e], mean.x[e]);
+      }
+    } else {  // the vector's tail past d: element by element
+      for (int e = 0; j + e < p.total; ++e) {
+        const uint64_t m = static_cast<uint64_t>(__ldg(mask + j + e));
+        sync_elem<T, false>(p, tix, s, o + e, m, st);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, st != 0) && st && p.status) atomicOr(p.status, st);
+}
+
 template <typename T>
 __global__ void k_nesterov(int64_t total, T* __restrict__ theta, T* __restrict__ vel,
                            const T* __restrict__ grad, double lr, double momentum,
@@ -760,8 +823,22 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
   if (a->slots && a->slot_stride < (a->total + a->tile - 1) / a->tile)
     return set_error(SDP_ERR_USAGE, "slot_stride %lld is below the tile count", (long long)a->slot_stride);
 
-  const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
   cudaStream_t s = as_stream(stream);
+  if (a->flags & SDP_SYNC_DIRECT) {
+    if (a->world != 1 || a->slots || local_update || a->n_workers > 8 || mb != 1 || !a->owner_mask)
+      return set_error(SDP_ERR_USAGE, "SDP_SYNC_DIRECT needs world 1, flat replicas, N <= 8 (1-byte owner "
+                                      "masks) and the owner mask");
+    const int vn = a->dtype == SDP_DTYPE_F32 ? 4 : 2;
+    const int64_t per_cta = static_cast<int64_t>(kSyncThreads) * vn;
+    const unsigned dgrid = static_cast<unsigned>((a->total + per_cta - 1) / per_cta);
+    if (a->dtype == SDP_DTYPE_F32)
+      k_owner_sync_direct<float, 1, 8><<<dgrid, kSyncThreads, 0, s>>>(p);
+    else
+      k_owner_sync_direct<double, 1, 8><<<dgrid, kSyncThreads, 0, s>>>(p);
+    SDP_LAUNCH_CHECK();
+    return SDP_OK;
+  }
+  const int grid = a->grid > 0 ? a->grid : (a->n_tiles + a->tiles_per_cta - 1) / a->tiles_per_cta;
   // R vectors of 16 B per thread per round: R = 4 for 4096-element fp32 tiles,
   // smaller tiles (shorter tail on small buffers) run R = 2 or 1.
   const int vn = a->dtype == SDP_DTYPE_F32 ? 4 : 2;

@@ -87,6 +87,13 @@ def tile_leaders(tiles: np.ndarray, gpu_of: np.ndarray, world: int) -> np.ndarra
 
 
 BIG_TRAFFIC = 1.5e9  # bytes per launch above which one CTA per tile wins
+def direct_wins(d: int, owned_frac: float) -> bool:
+    """Whether the one-round-trip small-buffer kernel (SDP_SYNC_DIRECT, which
+    also reads the non-owned replica bytes) beats the tiled one.  Same-box
+    A/B, graph-amortised cold launches (profiles/r2_small_buffers_direct_ab.jsonl):
+    it wins up to 1 MiB at any P (10-20 %), up to 2 MiB at P = N/2, and up to
+    16 MiB when every worker owns (nearly) everything (P = N)."""
+    return d <= 1 << 18 or (d <= 1 << 19 and owned_frac >= 0.5) or (d <= 1 << 22 and owned_frac >= 0.99)
 
 
 def plan_grid(n_tiles: int, sms: int, resident: bool, traffic: float = 0.0) -> int:
@@ -131,7 +138,10 @@ class SyncPlan:
                  resident: bool = False, max_grid: int | None = None,
                  force_grid: int | None = None, tile_lo: int | None = None,
                  tile_hi: int | None = None, owner_mask: torch.Tensor | None = None,
-                 order: str = "mixed_first"):
+                 order: str = "mixed_first", direct: bool | None = None):
+        """direct: use the small-buffer kernel (SDP_SYNC_DIRECT) -- by default
+        where direct_wins() says so, for world-1, non-resident, unchunked
+        plans with N <= 8 workers."""
         self.assignment = assignment
         dev = assignment.device
         d = assignment.topology.total
@@ -178,6 +188,9 @@ class SyncPlan:
             self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
         self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
+        self.direct = (direct_wins(d, owned_total / max(1, d * nw)) if direct is None else bool(direct)) \
+            and world == 1 and not resident and tile_lo is None and tile_hi is None \
+            and nw <= 8 and assignment.mask_bytes == 1
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
     def leader_cta(self) -> np.ndarray:
@@ -317,6 +330,10 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     plan = plan or assignment.sync_plan()
     a = plan.args(sdp_dtype(dt))
     flags = 0
+    # small buffers: the one-round-trip kernel (its extra reads of non-owned
+    # replica bytes would cross PCIe on the zero-copy path: device only)
+    if plan.direct and compact is None and local_update is None and not zero_copy:
+        flags |= N.SYNC_DIRECT
     if writeback:
         flags |= N.SYNC_WRITEBACK
     if check_uncovered:

@@ -76,9 +76,15 @@ def test_aggregate_random_instances_vs_loop_oracle(cuda):
         masks = rng.random((n, d)) < rng.uniform(0.0, 1.0)
         grads = [rng.standard_normal(d) * masks[i] for i in range(n)]
         a = masking.MaskAssignment(n, 1, "block", 0, topo, {}, masks, torch.zeros(d, dtype=torch.int64))
-        got = engine.aggregate([torch.from_numpy(g).to(cuda) for g in grads], a).gbar.cpu().numpy()
+        reps = [torch.from_numpy(g).to(cuda) for g in grads]
+        got = engine.aggregate(reps, a).gbar.cpu().numpy()
         want = _aggregate_loops(grads, masks)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), inst
+        # both kernels: the small-buffer one (the default here) and the tiled one
+        out = torch.empty(d, dtype=torch.float64, device=cuda)
+        engine.owner_sync(reps, a, out=out, writeback=False,
+                          plan=engine.SyncPlan(a, direct=not a.sync_plan().direct))
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want.view(np.uint64)), inst
         if inst % 50 == 0:  # the vectorised oracle agrees too
             assert np.array_equal(want, O.aggregate_f64(grads, masks, np.maximum(masks.sum(0), 1).astype(np.float64)))
 

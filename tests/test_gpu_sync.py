@@ -414,6 +414,10 @@ def test_mask_widths_and_partial_tiles(cuda, n, p):
         want = O.aggregate_f32_ordered([r.cpu().numpy() for r in reps], masks)
         got = engine.aggregate(reps, a).gbar.cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (strategy, n, p)
+        # the tiled kernel explicitly (small buffers default to SDP_SYNC_DIRECT at N <= 8)
+        out = torch.empty(topo.total, device=cuda)
+        engine.owner_sync(reps, a, out=out, writeback=False, plan=engine.SyncPlan(a, direct=False))
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), (strategy, n, p)
 
 
 @pytest.mark.slow
@@ -443,3 +447,52 @@ def test_resnet18_and_gpt2_full_size_properties(cuda):
         assert torch.equal(out3, x)
         del reps, doubled, same
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_direct_small_buffer_kernel_equals_tiled(cuda, strategy, dtype):
+    """SDP_SYNC_DIRECT (one round trip: masks + all N replicas loaded at once)
+    == the tiled kernel bit for bit -- mean, bf16 mean, every owner's
+    write-back and bf16 shadow, the fused Nesterov epilogue and the status
+    word -- on sizes with a ragged tail (d not a multiple of the vector)."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    for topo in (zoo.mini_resnet_topology(26, 8, 10, 2, 3, (8, 8)),
+                 zoo.residual_mlp_topology(width=37, blocks=8, classes=3, in_dim=5)):
+        a = masking.build_assignment(topo, strategy, 8, 3, seed=11)
+        d = topo.total
+        pm = a.param_masks
+        gen = torch.Generator(device=cuda)
+        gen.manual_seed(d)
+        base = [(torch.randn(d, generator=gen, device=cuda) * pm[w]).to(dtype) for w in range(8)]
+        th0 = torch.randn(d, generator=gen, device=cuda).to(dtype)
+        res = {}
+        for direct in (False, True):
+            plan = engine.SyncPlan(a, direct=direct)
+            assert plan.direct == direct
+            reps = [b.clone() for b in base]
+            sh = [torch.zeros(d, dtype=torch.bfloat16, device=cuda) for _ in reps]
+            out = torch.empty(d, dtype=dtype, device=cuda)
+            outb = torch.empty(d, dtype=torch.bfloat16, device=cuda)
+            th, v = th0.clone(), torch.zeros_like(th0)
+            tb = torch.empty(d, dtype=torch.bfloat16, device=cuda)
+            status = torch.zeros(1, dtype=torch.int32, device=cuda)
+            engine.PreparedSync(reps, a, writeback=True, shadows_bf16=sh, out=out, out_bf16=outb, plan=plan,
+                                check_finite=True, check_uncovered=True, status=status,
+                                nesterov={"theta": th, "velocity": v, "lr": 0.1, "momentum": 0.9,
+                                          "theta_bf16": tb}).launch()
+            res[direct] = [out, outb.view(torch.int16), th, v, tb.view(torch.int16), status] + reps + \
+                [x.view(torch.int16) for x in sh]
+        for x, y in zip(res[False], res[True]):
+            assert torch.equal(x, y)
+        assert int(res[True][5].item()) == 0
+    # the leak check fires the same way
+    reps = [b.clone() for b in base]
+    unc = torch.nonzero(pm.sum(0) == 0)
+    if len(unc):
+        reps[3][int(unc[0])] = float("inf")
+        st = torch.zeros(1, dtype=torch.int32, device=cuda)
+        engine.PreparedSync(reps, a, writeback=False, out=torch.empty_like(reps[0]), check_uncovered=True,
+                            status=st, plan=engine.SyncPlan(a, direct=True)).launch()
+        assert int(st.item()) & 0x1

@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--strategy", default="block")
     ap.add_argument("--lib", default=None)
     ap.add_argument("--graph-only", action="store_true")
+    ap.add_argument("--direct", type=int, default=None, help="force the small-buffer kernel on (1) / off (0)")
     args = ap.parse_args()
     FW = torch.empty(64 << 20, device=DEV)
     FR = torch.zeros(64 << 20, device=DEV)
@@ -65,8 +66,8 @@ def main():
     tiny = torch.zeros(1, device=DEV)
     med, mn = timed(lambda: tiny.add_(1))
     print(json.dumps({"row": "empty kernel", "us": round(med, 2), "us_min": round(mn, 2)}), flush=True)
-    for mib in [int(x) for x in args.sizes.split(",")]:
-        d = mib * (1 << 20) // 4
+    for mib in [float(x) for x in args.sizes.split(",")]:
+        d = int(mib * (1 << 20)) // 4
         topo = zoo.sweep_topology(d)
         for p in [int(x) for x in args.ps.split(",")]:
             a = masking.build_assignment(topo, args.strategy, args.n, p, seed=1)
@@ -99,7 +100,8 @@ def main():
             for _ in range(k_sets):
                 r_ = [torch.randn(d, device=DEV) * a.param_masks[w] for w in range(args.n)]
                 s_ = [torch.zeros(d, dtype=torch.bfloat16, device=DEV) for _ in r_]
-                sets.append(engine.PreparedSync(r_, a, writeback=True, shadows_bf16=s_, plan=a.sync_plan()))
+                sets.append(engine.PreparedSync(r_, a, writeback=True, shadows_bf16=s_,
+                                                plan=a.sync_plan(direct=args.direct)))
             m_launch = 4 * k_sets
             cs = torch.cuda.Stream()
             with torch.cuda.stream(cs):
@@ -121,7 +123,8 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e3 / m_launch)
             m = sorted(ts)[len(ts) // 2]
-            print(json.dumps({"row": "sync graph", "MiB": mib, "p": p, "sets": k_sets, "launches": m_launch,
+            print(json.dumps({"row": "sync graph", "MiB": mib, "p": p, "direct": sets[0].args.flags & 0x40 != 0,
+                              "sets": k_sets, "launches": m_launch,
                               "bytes": nbytes, "us": round(m, 2), "frac": round(nbytes / m / 1e3 / peak, 3)}),
                   flush=True)
             del reps, shadows, src, dst, sets, g
