@@ -181,7 +181,9 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
                                         rank's local workers' (compact) state, after
                                         the exit barrier, instead of in the leader's
                                         epilogue on one flat theta */
-#define SDP_SYNC_DIRECT 0x40         /* small buffers (world 1, flat replicas, N <= 8):
+#define SDP_SYNC_DIRECT 0x40         /* world 1, flat replicas, N <= 8 (small buffers;
+                                        width-wise plans whose owners hold most of
+                                        the vector):
                                         no tile table -- every thread loads its
                                         elements' owner masks and ALL N replicas at
                                         once (one DRAM round trip instead of the

@@ -621,6 +621,9 @@ k_owner_sync_direct(const __grid_constant__ SyncParams p) {
       uint64_t m[VN];
 #pragma unroll
       for (int e = 0; e < VN; ++e) m[e] = static_cast<uint64_t>(__ldg(mask + j + e));
+      // every worker's vector, issued before the masks arrive (a filtered
+      // form that loaded only the workers a warp's lanes own -- mask first,
+      // then data -- measured slower: profiles/r2_direct_ab.jsonl)
       Vt g[NW];
 #pragma unroll
       for (int w = 0; w < NW; ++w)

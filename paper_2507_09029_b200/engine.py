@@ -87,13 +87,18 @@ def tile_leaders(tiles: np.ndarray, gpu_of: np.ndarray, world: int) -> np.ndarra
 
 
 BIG_TRAFFIC = 1.5e9  # bytes per launch above which one CTA per tile wins
-def direct_wins(d: int, owned_frac: float) -> bool:
-    """Whether the one-round-trip small-buffer kernel (SDP_SYNC_DIRECT, which
-    also reads the non-owned replica bytes) beats the tiled one.  Same-box
-    A/B, graph-amortised cold launches (profiles/r2_small_buffers_direct_ab.jsonl):
-    it wins up to 1 MiB at any P (10-20 %), up to 2 MiB at P = N/2, and up to
-    16 MiB when every worker owns (nearly) everything (P = N)."""
-    return d <= 1 << 18 or (d <= 1 << 19 and owned_frac >= 0.5) or (d <= 1 << 22 and owned_frac >= 0.99)
+def direct_wins(d: int, owned_frac: float, mixed_frac: float = 0.0) -> bool:
+    """Whether the one-round-trip kernel (SDP_SYNC_DIRECT, which also reads
+    the non-owned replica bytes) beats the tiled one.  Same-box A/Bs:
+    * small buffers (profiles/r2_small_buffers_direct_ab.jsonl, graph-
+      amortised cold): up to 1 MiB at any P (10-20 %), up to 2 MiB at
+      P = N/2, up to 16 MiB when every worker owns (nearly) everything;
+    * width-wise plans whose tiles are largely mixed while the owners hold
+      most of the vector (profiles/r2_direct_ab.jsonl): GPT-2 channel units
+      (owned 0.77, mixed tiles 0.41) 795 -> 670 us; ResNet-18 width-wise
+      (owned 0.37) and the block plans stay tiled."""
+    small = d <= 1 << 18 or (d <= 1 << 19 and owned_frac >= 0.5) or (d <= 1 << 22 and owned_frac >= 0.99)
+    return small or (mixed_frac >= 0.3 and owned_frac >= 0.6)
 
 
 def plan_grid(n_tiles: int, sms: int, resident: bool, traffic: float = 0.0) -> int:
@@ -188,7 +193,9 @@ class SyncPlan:
             self.tiles_per_cta = max(1, -(-self.n_tiles // self.grid))
         self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
-        self.direct = (direct_wins(d, owned_total / max(1, d * nw)) if direct is None else bool(direct)) \
+        mixed_frac = 1.0 - self.n_uniform / max(1, len(tiles))
+        self.direct = (direct_wins(d, owned_total / max(1, d * nw), mixed_frac) if direct is None
+                       else bool(direct)) \
             and world == 1 and not resident and tile_lo is None and tile_hi is None \
             and nw <= 8 and assignment.mask_bytes == 1
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())

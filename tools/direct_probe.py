@@ -1,0 +1,39 @@
+"""SDP_SYNC_DIRECT vs the tiled kernel on the width-wise flat-layout aggregate
+(C3 ResNet-18, C4 GPT-2 channel units) and the block configs.  Probe-only."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import measure_all as M  # noqa: E402
+from paper_2507_09029_b200 import engine, masking, zoo  # noqa: E402
+
+
+def main():
+    M.FLUSH_W = torch.empty(64 << 20, device=M.DEV)
+    M.FLUSH_R = torch.zeros(64 << 20, device=M.DEV)
+    for name, topo, strategy in (("C3", zoo.resnet18_cifar_topology(), "neuron"),
+                                 ("C2", zoo.resnet18_cifar_topology(), "block"),
+                                 ("C4n", zoo.gpt2_small_topology(), "neuron"),
+                                 ("C4", zoo.gpt2_small_topology(), "block"),
+                                 ("C5n", zoo.mini_resnet_topology(512, 8, 10, 2, 3, (8, 8)), "neuron")):
+        a = masking.build_assignment(topo, strategy, 8, 4, seed=1)
+        d = topo.total
+        reps = [torch.randn(d, device=M.DEV) * a.param_masks[w] for w in range(8)]
+        out = torch.empty(d, device=M.DEV)
+        for direct in (False, True):
+            plan = engine.SyncPlan(a, direct=direct)
+            prep = engine.PreparedSync(reps, a, writeback=False, out=out, plan=plan)
+            us, mn = M.timed(prep.launch)
+            own = plan.owned_elems
+            nbytes = own * 4 + d * 4 + (plan.n_tiles - plan.n_uniform) * plan.tile
+            print(json.dumps({"cfg": name, "direct": direct, "auto": engine.SyncPlan(a).direct, "us": round(us, 1),
+                              "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
+        del reps
+
+
+if __name__ == "__main__":
+    main()
