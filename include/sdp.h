@@ -189,6 +189,11 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
                                         once (one DRAM round trip instead of the
                                         descriptor -> mask -> owners chain) and adds
                                         exactly each element's owners, ascending */
+#define SDP_SYNC_STREAM 0x80         /* with SDP_SYNC_DIRECT: grid-stride over resident
+                                        CTAs, replica loads only for the workers a
+                                        warp's lanes own, the next vector's masks
+                                        prefetched (owned-line traffic, one round
+                                        trip per vector) */
 
 /* status word bits written (atomicOr) by the kernel */
 #define SDP_STATUS_UNCOVERED_LEAK 0x1

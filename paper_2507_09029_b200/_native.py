@@ -31,6 +31,7 @@ SYNC_NESTEROV = 0x8
 SYNC_ADAM = 0x10
 SYNC_LOCAL_UPDATE = 0x20
 SYNC_DIRECT = 0x40
+SYNC_STREAM = 0x80
 
 SCATTER_ZERO_FILL = 0x1
 SCATTER_ACCUMULATE = 0x2

@@ -18,6 +18,7 @@
 #include "sdp_common.cuh"
 
 #include <cmath>
+#include <type_traits>
 
 namespace sdp {
 
@@ -662,6 +663,88 @@ k_owner_sync_direct(const __grid_constant__ SyncParams p) {
   if (__any_sync(0xffffffffu, st != 0) && st && p.status) atomicOr(p.status, st);
 }
 
+// SDP_SYNC_STREAM: the same per-vector sum as k_owner_sync_direct, in a
+// grid-stride loop of resident CTAs that reads only what the owners hold:
+// a vector's replica loads are issued for the workers some lane of the warp
+// owns (a warp-uniform OR of the lanes' masks; a worker's 128-B lines are
+// fetched whole anyway, so no owned byte is skipped), and the NEXT vector's
+// mask words are requested before this vector's data arrives -- one DRAM
+// round trip per iteration with the owned-line traffic of the tiled kernel.
+template <typename T, int MB, int NW>
+__global__ void __launch_bounds__(kSyncThreads, 4)
+k_owner_sync_stream(const __grid_constant__ SyncParams p) {
+  constexpr int VN = V<T>::N;
+  using Vt = typename V<T>::type;
+  using W = typename std::conditional<VN == 4, uint32_t, uint16_t>::type;  // VN one-byte masks
+  static_assert(MB == 1, "one-byte owner masks");
+  uint32_t st = 0;
+  const int64_t nvec = p.total / VN;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kSyncThreads;
+  const W* mw = reinterpret_cast<const W*>(p.owner_mask);
+  const int tile = p.tile;
+  int64_t v = static_cast<int64_t>(blockIdx.x) * kSyncThreads + threadIdx.x;
+  uint32_t nxt = v < nvec ? static_cast<uint32_t>(__ldg(mw + v)) : 0u;
+  for (; v < nvec; v += stride) {
+    const uint32_t cur = nxt;
+    uint32_t any = 0;
+    bool uncov = false;
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      any |= (cur >> (8 * e)) & 0xFFu;
+      uncov |= ((cur >> (8 * e)) & 0xFFu) == 0u;
+    }
+    // the leak check (engine.py:75-78) reads every worker at zero-coverage
+    // elements, as the tiled kernel does
+    if ((p.flags & SDP_SYNC_CHECK_UNCOVERED) && uncov) any = 0xFFu;
+    const uint32_t need = __reduce_or_sync(__activemask(), any);
+    const int64_t j = v * VN;
+    Vt g[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+      if (w < p.n_workers && ((need >> w) & 1u)) g[w] = V<T>::ld(static_cast<const T*>(p.replicas[w]) + j);
+    if (v + stride < nvec) nxt = static_cast<uint32_t>(__ldg(mw + v + stride));
+    Vt mean;
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      const uint32_t me = (cur >> (8 * e)) & 0xFFu;
+      T acc = static_cast<T>(0);
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        if ((me >> w) & 1u) acc = add_rn(acc, g[w].x[e]);
+      const int c = __popc(me);
+      mean.x[e] = div_rn(acc, static_cast<T>(c > 0 ? c : 1));
+      if ((p.flags & SDP_SYNC_CHECK_FINITE) && !finite(mean.x[e])) st |= SDP_STATUS_NONFINITE;
+      if (c == 0 && (p.flags & SDP_SYNC_CHECK_UNCOVERED)) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+          if (w < p.n_workers && !finite(g[w].x[e])) st |= SDP_STATUS_UNCOVERED_LEAK;
+      }
+    }
+    const uint32_t tix = static_cast<uint32_t>(j / tile);
+    const int64_t s = static_cast<int64_t>(tix) * tile;
+    const int o = static_cast<int>(j - s);
+    bool same = true;
+#pragma unroll
+    for (int e = 1; e < VN; ++e) same &= ((cur >> (8 * e)) & 0xFFu) == (cur & 0xFFu);
+    if (same) {
+      emit_vec<T, false>(p, tix, s, o, cur & 0xFFu, mean);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VN; ++e) emit_scalar<T, false>(p, tix, s, o + e, (cur >> (8 * e)) & 0xFFu, mean.x[e]);
+    }
+  }
+  // the last total % VN elements
+  const int64_t t0 = nvec * VN;
+  if (blockIdx.x == 0 && t0 + threadIdx.x < p.total) {
+    const int64_t j = t0 + threadIdx.x;
+    const uint32_t tix = static_cast<uint32_t>(j / tile);
+    const int64_t s = static_cast<int64_t>(tix) * tile;
+    const uint64_t m = static_cast<uint64_t>(__ldg(static_cast<const uint8_t*>(p.owner_mask) + j));
+    sync_elem<T, false>(p, tix, s, static_cast<int>(j - s), m, st);
+  }
+  if (st && p.status) atomicOr(p.status, st);
+}
+
 template <typename T>
 __global__ void k_nesterov(int64_t total, T* __restrict__ theta, T* __restrict__ vel,
                            const T* __restrict__ grad, double lr, double momentum,
@@ -834,10 +917,18 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
     const int vn = a->dtype == SDP_DTYPE_F32 ? 4 : 2;
     const int64_t per_cta = static_cast<int64_t>(kSyncThreads) * vn;
     const unsigned dgrid = static_cast<unsigned>((a->total + per_cta - 1) / per_cta);
-    if (a->dtype == SDP_DTYPE_F32)
+    if (a->flags & SDP_SYNC_STREAM) {
+      const unsigned sgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(
+          (a->total / vn + kSyncThreads - 1) / kSyncThreads, static_cast<int64_t>(sm_count()) * 4)));
+      if (a->dtype == SDP_DTYPE_F32)
+        k_owner_sync_stream<float, 1, 8><<<sgrid, kSyncThreads, 0, s>>>(p);
+      else
+        k_owner_sync_stream<double, 1, 8><<<sgrid, kSyncThreads, 0, s>>>(p);
+    } else if (a->dtype == SDP_DTYPE_F32) {
       k_owner_sync_direct<float, 1, 8><<<dgrid, kSyncThreads, 0, s>>>(p);
-    else
+    } else {
       k_owner_sync_direct<double, 1, 8><<<dgrid, kSyncThreads, 0, s>>>(p);
+    }
     SDP_LAUNCH_CHECK();
     return SDP_OK;
   }

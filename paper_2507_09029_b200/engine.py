@@ -93,12 +93,13 @@ def direct_wins(d: int, owned_frac: float, mixed_frac: float = 0.0) -> bool:
     * small buffers (profiles/r2_small_buffers_direct_ab.jsonl, graph-
       amortised cold): up to 1 MiB at any P (10-20 %), up to 2 MiB at
       P = N/2, up to 16 MiB when every worker owns (nearly) everything;
-    * width-wise plans whose tiles are largely mixed while the owners hold
-      most of the vector (profiles/r2_direct_ab.jsonl): GPT-2 channel units
-      (owned 0.77, mixed tiles 0.41) 795 -> 670 us; ResNet-18 width-wise
-      (owned 0.37) and the block plans stay tiled."""
+    * width-wise (flat-layout) plans with >= 30 % mixed tiles, in the
+      streaming form (SDP_SYNC_STREAM, owner-filtered lines, prefetched
+      masks; profiles/r2_direct_ab.jsonl): C3 73.6 -> 57.4 us, the c=512
+      neuron sweep 196 -> 172 us, GPT-2 channel units 796 -> 679 us; block
+      plans (uniform tiles) stay tiled."""
     small = d <= 1 << 18 or (d <= 1 << 19 and owned_frac >= 0.5) or (d <= 1 << 22 and owned_frac >= 0.99)
-    return small or (mixed_frac >= 0.3 and owned_frac >= 0.6)
+    return small or mixed_frac >= 0.3
 
 
 def plan_grid(n_tiles: int, sms: int, resident: bool, traffic: float = 0.0) -> int:
@@ -143,7 +144,8 @@ class SyncPlan:
                  resident: bool = False, max_grid: int | None = None,
                  force_grid: int | None = None, tile_lo: int | None = None,
                  tile_hi: int | None = None, owner_mask: torch.Tensor | None = None,
-                 order: str = "mixed_first", direct: bool | None = None):
+                 order: str = "mixed_first", direct: bool | None = None,
+                 stream: bool | None = None):
         """direct: use the small-buffer kernel (SDP_SYNC_DIRECT) -- by default
         where direct_wins() says so, for world-1, non-resident, unchunked
         plans with N <= 8 workers."""
@@ -198,6 +200,8 @@ class SyncPlan:
                        else bool(direct)) \
             and world == 1 and not resident and tile_lo is None and tile_hi is None \
             and nw <= 8 and assignment.mask_bytes == 1
+        # a width-wise plan with many mixed tiles: stream owner-filtered lines
+        self.stream = (mixed_frac >= 0.3 if stream is None else bool(stream)) and self.direct
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
     def leader_cta(self) -> np.ndarray:
@@ -341,6 +345,8 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     # replica bytes would cross PCIe on the zero-copy path: device only)
     if plan.direct and compact is None and local_update is None and not zero_copy:
         flags |= N.SYNC_DIRECT
+        if plan.stream:
+            flags |= N.SYNC_STREAM
     if writeback:
         flags |= N.SYNC_WRITEBACK
     if check_uncovered:

@@ -24,16 +24,36 @@ def main():
         d = topo.total
         reps = [torch.randn(d, device=M.DEV) * a.param_masks[w] for w in range(8)]
         out = torch.empty(d, device=M.DEV)
-        for direct in (False, True):
-            plan = engine.SyncPlan(a, direct=direct)
+        for direct, stream in ((False, False), (True, False), (True, True)):
+            plan = engine.SyncPlan(a, direct=direct, stream=stream)
             prep = engine.PreparedSync(reps, a, writeback=False, out=out, plan=plan)
             us, mn = M.timed(prep.launch)
             own = plan.owned_elems
             nbytes = own * 4 + d * 4 + (plan.n_tiles - plan.n_uniform) * plan.tile
-            print(json.dumps({"cfg": name, "direct": direct, "auto": engine.SyncPlan(a).direct, "us": round(us, 1),
+            print(json.dumps({"cfg": name, "direct": direct, "stream": stream, "auto": engine.SyncPlan(a).direct,
+                              "us": round(us, 1),
                               "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
         del reps
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--aggregate" not in sys.argv:
     main()
+
+
+def aggregate_c3():
+    """The drop-in engine.aggregate at C3 (leak check on: uncovered entries)."""
+    topo = zoo.resnet18_cifar_topology()
+    a = masking.build_assignment(topo, "neuron", 8, 4, seed=1)
+    d = topo.total
+    reps = [torch.randn(d, device=M.DEV) * a.param_masks[w] for w in range(8)]
+    us, _ = M.timed(lambda: engine.aggregate(reps, a))
+    plan = a.sync_plan()
+    nbytes = plan.owned_elems * 4 + d * 4
+    print(json.dumps({"cfg": "C3 engine.aggregate", "direct": plan.direct, "stream": plan.stream,
+                      "us": round(us, 1), "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
+
+
+if __name__ == "__main__" and "--aggregate" in sys.argv:
+    M.FLUSH_W = torch.empty(64 << 20, device=M.DEV)
+    M.FLUSH_R = torch.zeros(64 << 20, device=M.DEV)
+    aggregate_c3()
