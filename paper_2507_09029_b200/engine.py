@@ -87,19 +87,22 @@ def tile_leaders(tiles: np.ndarray, gpu_of: np.ndarray, world: int) -> np.ndarra
 
 
 BIG_TRAFFIC = 1.5e9  # bytes per launch above which one CTA per tile wins
-def direct_wins(d: int, owned_frac: float, mixed_frac: float = 0.0) -> bool:
-    """Whether the one-round-trip kernel (SDP_SYNC_DIRECT, which also reads
-    the non-owned replica bytes) beats the tiled one.  Same-box A/Bs:
+def direct_wins(d: int, owned_frac: float, mixed_frac: float = 0.0) -> tuple[bool, bool]:
+    """(small, mixed): whether the one-round-trip kernel (SDP_SYNC_DIRECT,
+    which also reads the non-owned replica bytes) beats the tiled one for
+    every launch of the plan, and whether the streaming form does for its
+    plain `aggregate` launches.  Same-box A/Bs:
     * small buffers (profiles/r2_small_buffers_direct_ab.jsonl, graph-
       amortised cold): up to 1 MiB at any P (10-20 %), up to 2 MiB at
       P = N/2, up to 16 MiB when every worker owns (nearly) everything;
     * width-wise (flat-layout) plans with >= 30 % mixed tiles, in the
       streaming form (SDP_SYNC_STREAM, owner-filtered lines, prefetched
       masks; profiles/r2_direct_ab.jsonl): C3 73.6 -> 57.4 us, the c=512
-      neuron sweep 196 -> 172 us, GPT-2 channel units 796 -> 679 us; block
-      plans (uniform tiles) stay tiled."""
+      neuron sweep 196 -> 172 us, GPT-2 channel units 796 -> 679 us -- in
+      the mean-only form; with the per-owner write-back it lost (C3 128 ->
+      147 us), so those launches stay tiled, as do the block plans."""
     small = d <= 1 << 18 or (d <= 1 << 19 and owned_frac >= 0.5) or (d <= 1 << 22 and owned_frac >= 0.99)
-    return small or mixed_frac >= 0.3
+    return small, (not small) and mixed_frac >= 0.3
 
 
 def plan_grid(n_tiles: int, sms: int, resident: bool, traffic: float = 0.0) -> int:
@@ -196,12 +199,15 @@ class SyncPlan:
         self.mine = mine
         self.table = upload_struct(cta_major(mine, self.grid, self.tiles_per_cta), dev)
         mixed_frac = 1.0 - self.n_uniform / max(1, len(tiles))
-        self.direct = (direct_wins(d, owned_total / max(1, d * nw), mixed_frac) if direct is None
-                       else bool(direct)) \
-            and world == 1 and not resident and tile_lo is None and tile_hi is None \
+        eligible = world == 1 and not resident and tile_lo is None and tile_hi is None \
             and nw <= 8 and assignment.mask_bytes == 1
-        # a width-wise plan with many mixed tiles: stream owner-filtered lines
-        self.stream = (mixed_frac >= 0.3 if stream is None else bool(stream)) and self.direct
+        small, mixed = direct_wins(d, owned_total / max(1, d * nw), mixed_frac)
+        # direct / stream given: that kernel for every launch (tests, A/B);
+        # by default the small-buffer kernel for every launch of a small plan
+        # and the streaming one for the mean-only launches of a mixed plan
+        self.direct = eligible and (small if direct is None else bool(direct))
+        self.stream = eligible and bool(stream)
+        self.stream_mean = eligible and mixed and direct is None and stream is None
         self.owned_elems = int(self.tile_owned[mine["tile_index"].astype(np.int64)].sum())
 
     def leader_cta(self) -> np.ndarray:
@@ -343,10 +349,15 @@ def _bind(replicas, assignment, *, out: torch.Tensor | None = None,
     flags = 0
     # small buffers: the one-round-trip kernel (its extra reads of non-owned
     # replica bytes would cross PCIe on the zero-copy path: device only)
-    if plan.direct and compact is None and local_update is None and not zero_copy:
-        flags |= N.SYNC_DIRECT
-        if plan.stream:
-            flags |= N.SYNC_STREAM
+    # small buffers: the one-round-trip kernel; a mixed-tile (width-wise flat)
+    # plan in the plain `aggregate` form (mean out only -- its per-owner
+    # write-back / optimizer epilogue measured slower there): the streaming one
+    pure_mean = not writeback and nesterov is None and adam is None
+    if compact is None and local_update is None and not zero_copy:
+        if plan.stream or (plan.stream_mean and pure_mean):
+            flags |= N.SYNC_DIRECT | N.SYNC_STREAM
+        elif plan.direct:
+            flags |= N.SYNC_DIRECT
     if writeback:
         flags |= N.SYNC_WRITEBACK
     if check_uncovered:

@@ -30,7 +30,9 @@ def main():
             us, mn = M.timed(prep.launch)
             own = plan.owned_elems
             nbytes = own * 4 + d * 4 + (plan.n_tiles - plan.n_uniform) * plan.tile
-            print(json.dumps({"cfg": name, "direct": direct, "stream": stream, "auto": engine.SyncPlan(a).direct,
+            auto = engine.SyncPlan(a)
+            print(json.dumps({"cfg": name, "direct": direct, "stream": stream,
+                              "auto": [auto.direct, auto.stream_mean],
                               "us": round(us, 1),
                               "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
         del reps
@@ -49,7 +51,7 @@ def aggregate_c3():
     us, _ = M.timed(lambda: engine.aggregate(reps, a))
     plan = a.sync_plan()
     nbytes = plan.owned_elems * 4 + d * 4
-    print(json.dumps({"cfg": "C3 engine.aggregate", "direct": plan.direct, "stream": plan.stream,
+    print(json.dumps({"cfg": "C3 engine.aggregate", "direct": plan.direct, "stream_mean": plan.stream_mean,
                       "us": round(us, 1), "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
 
 
