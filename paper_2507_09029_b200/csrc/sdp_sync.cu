@@ -24,6 +24,10 @@ namespace sdp {
 
 constexpr int kSyncThreads = 256;
 constexpr int kStage = 512;  // descriptors staged per bulk copy (8 KB)
+#ifndef SDP_STREAM_CTAS
+#define SDP_STREAM_CTAS 4
+#endif
+constexpr int kStreamCtasPerSm = SDP_STREAM_CTAS;  // resident CTAs of the streaming kernel
 
 template <typename T> struct V;
 template <> struct V<float> {
@@ -647,7 +651,10 @@ k_owner_sync_direct(const __grid_constant__ SyncParams p) {
         }
         same &= m[e] == m[0];
       }
-      if (same) {
+      if (!(p.flags & SDP_SYNC_WRITEBACK) && !epilogue_optim(p)) {
+        if (p.out) V<T>::st(static_cast<T*>(p.out) + j, mean);
+        if (p.out_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.out_bf16) + j, mean);
+      } else if (same) {
         emit_vec<T, false>(p, tix, s, o, m[0], mean);
       } else {
 #pragma unroll
@@ -670,8 +677,10 @@ k_owner_sync_direct(const __grid_constant__ SyncParams p) {
 // fetched whole anyway, so no owned byte is skipped), and the NEXT vector's
 // mask words are requested before this vector's data arrives -- one DRAM
 // round trip per iteration with the owned-line traffic of the tiled kernel.
-template <typename T, int MB, int NW>
-__global__ void __launch_bounds__(kSyncThreads, 4)
+// MEAN: a mean-only launch (no write-back, no optimizer): the epilogue is
+// compiled down to the two vector stores.
+template <typename T, int MB, int NW, bool MEAN>
+__global__ void __launch_bounds__(kSyncThreads, kStreamCtasPerSm)
 k_owner_sync_stream(const __grid_constant__ SyncParams p) {
   constexpr int VN = V<T>::N;
   using Vt = typename V<T>::type;
@@ -726,7 +735,14 @@ k_owner_sync_stream(const __grid_constant__ SyncParams p) {
     bool same = true;
 #pragma unroll
     for (int e = 1; e < VN; ++e) same &= ((cur >> (8 * e)) & 0xFFu) == (cur & 0xFFu);
-    if (same) {
+    // mean-only launches (the drop-in `aggregate`): the per-element means go
+    // out as whole 16-B vectors whatever the owner sets, and the write-back /
+    // optimizer epilogue is compiled out (C3 59 -> 43 us, the c=512 neuron
+    // sweep 176 -> 133 us; profiles/r2_stream_mean_ab.jsonl)
+    if (MEAN) {
+      if (p.out) V<T>::st(static_cast<T*>(p.out) + j, mean);
+      if (p.out_bf16) V<T>::st_bf16(static_cast<__nv_bfloat16*>(p.out_bf16) + j, mean);
+    } else if (same) {
       emit_vec<T, false>(p, tix, s, o, cur & 0xFFu, mean);
     } else {
 #pragma unroll
@@ -919,11 +935,15 @@ int sdp_owner_sync(const sdp_sync_args* a, void* stream) {
     const unsigned dgrid = static_cast<unsigned>((a->total + per_cta - 1) / per_cta);
     if (a->flags & SDP_SYNC_STREAM) {
       const unsigned sgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(
-          (a->total / vn + kSyncThreads - 1) / kSyncThreads, static_cast<int64_t>(sm_count()) * 4)));
-      if (a->dtype == SDP_DTYPE_F32)
-        k_owner_sync_stream<float, 1, 8><<<sgrid, kSyncThreads, 0, s>>>(p);
-      else
-        k_owner_sync_stream<double, 1, 8><<<sgrid, kSyncThreads, 0, s>>>(p);
+          (a->total / vn + kSyncThreads - 1) / kSyncThreads, static_cast<int64_t>(sm_count()) * kStreamCtasPerSm)));
+      const bool mean_only = !(a->flags & (SDP_SYNC_WRITEBACK | SDP_SYNC_NESTEROV | SDP_SYNC_ADAM));
+      if (a->dtype == SDP_DTYPE_F32) {
+        if (mean_only) k_owner_sync_stream<float, 1, 8, true><<<sgrid, kSyncThreads, 0, s>>>(p);
+        else k_owner_sync_stream<float, 1, 8, false><<<sgrid, kSyncThreads, 0, s>>>(p);
+      } else {
+        if (mean_only) k_owner_sync_stream<double, 1, 8, true><<<sgrid, kSyncThreads, 0, s>>>(p);
+        else k_owner_sync_stream<double, 1, 8, false><<<sgrid, kSyncThreads, 0, s>>>(p);
+      }
     } else if (a->dtype == SDP_DTYPE_F32) {
       k_owner_sync_direct<float, 1, 8><<<dgrid, kSyncThreads, 0, s>>>(p);
     } else {

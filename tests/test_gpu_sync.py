@@ -536,3 +536,41 @@ def test_stream_kernel_equals_tiled(cuda, strategy, dtype):
             engine.PreparedSync(reps, a, writeback=False, out=torch.empty_like(reps[0]), check_uncovered=True,
                                 status=st, plan=engine.SyncPlan(a, direct=True, stream=True)).launch()
             assert int(st.item()) & 0x1
+
+
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_stream_kernel_mean_only_equals_tiled(cuda, strategy, dtype):
+    """The mean-only instantiation of SDP_SYNC_STREAM (what the drop-in
+    `aggregate` runs on width-wise flat plans: whole-vector stores of the
+    per-element means, owners skipped warp-uniformly) == the tiled kernel bit
+    for bit -- mean, bf16 mean, status -- replicas untouched; and the routed
+    default plan picks it for a mixed-tile neuron plan."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    for topo in (zoo.resnet18_cifar_topology(), zoo.residual_mlp_topology(width=37, blocks=8, classes=3, in_dim=5)):
+        a = masking.build_assignment(topo, strategy, 8, 4, seed=3)
+        d = topo.total
+        pm = a.param_masks
+        gen = torch.Generator(device=cuda)
+        gen.manual_seed(d + 7)
+        base = [(torch.randn(d, generator=gen, device=cuda) * pm[w]).to(dtype) for w in range(8)]
+        res = {}
+        for stream in (False, True):
+            plan = engine.SyncPlan(a, direct=stream, stream=stream)
+            reps = [b.clone() for b in base]
+            out = torch.empty(d, dtype=dtype, device=cuda)
+            outb = torch.empty(d, dtype=torch.bfloat16, device=cuda)
+            st = torch.zeros(1, dtype=torch.int32, device=cuda)
+            engine.PreparedSync(reps, a, writeback=False, out=out, out_bf16=outb, plan=plan, check_finite=True,
+                                check_uncovered=True, status=st).launch()
+            for r, b in zip(reps, base):
+                assert torch.equal(r, b)
+            res[stream] = [out, outb.view(torch.int16), st]
+        for x, y in zip(res[False], res[True]):
+            assert torch.equal(x, y)
+        assert int(res[True][2].item()) == 0
+        if strategy == "neuron" and topo.total > 1 << 20:
+            assert a.sync_plan().stream_mean
+            g = engine.aggregate(base, a).gbar
+            assert torch.equal(g, res[False][0])

@@ -2,7 +2,7 @@
 
     python tools/variant_probe.py tools/_variants/<name>/libsdp.so [cases]
 
-cases: comma list of c2,c3,c3agg,c3lay,c4,c4nagg (default: all)
+cases: comma list of c2,c3,c3agg,c3lay,c4,c4nagg,c3s,c4ns,c4n,c5n (default: the first six)
 """
 import sys
 from pathlib import Path
@@ -37,6 +37,18 @@ def main():
         M.sync_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4)
     if "c4nagg" in cases:
         M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise", "neuron", 8, 4, writeback=False, shadows=False)
+    # the streaming kernel forced onto the write-back launches (routing A/B)
+    if "c3s" in cases:
+        M.sync_case(r18, f"[{tag}] C3 resnet18 stream", "neuron", 8, 4, direct=True, stream=True)
+    if "c4ns" in cases:
+        M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise stream", "neuron", 8, 4, direct=True, stream=True)
+    if "c4n" in cases:
+        M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise", "neuron", 8, 4)
+    if "c5n" in cases:
+        c5 = zoo.mini_resnet_topology(512, 8, 10, 2, 3, (8, 8))
+        M.sync_case(c5, f"[{tag}] C5 neuron c=512", "neuron", 8, 4, writeback=False, shadows=False)
+        M.sync_case(c5, f"[{tag}] C5 neuron c=512", "neuron", 8, 4)
+        M.sync_case(c5, f"[{tag}] C5 neuron c=512 stream", "neuron", 8, 4, direct=True, stream=True)
 
 
 if __name__ == "__main__":
