@@ -554,7 +554,19 @@ k_build_masks(const sdp_param_desc* __restrict__ params, int n_params,
   for (int g = 0; g < kGroups; ++g) packed[g] = 0;
   ParamCursor cur;
   cur.pi = -1;
-  for (int64_t k = warp0; k < n_steps; k += n_warps) {  // warp-uniform trip count
+  // Which steps a warp takes: a contiguous share when the share is small
+  // (<= 16 steps: consecutive steps stay in one parameter, so the cursor --
+  // binary search + rule loads -- is reused; ResNet-18 C2 / C3 82-87 ->
+  // 70-73 / 69 us), else the interleaved grid stride, which keeps the
+  // per-warp cost even where the per-element rule walk is dear in some
+  // parameters only (GPT-2 channel units: contiguous shares were 4% slower;
+  // profiles/r2_build_steps_ab.jsonl).
+  const int64_t per_warp = (n_steps + n_warps - 1) / n_warps;
+  const bool contiguous = per_warp <= 16;
+  const int64_t k0 = contiguous ? warp0 * per_warp : warp0;
+  const int64_t k_step = contiguous ? 1 : n_warps;
+  const int64_t k_end = contiguous ? min(n_steps, k0 + per_warp) : n_steps;
+  for (int64_t k = k0; k < k_end; k += k_step) {  // warp-uniform trip count
     // Whole step inside one parameter with one owner set (block rules or no
     // rule: the block strategy almost everywhere): constant fills, no
     // per-element work.  The cursor is loaded from the step start, so it is

@@ -37,6 +37,14 @@ def main():
         M.sync_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4)
     if "c4nagg" in cases:
         M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise", "neuron", 8, 4, writeback=False, shadows=False)
+    # the mask builder (k_assign + k_build_masks)
+    if "b2" in cases:
+        M.build_case(r18, f"[{tag}] C2 resnet18", "block", 8, 4)
+    if "b3" in cases:
+        M.build_case(r18, f"[{tag}] C3 resnet18", "neuron", 8, 4)
+    if "b4" in cases:
+        M.build_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4)
+        M.build_case(gpt2, f"[{tag}] C4 gpt2 neuron", "neuron", 8, 4)
     # the streaming kernel forced onto the write-back launches (routing A/B)
     if "c3s" in cases:
         M.sync_case(r18, f"[{tag}] C3 resnet18 stream", "neuron", 8, 4, direct=True, stream=True)
