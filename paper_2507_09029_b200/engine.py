@@ -619,7 +619,7 @@ def _aggregate_host_staged(grads, assignment, check: bool) -> AggregatedGradient
         return _host_staged(grads, assignment, check)
 
 
-def _host_staged(grads, assignment, check: bool) -> AggregatedGradient:
+def _host_staged(grads, assignment, check: bool, pinned=None, chunk_bytes: int | None = None) -> AggregatedGradient:
     """Host-buffer aggregate over ordinary (pageable) numpy arrays -- what a
     reference caller passes (engine.run hands over flat_gradient outputs).
     The vector is cut into tile-range chunks of ~STAGE_CHUNK_BYTES of input;
@@ -629,17 +629,20 @@ def _host_staged(grads, assignment, check: bool) -> AggregatedGradient:
     sync runs on the chunk, and the mean's D2H goes into a pinned result --
     host copies of chunk c+1 overlap the H2D / sync / D2H of chunk c.  With
     the uncovered-leak check every worker's full range is staged (the kernel
-    reads all workers at zero-coverage entries)."""
+    reads all workers at zero-coverage entries).
+
+    pinned: the inputs as pinned host tensors -- then the copy engine moves
+    each chunk's owned ranges straight from them (no staging copies)."""
     n, d = assignment.n_workers, assignment.topology.total
     dev = assignment.device
-    dt = torch.float64 if grads[0].dtype == np.float64 else torch.float32
+    dt = pinned[0].dtype if pinned is not None else (torch.float64 if grads[0].dtype == np.float64 else torch.float32)
     esz = 8 if dt == torch.float64 else 4
     full = assignment.sync_plan()
     tile = full.tile
     n_tiles = len(full.all_tiles)
     ranges = [[(0, d)] if check else full.worker_ranges(w) for w in range(n)]
     staged = sum(ln for rs in ranges for _, ln in rs)
-    k = max(1, min(n_tiles, -(-staged * esz // STAGE_CHUNK_BYTES)))
+    k = max(1, min(n_tiles, -(-staged * esz // (chunk_bytes or STAGE_CHUNK_BYTES))))
     bounds = [n_tiles * c // k for c in range(k + 1)]
     chunks = []
     for c in range(k):
@@ -653,7 +656,8 @@ def _host_staged(grads, assignment, check: bool) -> AggregatedGradient:
                     off += b - a
         chunks.append((lo_e, hi_e, pieces, off))
     slot_elems = max(1, max(ch[3] for ch in chunks))
-    buf, buf_np, evs, used = _staging(dev, dt, slot_elems)
+    if pinned is None:
+        buf, buf_np, evs, used = _staging(dev, dt, slot_elems)
     reps = [torch.empty(d, dtype=dt, device=dev) for _ in range(n)]
     gbar = torch.empty(d, dtype=dt, device=dev)
     out_np, out = _RESULTS.get(d, dt)
@@ -664,20 +668,28 @@ def _host_staged(grads, assignment, check: bool) -> AggregatedGradient:
     piece = max(1, STAGE_PIECE // esz)
     status = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
     for c, (lo_e, hi_e, pieces, _) in enumerate(chunks):
-        slot = c % STAGE_SLOTS
-        if used[slot]:
-            evs[slot].synchronize()  # the slot's previous H2D has drained
-        base = slot * slot_elems
-        jobs = [(w, a0, min(a0 + piece, b), off + (a0 - a))
-                for w, a, b, off in pieces for a0 in range(a, b, piece)]
-        list(pool.map(lambda j: np.copyto(buf_np[base + j[3]:base + j[3] + j[2] - j[1]], grads[j[0]][j[1]:j[2]]),
-                      jobs))
-        with torch.cuda.stream(s_in):
-            for w, a, b, off in pieces:
-                reps[w][a:b].copy_(buf[base + off:base + off + b - a], non_blocking=True)
-            evs[slot].record(s_in)
-            used[slot] = True
-        cur.wait_event(evs[slot])
+        if pinned is not None:
+            ev_in = torch.cuda.Event()
+            with torch.cuda.stream(s_in):
+                for w, a, b, off in pieces:
+                    reps[w][a:b].copy_(pinned[w][a:b], non_blocking=True)
+                ev_in.record(s_in)
+            cur.wait_event(ev_in)
+        else:
+            slot = c % STAGE_SLOTS
+            if used[slot]:
+                evs[slot].synchronize()  # the slot's previous H2D has drained
+            base = slot * slot_elems
+            jobs = [(w, a0, min(a0 + piece, b), off + (a0 - a))
+                    for w, a, b, off in pieces for a0 in range(a, b, piece)]
+            list(pool.map(lambda j: np.copyto(buf_np[base + j[3]:base + j[3] + j[2] - j[1]],
+                                              grads[j[0]][j[1]:j[2]]), jobs))
+            with torch.cuda.stream(s_in):
+                for w, a, b, off in pieces:
+                    reps[w][a:b].copy_(buf[base + off:base + off + b - a], non_blocking=True)
+                evs[slot].record(s_in)
+                used[slot] = True
+            cur.wait_event(evs[slot])
         plan = assignment.sync_plan(tile=tile, tile_lo=bounds[c], tile_hi=bounds[c + 1])
         owner_sync(reps, assignment, out=gbar, writeback=False, plan=plan, check_uncovered=check, status=status)
         ev_c = torch.cuda.Event()

@@ -168,6 +168,26 @@ def test_pageable_staged_many_chunks_bitexact(cuda, strategy, monkeypatch):
     assert np.array_equal(host.view(np.uint32), O.aggregate_f32_ordered(list(g32), masks).view(np.uint32))
 
 
+@pytest.mark.parametrize("strategy", ["block", "neuron"])
+def test_pinned_copy_pipeline_bitexact(cuda, strategy):
+    """The copy-engine pipeline over pinned inputs (the measured alternative
+    to the zero-copy path, profiles/r2_pinned_pipeline_ab.jsonl) with many
+    small chunks == the zero-copy path == the ordered restatement."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (8, 8))
+    a = masking.build_assignment(topo, strategy, 8, 3, seed=9)
+    masks = a.param_masks.cpu().numpy()
+    rng = np.random.default_rng(8)
+    g32 = (rng.standard_normal((8, topo.total)) * masks).astype(np.float32)
+    pinned = [torch.from_numpy(g).pin_memory() for g in g32]
+    check = a.uncovered_params > 0
+    pipe = engine._host_staged(None, a, check, pinned=pinned, chunk_bytes=1 << 16).gbar.copy()
+    zero = engine.aggregate([p.numpy() for p in pinned], a).gbar
+    assert np.array_equal(pipe.view(np.uint32), zero.view(np.uint32))
+    assert np.array_equal(pipe.view(np.uint32), O.aggregate_f32_ordered(list(g32), masks).view(np.uint32))
+
+
 def test_disjoint_known_answer(cuda):
     """SPEC.md:298: m1=[1,0], m2=[0,1], g1=[2,0], g2=[0,4] -> [2,4]."""
     engine, masking = _pkg()
