@@ -317,23 +317,38 @@ __device__ __forceinline__ void scatter_tiled(const sdp_slice_task& tk, const sd
         fr[j] = fbase + static_cast<uint32_t>(f) * row_len + eb;
       }
       T v[kRowsPerIter][kSliceBatch];
-#pragma unroll
-      for (int j = 0; j < kRowsPerIter; ++j) {
-        const T* crow = cbase + static_cast<uint32_t>(max(a[j], 0)) * crow_len;
-#pragma unroll
-        for (int k = 0; k < kSliceBatch; ++k) {
-          v[j][k] = T(0);
-          if (a[j] >= 0 && co[k] >= 0) v[j][k] = __ldg(crow + co[k]);
-        }
-      }
       if (accumulate) {
+        // the full-side loads go out with the compact ones (one round trip);
         // not idempotent: never apply a duplicated last row twice
+        T o[kRowsPerIter][kSliceBatch];
+#pragma unroll
+        for (int j = 0; j < kRowsPerIter; ++j) {
+          const T* crow = cbase + static_cast<uint32_t>(max(a[j], 0)) * crow_len;
+          const bool live = r0 + j < tk.row_end && a[j] >= 0;
+#pragma unroll
+          for (int k = 0; k < kSliceBatch; ++k) {
+            v[j][k] = T(0);
+            o[j][k] = T(0);
+            if (live && co[k] >= 0) {
+              v[j][k] = __ldg(crow + co[k]);
+              o[j][k] = fr[j][k * kSliceThreads];
+            }
+          }
+        }
 #pragma unroll
         for (int j = 0; j < kRowsPerIter; ++j)
 #pragma unroll
-          for (int k = 0; k < kSliceBatch; ++k)
-            if (r0 + j < tk.row_end && a[j] >= 0 && co[k] >= 0)
-              v[j][k] = static_cast<T>(fr[j][k * kSliceThreads] + v[j][k]);
+          for (int k = 0; k < kSliceBatch; ++k) v[j][k] = static_cast<T>(o[j][k] + v[j][k]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kRowsPerIter; ++j) {
+          const T* crow = cbase + static_cast<uint32_t>(max(a[j], 0)) * crow_len;
+#pragma unroll
+          for (int k = 0; k < kSliceBatch; ++k) {
+            v[j][k] = T(0);
+            if (a[j] >= 0 && co[k] >= 0) v[j][k] = __ldg(crow + co[k]);
+          }
+        }
       }
 #pragma unroll
       for (int j = 0; j < kRowsPerIter; ++j) {

@@ -37,6 +37,11 @@ def main():
         M.sync_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4)
     if "c4nagg" in cases:
         M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise", "neuron", 8, 4, writeback=False, shadows=False)
+    # the slice kernels (per worker and all workers per launch)
+    if "s3" in cases:
+        M.slices_case(r18, f"[{tag}] C3 resnet18", "neuron", 8, 4)
+    if "s4" in cases:
+        M.slices_case(gpt2, f"[{tag}] C4 gpt2 (mlp units)", "neuron", 8, 4)
     # the mask builder (k_assign + k_build_masks)
     if "b2" in cases:
         M.build_case(r18, f"[{tag}] C2 resnet18", "block", 8, 4)
