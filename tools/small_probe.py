@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--lib", default=None)
     ap.add_argument("--graph-only", action="store_true")
     ap.add_argument("--direct", type=int, default=None, help="force the small-buffer kernel on (1) / off (0)")
+    ap.add_argument("--plans", default="{}", help="JSON list of extra sync_plan kwargs for the graph rows")
     args = ap.parse_args()
     FW = torch.empty(64 << 20, device=DEV)
     FR = torch.zeros(64 << 20, device=DEV)
@@ -94,6 +95,14 @@ def main():
             # graph-amortised: M back-to-back launches over K distinct replica
             # sets whose footprint is > 2x L2 (each launch reads cold HBM), so
             # the per-launch time is free of the ~6 us event / launch floor
+            for pk in ([{}] + json.loads(args.plans) if args.plans != "{}" else [{}]):
+                graph_row(args, a, d, mib, p, nbytes, peak, pk)
+            del reps, shadows, src, dst
+
+
+def graph_row(args, a, d, mib, p, nbytes, peak, pk):
+    if True:
+        if True:
             n_bytes_set = args.n * d * 6
             k_sets = max(2, min(64, -(-(300 << 20) // n_bytes_set)))
             sets = []
@@ -101,7 +110,7 @@ def main():
                 r_ = [torch.randn(d, device=DEV) * a.param_masks[w] for w in range(args.n)]
                 s_ = [torch.zeros(d, dtype=torch.bfloat16, device=DEV) for _ in r_]
                 sets.append(engine.PreparedSync(r_, a, writeback=True, shadows_bf16=s_,
-                                                plan=a.sync_plan(direct=args.direct)))
+                                                plan=a.sync_plan(direct=args.direct, **pk)))
             m_launch = 4 * k_sets
             cs = torch.cuda.Stream()
             with torch.cuda.stream(cs):
@@ -124,10 +133,11 @@ def main():
                 ts.append(e0.elapsed_time(e1) * 1e3 / m_launch)
             m = sorted(ts)[len(ts) // 2]
             print(json.dumps({"row": "sync graph", "MiB": mib, "p": p, "direct": sets[0].args.flags & 0x40 != 0,
+                              "plan": pk, "grid": sets[0].args.grid, "tile": sets[0].args.tile,
                               "sets": k_sets, "launches": m_launch,
                               "bytes": nbytes, "us": round(m, 2), "frac": round(nbytes / m / 1e3 / peak, 3)}),
                   flush=True)
-            del reps, shadows, src, dst, sets, g
+            del sets, g
 
 
 if __name__ == "__main__":
