@@ -8,6 +8,9 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 sys.path.insert(0, str(Path(__file__).resolve().parent))
+if "--lib" in sys.argv:  # an A/B variant (tools/variant_build.py) instead of the in-tree build
+    from paper_2507_09029_b200 import _native as _N  # noqa: E402
+    _N.load(sys.argv[sys.argv.index("--lib") + 1])
 import measure_all as M  # noqa: E402
 from paper_2507_09029_b200 import engine, masking, zoo  # noqa: E402
 
@@ -51,6 +54,13 @@ def aggregate_c3():
     us, _ = M.timed(lambda: engine.aggregate(reps, a))
     plan = a.sync_plan()
     nbytes = plan.owned_elems * 4 + d * 4
+    st = torch.zeros(1, dtype=torch.int32, device=M.DEV)
+    out = torch.empty(d, device=M.DEV)
+    prep = engine.PreparedSync(reps, a, writeback=False, out=out, check_uncovered=True, status=st)
+    us_k, _ = M.timed(prep.launch)
+    print(json.dumps({"cfg": "C3 kernel with the leak check", "lib": sys.argv[sys.argv.index("--lib") + 1]
+                      if "--lib" in sys.argv else "in-tree", "us": round(us_k, 1),
+                      "frac": round(nbytes / us_k / 1e3 / M.PEAK, 3)}), flush=True)
     print(json.dumps({"cfg": "C3 engine.aggregate", "direct": plan.direct, "stream_mean": plan.stream_mean,
                       "us": round(us, 1), "frac": round(nbytes / us / 1e3 / M.PEAK, 3)}), flush=True)
 
