@@ -193,7 +193,10 @@ int sdp_plan_tiles(const void* owner_mask, int mask_bytes, int64_t total,
                                         CTAs, replica loads only for the workers a
                                         warp's lanes own, the next vector's masks
                                         prefetched (owned-line traffic, one round
-                                        trip per vector) */
+                                        trip per vector); a launch with no
+                                        WRITEBACK / NESTEROV / ADAM runs the
+                                        mean-only instantiation (whole-vector
+                                        stores of the means, no epilogue) */
 
 /* status word bits written (atomicOr) by the kernel */
 #define SDP_STATUS_UNCOVERED_LEAK 0x1
