@@ -338,3 +338,35 @@ def test_channels_last_group_norm_matches_torch(cuda, relu, counts, affine):
     assert gg.dtype == affine and gb.dtype == affine
     assert torch.allclose(gg.float(), rg, rtol=1e-2, atol=1e-2 * rg.abs().max().item())
     assert torch.allclose(gb.float(), rb, rtol=1e-2, atol=1e-2 * rb.abs().max().item())
+
+
+def test_slice_batch_accumulate_stays_in_bounds(cuda):
+    """Guard bands around every worker's full vector: the batched
+    accumulate / zero-fill scatters and the gather write only inside their
+    own [0, d) / [0, compact) ranges."""
+    from paper_2507_09029_b200 import masking, models, zoo
+    topo = zoo.mini_resnet_topology(26, 8, 10, 2, 3, (8, 8))
+    a = masking.build_assignment(topo, "neuron", 8, 3, seed=21)
+    d = topo.total
+    subs = [models.SubnetLayout(a, w) for w in range(8)]
+    guard = 4096
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(5)
+    theta = torch.randn(d, generator=gen, device=cuda)
+    cbig = [torch.full((max(1, s.compact_total) + guard,), 3.0, device=cuda) for s in subs]
+    comps = [c[:max(1, s.compact_total)] for c, s in zip(cbig, subs)]
+    models.SliceBatch([s.host_gather for s in subs], cuda).gather([theta] * 8, comps)
+    fbig = [torch.full((d + guard,), 5.0, device=cuda) for _ in subs]
+    fulls = [f[:d] for f in fbig]
+    sb = models.SliceBatch([s.host_scatter for s in subs], cuda)
+    sb.scatter(comps, fulls)
+    sb.scatter(comps, fulls, accumulate=True)
+    torch.cuda.synchronize()
+    for c, s in zip(cbig, subs):
+        assert torch.all(c[max(1, s.compact_total):] == 3.0)
+    for f, s in zip(fbig, subs):
+        assert torch.all(f[d:] == 5.0)
+    # zero fill then accumulate == 2 * theta on the worker's mask, 0 elsewhere
+    pm = a.param_masks
+    for w, f in enumerate(fulls):
+        assert torch.equal(f, torch.where(pm[w], theta + theta, torch.zeros_like(theta)))

@@ -594,3 +594,33 @@ def test_stream_kernel_mean_only_equals_tiled(cuda, strategy, dtype):
             assert a.sync_plan().stream_mean
             g = engine.aggregate(base, a).gbar
             assert torch.equal(g, res[False][0])
+
+
+@pytest.mark.parametrize("d_extra", [0, 1, 3])
+def test_stream_mean_writes_stay_in_bounds(cuda, d_extra):
+    """Guard bands (compute-sanitizer is not available on the GPU pool): the
+    mean-only streaming kernel writes `out` / `out_bf16` inside [0, d) only,
+    on vectors with a ragged tail, and never touches the replicas."""
+    engine, masking = _pkg()
+    from paper_2507_09029_b200 import zoo
+    topo = zoo.residual_mlp_topology(width=64 + d_extra, blocks=8, classes=3, in_dim=5)
+    a = masking.build_assignment(topo, "neuron", 8, 4, seed=13)
+    d = topo.total
+    pm = a.param_masks
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(17)
+    reps = [torch.randn(d, generator=gen, device=cuda) * pm[w] for w in range(8)]
+    keep = [r.clone() for r in reps]
+    guard = 1024
+    big = torch.full((d + guard,), 7.0, device=cuda)
+    bigb = torch.full((d + guard,), 7.0, device=cuda).to(torch.bfloat16)
+    out, outb = big[:d], bigb[:d]
+    plan = engine.SyncPlan(a, direct=True, stream=True)
+    engine.PreparedSync(reps, a, writeback=False, out=out, out_bf16=outb, plan=plan).launch()
+    torch.cuda.synchronize()
+    assert torch.all(big[d:] == 7.0) and torch.all(bigb[d:] == 7.0)
+    for r, k in zip(reps, keep):
+        assert torch.equal(r, k)
+    want = torch.empty(d, device=cuda)
+    engine.PreparedSync(reps, a, writeback=False, out=want, plan=engine.SyncPlan(a, direct=False, stream=False)).launch()
+    assert torch.equal(out, want)
