@@ -37,6 +37,14 @@ def main():
         M.sync_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4)
     if "c4nagg" in cases:
         M.sync_case(gpt2, f"[{tag}] C4 gpt2 width-wise", "neuron", 8, 4, writeback=False, shadows=False)
+    # block plans, mean-only: tiled (routed default) vs the streaming kernel
+    if "blkagg" in cases:
+        M.sync_case(r18, f"[{tag}] C2 resnet18", "block", 8, 4, writeback=False, shadows=False)
+        M.sync_case(r18, f"[{tag}] C2 resnet18 stream", "block", 8, 4, writeback=False, shadows=False,
+                    direct=True, stream=True)
+        M.sync_case(gpt2, f"[{tag}] C4 gpt2", "block", 8, 4, writeback=False, shadows=False)
+        M.sync_case(gpt2, f"[{tag}] C4 gpt2 stream", "block", 8, 4, writeback=False, shadows=False,
+                    direct=True, stream=True)
     # the slice kernels (per worker and all workers per launch)
     if "s3" in cases:
         M.slices_case(r18, f"[{tag}] C3 resnet18", "neuron", 8, 4)
